@@ -1,0 +1,212 @@
+/*
+ * cubics.h - C ABI of the B200-native CUBICS search engine (libcubics.so).
+ *
+ * This is the drop-in boundary for the reference solver's hot path: depth-first labeling,
+ * propagation to a fixpoint and backtracking. Nothing here uses C++ or torch types: plain
+ * integers, pointers and sizes, so any FFI (ctypes, cgo, JNI, N-API) can bind it.
+ * The C++ adapter in adapter/fd_b200.cpp implements the reference's own C++ API
+ * (proj/include/fd/search.hpp, propagation.hpp) on top of these entry points; see
+ * INTEGRATION.md for how a maintainer links it.
+ *
+ * Reference interface each entry point replaces (paths relative to /root/reference/proj):
+ *   cubics_solve_satisfy       fd::solve_satisfy        include/fd/search.hpp:62, src/search.cpp:174-177
+ *                              fd::enumerate_solutions  include/fd/search.hpp:65-66, src/search.cpp:179-189
+ *   cubics_solve_optimize      fd::solve_optimize       include/fd/search.hpp:77, src/search.cpp:191-201
+ *   cubics_propagate           fd::propagate_fixpoint   include/fd/propagation.hpp:114-118, src/propagation.cpp:516-532
+ *                              fd::propagate_round      include/fd/propagation.hpp:102-104 (max_rounds = 1)
+ *   cubics_removals            fd::run_batch / fd::propagate_one / fd::prop_*
+ *                                                       include/fd/propagation.hpp:78-89
+ *   cubics_model_parse         fd::parse_model          include/fd/parser.hpp:38 (host-side loader)
+ *   cubics_model_validate      fd::model_validate       include/fd/model.hpp:93
+ *   cubics_solve_shard         (new) one rank's share of a multi-GPU search; SURVEY.md 8(e)
+ *
+ * Threading: every call is synchronous and blocks until the device finishes. Calls on
+ * different models may run from different host threads. Error details for the last failing
+ * call on the calling thread are in cubics_last_error().
+ */
+#ifndef CUBICS_H
+#define CUBICS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CUBICS_ABI_VERSION 1
+
+/* ---- status codes (no exception ever crosses the ABI) ---------------------------------- */
+enum cubics_status {
+    CUBICS_OK = 0,
+    CUBICS_E_INVALID = 1,      /* bad argument or malformed model description                 */
+    CUBICS_E_PARSE = 2,        /* model text rejected; details in cubics_parse_error            */
+    CUBICS_E_OVERFLOW = 3,     /* fd::ArithmeticOverflowError (src/propagation.cpp:198-210)     */
+    CUBICS_E_NO_OBJECTIVE = 4, /* std::logic_error: optimize without a goal (search.cpp:192)    */
+    CUBICS_E_CUDA = 5,         /* CUDA runtime failure or no usable sm_100 device               */
+    CUBICS_E_CAPACITY = 6,     /* device decision stack / solution buffer capacity exceeded     */
+    CUBICS_E_UNSUPPORTED = 7   /* instance outside the device engine's limits   */
+};
+
+/* ---- model vocabulary, numerically identical to the reference enums --------------------- */
+enum cubics_kind { CUBICS_RELBIN = 0, CUBICS_LINEAR = 1, CUBICS_ALLDIFF = 2 }; /* fd::ConstraintKind */
+enum cubics_relop { CUBICS_LT = 0, CUBICS_LE, CUBICS_GT, CUBICS_GE, CUBICS_EQ, CUBICS_NE }; /* fd::RelOp */
+enum cubics_linop { CUBICS_LIN_LE = 0, CUBICS_LIN_EQ = 1 };                    /* fd::LinOp */
+enum cubics_goal { CUBICS_SATISFY = 0, CUBICS_MINIMIZE = 1, CUBICS_MAXIMIZE = 2 }; /* fd::Goal */
+enum cubics_var_heuristic { CUBICS_INPUT_ORDER = 0, CUBICS_FIRST_FAIL = 1 };   /* fd::VarHeuristic */
+enum cubics_alldiff { CUBICS_FORWARD_CHECKING = 0, CUBICS_ARC_CONSISTENT = 1 }; /* fd::AlldiffLevel */
+
+#define CUBICS_MAX_WIDTH 1024 /* fd::Domain::kMaxWidth (include/fd/domain.hpp:27) */
+
+/*
+ * Flat description of an fd::Model (include/fd/model.hpp:67-74).
+ * Domains: var v covers [var_offset[v], var_offset[v] + var_width[v]); its bitset is
+ *   ceil(width/64) little-endian u64 words (bit i = value offset+i, fd::Domain::words()),
+ *   packed back to back in var order. var_words == NULL means every domain is full.
+ * Constraints: constraint c owns terms [con_start[c], con_start[c+1]).
+ *   RELBIN : terms = {lhs} (x op literal) or {lhs, rhs_var} (x op y + k); con_op = relop;
+ *            con_value = rhs_value (the literal, or k).               (model.hpp:26-32)
+ *   LINEAR : terms = (term_coeff, term_var) pairs; con_op = linop; con_value = bound. (:42-46)
+ *   ALLDIFF: terms = member vars; con_op and con_value ignored.        (:48-50)
+ * term_coeff may be NULL when there is no LINEAR constraint.
+ */
+typedef struct cubics_model_desc {
+    int32_t n_vars;
+    const int64_t* var_offset;
+    const int32_t* var_width;
+    const uint64_t* var_words;
+    int32_t n_cons;
+    const int32_t* con_kind;
+    const int32_t* con_op;
+    const int64_t* con_value;
+    const int32_t* con_start; /* n_cons + 1 entries */
+    const int32_t* term_var;
+    const int64_t* term_coeff;
+    int32_t goal;     /* enum cubics_goal */
+    int32_t goal_var; /* objective variable when goal != SATISFY */
+} cubics_model_desc;
+
+typedef struct cubics_model cubics_model; /* opaque, host-side */
+
+typedef struct cubics_parse_error { /* fd::ParseError (include/fd/parser.hpp:13-30) */
+    int32_t kind; /* 0 Syntax, 1 UnknownVariable, 2 DuplicateVariable, 3 EmptyDomain,
+                     4 DomainTooWide, 5 MissingSolveItem */
+    int32_t line;
+    int32_t column;
+    char message[256];
+} cubics_parse_error;
+
+typedef struct cubics_diagnostic { /* fd::Diagnostic (include/fd/model.hpp:76-90) */
+    int32_t kind; /* same order as fd::Diagnostic::Kind */
+    int32_t constraint_index;
+} cubics_diagnostic;
+
+int cubics_model_create(const cubics_model_desc* desc, cubics_model** out);
+int cubics_model_parse(const char* text, size_t len, cubics_model** out, cubics_parse_error* err);
+void cubics_model_free(cubics_model* m);
+/* Pointers in *out stay valid for the model's lifetime. */
+int cubics_model_describe(const cubics_model* m, cubics_model_desc* out);
+const char* cubics_model_var_name(const cubics_model* m, int32_t var);
+/* Writes up to cap diagnostics; *count receives the total (0 = valid). */
+int cubics_model_validate(const cubics_model* m, cubics_diagnostic* out, int32_t cap, int32_t* count);
+
+/* ---- search ------------------------------------------------------------------------------ */
+enum cubics_engine {
+    CUBICS_ENGINE_AUTO = 0,     /* PARALLEL for complete enumerations, else PARITY              */
+    CUBICS_ENGINE_PARITY = 1,   /* one device search context, reference node order: every stat
+                                   identical to the CPU reference                              */
+    CUBICS_ENGINE_PARALLEL = 2  /* many search contexts per GPU with work sharing: solutions and
+                                   all stats exact for complete enumerations; optimum exact for
+                                   branch-and-bound (node counts then schedule-dependent)       */
+};
+
+typedef struct cubics_search_config { /* fd::SearchConfig (include/fd/search.hpp:19-27) + engine */
+    int32_t var_heuristic;   /* enum cubics_var_heuristic, default FIRST_FAIL */
+    int32_t value_heuristic; /* 0 = MinValue (the only one)                 */
+    uint64_t max_solutions;  /* UINT64_MAX = unbounded (reference default)   */
+    int32_t thread_count;    /* accepted for API parity; no effect on the device engine */
+    uint64_t seed;           /* accepted for API parity; the DFS never reads it          */
+    int32_t alldiff;         /* enum cubics_alldiff, default ARC_CONSISTENT  */
+    uint64_t node_limit;     /* 0 = unbounded                                */
+    /* engine extension */
+    int32_t engine;          /* enum cubics_engine                           */
+    int32_t device;          /* CUDA ordinal, -1 = current device            */
+    int32_t contexts;        /* PARALLEL: search contexts (0 = auto)         */
+    int32_t block_threads;   /* threads per search context (0 = auto)        */
+    int32_t count_only;      /* 1 = do not materialise solutions (callback not called) */
+} cubics_search_config;
+
+void cubics_search_config_init(cubics_search_config* cfg); /* reference defaults */
+
+typedef struct cubics_stats { /* fd::SearchStats (include/fd/state.hpp:18-23) */
+    uint64_t nodes;
+    uint64_t failures;
+    uint64_t rounds;
+    uint64_t solutions;
+} cubics_stats;
+
+typedef struct cubics_result {
+    cubics_stats stats;
+    int32_t complete;      /* SatisfyResult.complete / OptimizeResult.complete */
+    int32_t has_solution;  /* >= 1 solution (satisfy) or an incumbent (optimize) */
+    int64_t objective;     /* best objective when optimizing and has_solution */
+    int32_t engine;        /* engine actually used */
+    int32_t contexts;      /* search contexts actually launched */
+    double device_ms;      /* search kernel time (CUDA events) */
+    double total_ms;       /* wall time of the whole call: upload + search + download */
+    uint64_t h2d_bytes;    /* bytes copied host -> device by this call */
+    uint64_t d2h_bytes;    /* bytes copied device -> host by this call */
+    uint64_t kernel_launches; /* CUDA kernels this call launched */
+} cubics_result;
+
+/* Receives each solution (values indexed by var id, as fd::Solution::values) in the
+ * reference's DFS order, on the calling thread. Return 0 to stop the stream. */
+typedef int32_t (*cubics_solution_cb)(void* user, const int64_t* values, int32_t n_vars);
+
+int cubics_solve_satisfy(const cubics_model* m, const cubics_search_config* cfg,
+                         cubics_solution_cb cb, void* user, cubics_result* out);
+
+/* best_values (n_vars entries, may be NULL) receives the optimal / last incumbent. */
+int cubics_solve_optimize(const cubics_model* m, const cubics_search_config* cfg,
+                          int64_t* best_values, cubics_result* out);
+
+/* One rank's share of a multi-GPU search: the search tree is expanded
+ * deterministically to a frontier of open subtrees; this call searches every subtree t with
+ * t % shard_count == shard_index (nodes above the frontier are counted by shard 0 only) and
+ * returns partial stats that sum exactly across shards. Solutions reach cb with their
+ * 64-bit-word DFS rank key (key_words words, lexicographic = reference DFS order). */
+typedef int32_t (*cubics_keyed_solution_cb)(void* user, const uint32_t* key, int32_t key_words,
+                                            const int64_t* values, int32_t n_vars);
+int cubics_solve_shard(const cubics_model* m, const cubics_search_config* cfg,
+                       int32_t shard_index, int32_t shard_count,
+                       cubics_keyed_solution_cb cb, void* user, cubics_result* out);
+
+/* ---- propagation (kernel-level API) ------------------------------------------------------ */
+typedef struct cubics_fixpoint_result { /* fd::FixpointResult (propagation.hpp:106-110) */
+    int32_t failed;
+    int32_t failed_var; /* lowest empty var id when failed, else -1 */
+    int32_t rounds;
+    int32_t last_status; /* fd::RoundResult::Status of the last round: 0 Changed 1 Stable 2 Failed */
+} cubics_fixpoint_result;
+
+/* Bulk-synchronous rounds over `words` (desc packing, in/out) until Stable or Failed, or until
+ * max_rounds rounds ran (max_rounds <= 0: unbounded = fd::propagate_fixpoint; 1 = one
+ * fd::propagate_round). */
+int cubics_propagate(const cubics_model* m, uint64_t* words, int32_t alldiff, int32_t max_rounds,
+                     cubics_fixpoint_result* out);
+
+/* Union of the removals the constraints `cons[0..n_cons)` (all constraints when cons == NULL)
+ * compute against the snapshot `words`, without applying them: fd::run_batch / propagate_one.
+ * removed (desc packing) receives the removal masks restricted to present values. */
+int cubics_removals(const cubics_model* m, const uint64_t* words, int32_t alldiff,
+                    const int32_t* cons, int32_t n_cons, uint64_t* removed);
+
+/* ---- misc -------------------------------------------------------------------------------- */
+const char* cubics_last_error(void);
+const char* cubics_build_info(void);
+int cubics_device_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CUBICS_H */

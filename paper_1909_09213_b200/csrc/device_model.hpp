@@ -1,0 +1,120 @@
+// Device-side model and search-state layout shared by the host orchestration (engine.cu) and
+// the kernels (kernels.cuh). Plain structs of device pointers; no torch types.
+//
+// HBM / shared-memory layout:
+//   domains  : n x W u32 words, var v at [v*W, v*W+W); bit i = value off[v] + i. W is a power of
+//              two >= every domain's and every alldifferent universe's word count (u32 words).
+//   RelBin   : one 16-byte record per constraint {x, (y+1)<<3 | op, k}      (model.hpp:26-32)
+//   Linear   : CSR {start[], op[], bound[]} over terms {var[], coeff[]}     (model.hpp:42-46)
+//   AllDiff  : CSR over members {var[], shift[]}; shift = off[var] - universe_offset, so a
+//              member's domain shifted left by `shift` bits lands in the common value universe.
+#pragma once
+
+#include <cstdint>
+
+namespace cubics {
+
+struct RelBinRec {
+    int32_t x;
+    int32_t yop;  // ((y + 1) << 3) | op ; y = -1 for the literal form
+    int64_t k;    // literal, or the offset added to y
+};
+
+struct DevModel {
+    int32_t n;           // variables
+    int32_t W;           // u32 words per domain (power of two)
+    const int64_t* off;  // [n]
+    const uint32_t* init_dom; // [n*W]
+    int32_t nr;
+    const RelBinRec* rb;
+    int32_t nl;
+    const int32_t* lin_start; // [nl+1]
+    const int32_t* lin_op;    // [nl]
+    const int64_t* lin_bound; // [nl]
+    const int32_t* lin_var;
+    const int64_t* lin_coeff;
+    int32_t na;
+    const int32_t* ad_start;  // [na+1]
+    const int32_t* ad_var;
+    const int32_t* ad_shift;
+    int32_t total_members;
+    int32_t goal;
+    int32_t goal_var;
+};
+
+enum KernelMode : int32_t { MODE_PARITY = 0, MODE_PARALLEL = 1 };
+
+enum DeviceError : int32_t {
+    DERR_NONE = 0,
+    DERR_OVERFLOW = 1,
+    DERR_CAPACITY = 2,
+};
+
+// Global coordination state for the parallel engine (one per launch, in HBM).
+struct WorkState {
+    int32_t lock;         // queue spin-lock
+    int32_t q_count;      // tasks waiting in queue[]
+    int32_t n_idle;       // contexts waiting for work
+    int32_t outstanding;  // busy contexts + queued tasks; 0 => search finished
+    int32_t stop;         // 1 => every context unwinds (error / limit / solution cap)
+    int32_t error;        // DeviceError
+    int32_t limit_hit;
+    int32_t user_stop;
+    uint64_t sol_count;   // solutions recorded (parallel: atomic slot allocator)
+    int64_t bound;        // branch-and-bound incumbent objective (parallel)
+    int32_t has_bound;
+    int32_t inc_lock;
+    uint64_t stats[4];    // nodes, failures, rounds, solutions
+    uint64_t donations;
+    uint64_t steals;
+};
+
+struct SearchParams {
+    DevModel M;
+    int32_t mode;          // KernelMode
+    int32_t var_heuristic; // 0 input order, 1 first fail
+    int32_t alldiff;       // 0 FC, 1 GAC
+    int32_t exact_wipe;    // 1: GAC failure wipes the reference's (Kuhn-order) member
+    uint64_t max_solutions;
+    uint64_t node_limit;
+    int32_t n_ctx;
+    int32_t frame_cap;     // decision frames per context
+    int32_t KW;            // u32 words of the DFS path key (parallel); 0 in parity mode
+    int32_t record;        // 1: materialise solutions
+    int32_t dom_in_smem;
+    // per-context global scratch
+    uint32_t* frames;      // [n_ctx][frame_cap][NW]
+    int32_t* frame_meta;   // [n_ctx][frame_cap][4] : var, bit, depth, pad
+    uint32_t* gdom;        // [n_ctx][2*NW] when domains do not fit in shared memory
+    // work sharing
+    WorkState* ws;
+    int32_t* queue;        // [n_ctx]
+    int32_t* outbox_busy;  // [n_ctx]
+    uint32_t* outbox;      // [n_ctx][NW + KW + 4]
+    // solutions
+    uint64_t sol_cap;
+    uint16_t* sol_vals;    // [sol_cap][n] bit index of each var's value
+    uint32_t* sol_keys;    // [sol_cap][KW]
+    uint64_t* sol_stats;   // [sol_cap][3] nodes, failures, rounds at emission (parity)
+    // per-context DFS-first solution (parallel, count-only friendly)
+    uint32_t* ctx_first_key;  // [n_ctx][KW]
+    uint16_t* ctx_first_vals; // [n_ctx][n]
+    int32_t* ctx_has_first;   // [n_ctx]
+    // branch-and-bound incumbent (parallel)
+    uint16_t* inc_vals;       // [n]
+    int64_t init_bound;
+    int32_t has_init_bound;
+};
+
+struct PropParams {
+    DevModel M;
+    int32_t alldiff;
+    int32_t max_rounds;    // <= 0 unbounded
+    int32_t removals_only; // 1: run propagators once, output rm & dom, do not apply
+    const uint8_t* enabled; // per constraint kind-local enable flags [nr + nl + na] or null
+    uint32_t* dom;         // [NW] in/out
+    uint32_t* out;         // removals output (removals_only)
+    int32_t* result;       // failed, failed_var, rounds, last_status, error
+};
+
+} // namespace cubics

@@ -1,0 +1,806 @@
+// Host orchestration of the device search engine and the solve / propagate entry points of the
+// C ABI (include/cubics.h). The model is flattened once per call into the device layout of
+// device_model.hpp, uploaded with one host->device copy, searched by one persistent kernel
+// launch, and the results (stats, solutions) come back with a few device->host copies.
+//
+// There is no CPU fallback: without a usable sm_100 device every entry point returns
+// CUBICS_E_CUDA with the CUDA error text in cubics_last_error().
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "cubics.h"
+#include "device_model.hpp"
+#include "model.hpp"
+#include "kernels.hpp"
+#include "layout.hpp"
+
+using namespace cubics;
+
+namespace {
+
+constexpr int kMaxAllDiffMembers = 64;
+constexpr size_t kSmemBudget = 200 * 1024;
+
+struct CudaError {
+    std::string msg;
+};
+
+#define CU(call)                                                                               \
+    do {                                                                                       \
+        cudaError_t e_ = (call);                                                               \
+        if (e_ != cudaSuccess) throw CudaError{std::string(#call) + ": " + cudaGetErrorString(e_)}; \
+    } while (0)
+
+struct StatusError {
+    int code;
+    std::string msg;
+};
+
+double now_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// ------------------------------------------------------------------ device arena (grow-only, per device)
+struct Arena {
+    void* ptr = nullptr;
+    size_t cap = 0;
+};
+std::mutex g_arena_mu;
+Arena g_arena[64];
+Arena g_pinned[64];
+
+uint8_t* device_arena(int dev, size_t bytes) {
+    Arena& a = g_arena[dev];
+    if (a.cap < bytes) {
+        if (a.ptr) cudaFree(a.ptr);
+        a.ptr = nullptr;
+        size_t want = std::max(bytes, a.cap * 3 / 2);
+        CU(cudaMalloc(&a.ptr, want));
+        a.cap = want;
+    }
+    return static_cast<uint8_t*>(a.ptr);
+}
+
+uint8_t* pinned_arena(int dev, size_t bytes) {
+    Arena& a = g_pinned[dev];
+    if (a.cap < bytes) {
+        if (a.ptr) cudaFreeHost(a.ptr);
+        a.ptr = nullptr;
+        size_t want = std::max(bytes, a.cap * 3 / 2);
+        CU(cudaMallocHost(&a.ptr, want));
+        a.cap = want;
+    }
+    return static_cast<uint8_t*>(a.ptr);
+}
+
+// ------------------------------------------------------------------ flattening to the device layout
+struct Blob { // host staging of every device array, packed with 16-byte alignment
+    std::vector<uint8_t> bytes;
+    template <class T>
+    size_t add(const T* p, size_t n) {
+        size_t at = (bytes.size() + 15) & ~size_t(15);
+        bytes.resize(at + std::max<size_t>(n * sizeof(T), 16), 0);
+        if (n) std::memcpy(bytes.data() + at, p, n * sizeof(T));
+        return at;
+    }
+};
+
+struct Prepared {
+    int W = 1;
+    int n = 0;
+    size_t NWP = 4;
+    int nr = 0, nl = 0, na = 0, total_members = 0;
+    bool has_empty = false;
+    uint64_t depth_bound = 0; // sum(|D| - 1): max binary-tree depth
+    Blob blob;
+    size_t o_off, o_dom, o_rb, o_ls, o_lo, o_lb, o_lv, o_lc, o_as, o_av, o_ash;
+    std::vector<int> kind_index; // constraint index -> kind-local index (rb | nr+lin | nr+nl+ad)
+    std::vector<int64_t> offsets;
+    DevModel bind(const uint8_t* base) const {
+        DevModel M{};
+        M.n = n;
+        M.W = W;
+        M.off = reinterpret_cast<const int64_t*>(base + o_off);
+        M.init_dom = reinterpret_cast<const uint32_t*>(base + o_dom);
+        M.nr = nr;
+        M.rb = reinterpret_cast<const RelBinRec*>(base + o_rb);
+        M.nl = nl;
+        M.lin_start = reinterpret_cast<const int32_t*>(base + o_ls);
+        M.lin_op = reinterpret_cast<const int32_t*>(base + o_lo);
+        M.lin_bound = reinterpret_cast<const int64_t*>(base + o_lb);
+        M.lin_var = reinterpret_cast<const int32_t*>(base + o_lv);
+        M.lin_coeff = reinterpret_cast<const int64_t*>(base + o_lc);
+        M.na = na;
+        M.ad_start = reinterpret_cast<const int32_t*>(base + o_as);
+        M.ad_var = reinterpret_cast<const int32_t*>(base + o_av);
+        M.ad_shift = reinterpret_cast<const int32_t*>(base + o_ash);
+        M.total_members = total_members;
+        return M;
+    }
+};
+
+void words_to_u32(const HostModel& m, int v, const uint64_t* src64, uint32_t* dst, int W) {
+    const int nw64 = m.word_start[v + 1] - m.word_start[v];
+    for (int w = 0; w < W; ++w) {
+        uint64_t x = (w / 2 < nw64) ? src64[m.word_start[v] + w / 2] : 0;
+        dst[(size_t)v * W + w] = static_cast<uint32_t>(w % 2 ? x >> 32 : x);
+    }
+}
+
+// check_ranges: the device engine limits
+void prepare(const HostModel& m, const uint64_t* words, Prepared& P) {
+    const int n = m.n_vars();
+    P.n = n;
+    int need = 1;
+    for (int v = 0; v < n; ++v) need = std::max(need, (m.width[v] + 31) / 32);
+    // constraint tables
+    std::vector<RelBinRec> rb;
+    std::vector<int32_t> ls{0}, lo, lv, as{0}, av, ash;
+    std::vector<int64_t> lb, lc;
+    P.kind_index.assign(m.n_cons(), 0);
+    std::vector<int> ad_cons;
+    for (int c = 0; c < m.n_cons(); ++c) {
+        const int b = m.con_start[c], e = m.con_start[c + 1];
+        switch (m.con_kind[c]) {
+        case CUBICS_RELBIN: {
+            RelBinRec r{};
+            r.x = m.term_var[b];
+            const int y = e - b == 2 ? m.term_var[b + 1] : -1;
+            r.yop = ((y + 1) << 3) | m.con_op[c];
+            r.k = m.con_value[c];
+            P.kind_index[c] = static_cast<int>(rb.size());
+            rb.push_back(r);
+            break;
+        }
+        case CUBICS_LINEAR: {
+            if (m.con_op[c] == CUBICS_LIN_EQ) {
+                bool bad = m.con_value[c] == std::numeric_limits<int64_t>::min();
+                for (int t = b; t < e; ++t) bad = bad || m.term_coeff[t] == std::numeric_limits<int64_t>::min();
+                if (bad) throw StatusError{CUBICS_E_OVERFLOW, "overflow in linear propagation"};
+            }
+            P.kind_index[c] = static_cast<int>(lo.size());
+            lo.push_back(m.con_op[c]);
+            lb.push_back(m.con_value[c]);
+            for (int t = b; t < e; ++t) {
+                lv.push_back(m.term_var[t]);
+                lc.push_back(m.term_coeff[t]);
+            }
+            ls.push_back(static_cast<int32_t>(lv.size()));
+            break;
+        }
+        default:
+            ad_cons.push_back(c);
+            break;
+        }
+    }
+    for (int c : ad_cons) {
+        const int b = m.con_start[c], e = m.con_start[c + 1];
+        if (e - b > kMaxAllDiffMembers)
+            throw StatusError{CUBICS_E_UNSUPPORTED, "alldifferent with more than 64 members"};
+        __int128 uoff = 0, uend = 0;
+        for (int t = b; t < e; ++t) {
+            const int v = m.term_var[t];
+            __int128 o = m.offset[v], en = (__int128)m.offset[v] + m.width[v];
+            if (t == b || o < uoff) uoff = o;
+            if (t == b || en > uend) uend = en;
+        }
+        const __int128 span = uend - uoff;
+        if (span > 32 * 32) throw StatusError{CUBICS_E_UNSUPPORTED, "alldifferent value universe wider than 1024"};
+        need = std::max(need, static_cast<int>((span + 31) / 32));
+        P.kind_index[c] = static_cast<int>(as.size()) - 1;
+        for (int t = b; t < e; ++t) {
+            av.push_back(m.term_var[t]);
+            ash.push_back(static_cast<int32_t>(m.offset[m.term_var[t]] - uoff));
+        }
+        as.push_back(static_cast<int32_t>(av.size()));
+    }
+    int W = 1;
+    while (W < need) W *= 2;
+    if (W > 32) throw StatusError{CUBICS_E_UNSUPPORTED, "domain wider than 1024 values"};
+    P.W = W;
+    P.NWP = dev::round4((size_t)std::max(n, 1) * W);
+    P.nr = static_cast<int>(rb.size());
+    P.nl = static_cast<int>(lo.size());
+    P.na = static_cast<int>(as.size()) - 1;
+    P.total_members = static_cast<int>(av.size());
+    std::vector<uint32_t> dom(P.NWP, 0);
+    P.depth_bound = 0;
+    P.has_empty = false;
+    for (int v = 0; v < n; ++v) {
+        words_to_u32(m, v, words, dom.data(), W);
+        int sz = 0;
+        for (int w = 0; w < W; ++w) sz += __builtin_popcount(dom[(size_t)v * W + w]);
+        if (sz == 0) P.has_empty = true;
+        P.depth_bound += sz > 0 ? (uint64_t)(sz - 1) : 0;
+    }
+    P.offsets = m.offset;
+    P.o_off = P.blob.add(m.offset.data(), m.offset.size());
+    P.o_dom = P.blob.add(dom.data(), dom.size());
+    P.o_rb = P.blob.add(rb.data(), rb.size());
+    P.o_ls = P.blob.add(ls.data(), ls.size());
+    P.o_lo = P.blob.add(lo.data(), lo.size());
+    P.o_lb = P.blob.add(lb.data(), lb.size());
+    P.o_lv = P.blob.add(lv.data(), lv.size());
+    P.o_lc = P.blob.add(lc.data(), lc.size());
+    P.o_as = P.blob.add(as.data(), as.size());
+    P.o_av = P.blob.add(av.data(), av.size());
+    P.o_ash = P.blob.add(ash.data(), ash.size());
+}
+
+int current_device(int want) {
+    int count = 0;
+    CU(cudaGetDeviceCount(&count));
+    if (count == 0) throw CudaError{"no CUDA device"};
+    int dev = want;
+    if (dev < 0) CU(cudaGetDevice(&dev));
+    if (dev >= count) throw CudaError{"device ordinal out of range"};
+    CU(cudaSetDevice(dev));
+    cudaDeviceProp prop;
+    CU(cudaGetDeviceProperties(&prop, dev));
+    if (prop.major < 10) throw CudaError{"device is not sm_100 class (Blackwell)"};
+    return dev;
+}
+
+// ------------------------------------------------------------------ kernel dispatch over W
+#define CUBICS_DISPATCH_W(W, CALL)                                                                  \
+    switch (W) {                                                                                   \
+    case 1: CU(CALL(1)); break;                                                                    \
+    case 2: CU(CALL(2)); break;                                                                    \
+    case 4: CU(CALL(4)); break;                                                                    \
+    case 8: CU(CALL(8)); break;                                                                    \
+    case 16: CU(CALL(16)); break;                                                                  \
+    case 32: CU(CALL(32)); break;                                                                  \
+    default: throw StatusError{CUBICS_E_UNSUPPORTED, "bad word count"};                            \
+    }
+
+int parity_block(const Prepared& P) {
+    const int work = P.nr + P.nl;
+    int prop_warps = std::min(16, std::max(1, (work + 31) / 32));
+    int ad_warps = std::min(P.na, 8);
+    int apply_warps = std::min(16, std::max(1, (P.n + 63) / 64));
+    int warps = std::max(prop_warps + ad_warps, apply_warps);
+    return std::min(1024, 32 * warps);
+}
+
+struct Records { // solutions copied back from the device
+    uint64_t count = 0;
+    std::vector<uint16_t> vals;
+    std::vector<uint32_t> keys;
+    std::vector<uint64_t> stats;
+};
+
+struct RunOut {
+    WorkState ws{};
+    Records rec;
+    int engine = CUBICS_ENGINE_PARITY;
+    int contexts = 1;
+    int KW = 0;
+    double device_ms = 0;
+    uint64_t h2d = 0, d2h = 0, launches = 0;
+    std::vector<uint16_t> inc_vals;
+    std::vector<uint32_t> first_key;  // parallel: DFS-first solution key/values
+    std::vector<uint16_t> first_vals;
+    bool has_first = false;
+};
+
+// One device search: upload, launch, download.
+void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine, bool record, uint64_t sol_cap,
+                RunOut& out) {
+    const int dev = current_device(cfg.device);
+    Prepared P;
+    prepare(hm, hm.words.data(), P);
+    const int n = P.n;
+    const bool parallel = engine == CUBICS_ENGINE_PARALLEL;
+    const int KW = parallel ? static_cast<int>((P.depth_bound + 1 + 31) / 32) : 0;
+    if (parallel && KW > 4096) throw StatusError{CUBICS_E_UNSUPPORTED, "search tree too deep for ordered parallel keys"};
+    out.KW = KW;
+    // launch geometry
+    int block = cfg.block_threads > 0 ? ((cfg.block_threads + 31) / 32) * 32 : 0;
+    if (!block) block = parallel ? (P.na > 0 && P.nr + P.nl > 0 ? 64 : 32) : parity_block(P);
+    block = std::min(std::max(block, 32), 1024);
+    const int nw = block / 32;
+    bool in_smem = true;
+    dev::SmemLayout L = dev::smem_layout(P.W, n, P.total_members, nw, KW, true);
+    if (L.total > kSmemBudget) {
+        in_smem = false;
+        L = dev::smem_layout(P.W, n, P.total_members, nw, KW, false);
+        if (L.total > kSmemBudget) throw StatusError{CUBICS_E_UNSUPPORTED, "search context does not fit in shared memory"};
+    }
+    int n_ctx = 1;
+    if (parallel) {
+        int per_sm = 0;
+#define OCC(w) occupancy_search<w>(block, L.total, &per_sm)
+        CUBICS_DISPATCH_W(P.W, OCC)
+#undef OCC
+        int sms = 0;
+        CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        const int cap = std::max(1, per_sm) * sms;
+        n_ctx = cfg.contexts > 0 ? std::min(cfg.contexts, cap) : cap;
+    }
+    out.contexts = n_ctx;
+    out.engine = engine;
+    int frame_cap = n + 1;
+    if (cfg.node_limit && cfg.node_limit + 1 < (uint64_t)frame_cap) frame_cap = static_cast<int>(cfg.node_limit + 1);
+    frame_cap = std::max(frame_cap, 1);
+    const size_t NWP = P.NWP;
+    const size_t OS = NWP + dev::round4((size_t)KW + 1);
+    if (!record) sol_cap = 0;
+
+    // one device allocation: [model blob | ws | queue | busy | has_first | frames | meta | gdom | outbox |
+    //                          sol_vals | sol_keys | sol_stats | first keys | first vals | inc_vals]
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t at = (off + 255) & ~size_t(255);
+        off = at + std::max<size_t>(bytes, 16);
+        return at;
+    };
+    const size_t a_blob = take(P.blob.bytes.size());
+    const size_t a_ws = take(sizeof(WorkState));
+    const size_t a_queue = take(sizeof(int32_t) * n_ctx);
+    const size_t a_busy = take(sizeof(int32_t) * n_ctx);
+    const size_t a_hf = take(sizeof(int32_t) * n_ctx);
+    const size_t zero_end = off;
+    const size_t a_frames = take(sizeof(uint32_t) * NWP * frame_cap * n_ctx);
+    const size_t a_meta = take(sizeof(int32_t) * 4 * frame_cap * n_ctx);
+    const size_t a_gdom = take(in_smem ? 0 : sizeof(uint32_t) * 2 * NWP * n_ctx);
+    const size_t a_outbox = take(parallel ? sizeof(uint32_t) * OS * n_ctx : 0);
+    const size_t a_svals = take(sizeof(uint16_t) * n * sol_cap);
+    const size_t a_skeys = take(sizeof(uint32_t) * KW * sol_cap);
+    const size_t a_sstats = take(parallel ? 0 : sizeof(uint64_t) * 3 * sol_cap);
+    const size_t a_fkey = take(sizeof(uint32_t) * KW * n_ctx);
+    const size_t a_fval = take(parallel ? sizeof(uint16_t) * n * n_ctx : 0);
+    const size_t a_inc = take(sizeof(uint16_t) * std::max(n, 1));
+    uint8_t* base = device_arena(dev, off);
+
+    cudaStream_t st = nullptr;
+    CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    cudaEvent_t e0, e1;
+    CU(cudaEventCreate(&e0));
+    CU(cudaEventCreate(&e1));
+    try {
+        // staging: blob + initial WorkState in pinned memory, one H2D copy
+        WorkState w0{};
+        w0.outstanding = n_ctx;
+        const size_t stage_bytes = a_ws + sizeof(WorkState);
+        uint8_t* stage = pinned_arena(dev, stage_bytes);
+        std::memset(stage, 0, stage_bytes);
+        std::memcpy(stage + a_blob, P.blob.bytes.data(), P.blob.bytes.size());
+        std::memcpy(stage + a_ws, &w0, sizeof w0);
+        CU(cudaMemcpyAsync(base, stage, stage_bytes, cudaMemcpyHostToDevice, st));
+        out.h2d += stage_bytes;
+        CU(cudaMemsetAsync(base + a_queue, 0, zero_end - a_queue, st));
+
+        SearchParams S{};
+        S.M = P.bind(base + a_blob);
+        S.M.goal = hm.goal;
+        S.M.goal_var = hm.goal_var;
+        S.mode = parallel ? MODE_PARALLEL : MODE_PARITY;
+        S.var_heuristic = cfg.var_heuristic == CUBICS_FIRST_FAIL ? 1 : 0;
+        S.alldiff = cfg.alldiff == CUBICS_FORWARD_CHECKING ? 0 : 1;
+        S.exact_wipe = P.has_empty ? 1 : 0;
+        S.max_solutions = cfg.max_solutions;
+        S.node_limit = cfg.node_limit;
+        S.n_ctx = n_ctx;
+        S.frame_cap = frame_cap;
+        S.KW = KW;
+        S.record = record ? 1 : 0;
+        S.dom_in_smem = in_smem ? 1 : 0;
+        S.frames = reinterpret_cast<uint32_t*>(base + a_frames);
+        S.frame_meta = reinterpret_cast<int32_t*>(base + a_meta);
+        S.gdom = reinterpret_cast<uint32_t*>(base + a_gdom);
+        S.ws = reinterpret_cast<WorkState*>(base + a_ws);
+        S.queue = reinterpret_cast<int32_t*>(base + a_queue);
+        S.outbox_busy = reinterpret_cast<int32_t*>(base + a_busy);
+        S.outbox = reinterpret_cast<uint32_t*>(base + a_outbox);
+        S.sol_cap = sol_cap;
+        S.sol_vals = reinterpret_cast<uint16_t*>(base + a_svals);
+        S.sol_keys = reinterpret_cast<uint32_t*>(base + a_skeys);
+        S.sol_stats = reinterpret_cast<uint64_t*>(base + a_sstats);
+        S.ctx_first_key = reinterpret_cast<uint32_t*>(base + a_fkey);
+        S.ctx_first_vals = reinterpret_cast<uint16_t*>(base + a_fval);
+        S.ctx_has_first = reinterpret_cast<int32_t*>(base + a_hf);
+        S.inc_vals = reinterpret_cast<uint16_t*>(base + a_inc);
+
+        CU(cudaEventRecord(e0, st));
+#define LS(w) launch_search<w>(S, n_ctx, block, L.total, st)
+        CUBICS_DISPATCH_W(P.W, LS)
+#undef LS
+        CU(cudaEventRecord(e1, st));
+        out.launches += 1;
+        CU(cudaMemcpyAsync(&out.ws, base + a_ws, sizeof(WorkState), cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        out.d2h += sizeof(WorkState);
+        float ms = 0;
+        CU(cudaEventElapsedTime(&ms, e0, e1));
+        out.device_ms = ms;
+        const uint64_t got = std::min<uint64_t>(out.ws.sol_count ? out.ws.sol_count : 0, sol_cap);
+        uint64_t recorded = parallel ? got : std::min<uint64_t>(out.ws.stats[3], sol_cap);
+        out.rec.count = recorded;
+        if (recorded) {
+            out.rec.vals.resize(recorded * n);
+            CU(cudaMemcpyAsync(out.rec.vals.data(), base + a_svals, sizeof(uint16_t) * n * recorded,
+                               cudaMemcpyDeviceToHost, st));
+            out.d2h += sizeof(uint16_t) * n * recorded;
+            if (KW) {
+                out.rec.keys.resize(recorded * KW);
+                CU(cudaMemcpyAsync(out.rec.keys.data(), base + a_skeys, sizeof(uint32_t) * KW * recorded,
+                                   cudaMemcpyDeviceToHost, st));
+                out.d2h += sizeof(uint32_t) * KW * recorded;
+            }
+            if (!parallel) {
+                out.rec.stats.resize(recorded * 3);
+                CU(cudaMemcpyAsync(out.rec.stats.data(), base + a_sstats, sizeof(uint64_t) * 3 * recorded,
+                                   cudaMemcpyDeviceToHost, st));
+                out.d2h += sizeof(uint64_t) * 3 * recorded;
+            }
+        }
+        if (parallel && KW && n) { // DFS-first solution over the contexts' firsts
+            std::vector<int32_t> hf(n_ctx);
+            std::vector<uint32_t> fk((size_t)KW * n_ctx);
+            CU(cudaMemcpyAsync(hf.data(), base + a_hf, sizeof(int32_t) * n_ctx, cudaMemcpyDeviceToHost, st));
+            CU(cudaMemcpyAsync(fk.data(), base + a_fkey, sizeof(uint32_t) * KW * n_ctx, cudaMemcpyDeviceToHost, st));
+            CU(cudaStreamSynchronize(st));
+            out.d2h += sizeof(int32_t) * n_ctx + sizeof(uint32_t) * KW * n_ctx;
+            int best = -1;
+            for (int c = 0; c < n_ctx; ++c) {
+                if (!hf[c]) continue;
+                if (best < 0 || std::lexicographical_compare(fk.begin() + (size_t)c * KW, fk.begin() + (size_t)(c + 1) * KW,
+                                                             fk.begin() + (size_t)best * KW,
+                                                             fk.begin() + (size_t)(best + 1) * KW))
+                    best = c;
+            }
+            if (best >= 0) {
+                out.has_first = true;
+                out.first_key.assign(fk.begin() + (size_t)best * KW, fk.begin() + (size_t)(best + 1) * KW);
+                out.first_vals.resize(n);
+                CU(cudaMemcpyAsync(out.first_vals.data(), base + a_fval + sizeof(uint16_t) * n * best,
+                                   sizeof(uint16_t) * n, cudaMemcpyDeviceToHost, st));
+                out.d2h += sizeof(uint16_t) * n;
+            }
+        }
+        if (parallel && hm.goal != CUBICS_SATISFY && n) {
+            out.inc_vals.resize(n);
+            CU(cudaMemcpyAsync(out.inc_vals.data(), base + a_inc, sizeof(uint16_t) * n, cudaMemcpyDeviceToHost, st));
+            out.d2h += sizeof(uint16_t) * n;
+        }
+        CU(cudaStreamSynchronize(st));
+    } catch (...) {
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaStreamDestroy(st);
+        throw;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(st);
+    if (out.ws.error == DERR_OVERFLOW) throw StatusError{CUBICS_E_OVERFLOW, "overflow in linear propagation"};
+    if (out.ws.error == DERR_CAPACITY) throw StatusError{CUBICS_E_CAPACITY, "device decision stack capacity exceeded"};
+}
+
+void fill_result(const RunOut& r, cubics_result* out) {
+    out->stats.nodes = r.ws.stats[0];
+    out->stats.failures = r.ws.stats[1];
+    out->stats.rounds = r.ws.stats[2];
+    out->stats.solutions = r.ws.stats[3];
+    out->engine = r.engine;
+    out->contexts = r.contexts;
+    out->device_ms = r.device_ms;
+    out->h2d_bytes = r.h2d;
+    out->d2h_bytes = r.d2h;
+    out->kernel_launches = r.launches;
+}
+
+int pick_engine(const cubics_search_config& cfg, bool optimize_goal) {
+    if (cfg.engine == CUBICS_ENGINE_PARITY || cfg.engine == CUBICS_ENGINE_PARALLEL) {
+        if (cfg.engine == CUBICS_ENGINE_PARALLEL &&
+            (cfg.node_limit != 0 || (!optimize_goal && cfg.max_solutions != std::numeric_limits<uint64_t>::max())))
+            throw StatusError{CUBICS_E_UNSUPPORTED,
+                              "parallel engine needs a complete search (no node_limit, unbounded max_solutions)"};
+        return cfg.engine;
+    }
+    if (!optimize_goal && cfg.node_limit == 0 && cfg.max_solutions == std::numeric_limits<uint64_t>::max())
+        return CUBICS_ENGINE_PARALLEL;
+    return CUBICS_ENGINE_PARITY;
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        return f();
+    } catch (const StatusError& e) {
+        set_error(e.msg);
+        return e.code;
+    } catch (const CudaError& e) {
+        set_error(e.msg);
+        return CUBICS_E_CUDA;
+    } catch (const std::bad_alloc&) {
+        set_error("host allocation failed");
+        return CUBICS_E_CAPACITY;
+    }
+}
+
+uint64_t default_sol_cap(const HostModel& m, const cubics_search_config& cfg) {
+    const uint64_t per = (uint64_t)m.n_vars() * 2 + 64;
+    uint64_t cap = (uint64_t)1 << 22;
+    cap = std::min<uint64_t>(cap, ((uint64_t)2 << 30) / per);
+    if (cfg.max_solutions != std::numeric_limits<uint64_t>::max()) cap = std::min<uint64_t>(cap, cfg.max_solutions);
+    return std::max<uint64_t>(cap, 1);
+}
+
+} // namespace
+
+// ============================================================================ C ABI
+extern "C" void cubics_search_config_init(cubics_search_config* c) {
+    if (!c) return;
+    std::memset(c, 0, sizeof *c);
+    c->var_heuristic = CUBICS_FIRST_FAIL;
+    c->value_heuristic = 0;
+    c->max_solutions = std::numeric_limits<uint64_t>::max();
+    c->thread_count = 1;
+    c->seed = 0;
+    c->alldiff = CUBICS_ARC_CONSISTENT;
+    c->node_limit = 0;
+    c->engine = CUBICS_ENGINE_AUTO;
+    c->device = -1;
+    c->contexts = 0;
+    c->block_threads = 0;
+    c->count_only = 0;
+}
+
+extern "C" int cubics_solve_satisfy(const cubics_model* h, const cubics_search_config* cfg, cubics_solution_cb cb,
+                                    void* user, cubics_result* out) {
+    if (!h || !cfg || !out) return CUBICS_E_INVALID;
+    return guarded([&] {
+        const double t0 = now_ms();
+        std::memset(out, 0, sizeof *out);
+        const HostModel& m = h->m;
+        const int engine = pick_engine(*cfg, false);
+        const bool record = cb && !cfg->count_only;
+        uint64_t cap = default_sol_cap(m, *cfg);
+        RunOut r;
+        run_search(m, *cfg, engine, record, cap, r);
+        if (record && r.ws.stats[3] > r.rec.count && r.rec.count == cap) { // buffer overflow: rerun exact
+            RunOut r2;
+            run_search(m, *cfg, engine, record, r.ws.stats[3], r2);
+            r2.h2d += r.h2d;
+            r2.d2h += r.d2h;
+            r2.launches += r.launches;
+            r = std::move(r2);
+        }
+        fill_result(r, out);
+        const int n = m.n_vars();
+        out->complete = !r.ws.limit_hit && !r.ws.user_stop;
+        out->has_solution = r.ws.stats[3] > 0;
+        if (m.goal != CUBICS_SATISFY && r.rec.count) {
+            const size_t last = r.rec.count - 1;
+            out->objective = m.offset[m.goal_var] + r.rec.vals[last * n + m.goal_var];
+        }
+        if (record && r.rec.count) {
+            std::vector<uint64_t> order(r.rec.count);
+            std::iota(order.begin(), order.end(), 0);
+            if (r.KW) {
+                const int KW = r.KW;
+                const uint32_t* K = r.rec.keys.data();
+                std::sort(order.begin(), order.end(), [&](uint64_t a, uint64_t b) {
+                    return std::lexicographical_compare(K + a * KW, K + (a + 1) * KW, K + b * KW, K + (b + 1) * KW);
+                });
+            }
+            std::vector<int64_t> vals(n);
+            for (uint64_t i = 0; i < order.size(); ++i) {
+                const uint64_t s = order[i];
+                for (int v = 0; v < n; ++v) vals[v] = m.offset[v] + r.rec.vals[s * n + v];
+                if (!cb(user, vals.data(), n)) {
+                    if (!r.KW && !r.rec.stats.empty()) { // parity: the reference stops right here
+                        out->stats.nodes = r.rec.stats[s * 3 + 0];
+                        out->stats.failures = r.rec.stats[s * 3 + 1];
+                        out->stats.rounds = r.rec.stats[s * 3 + 2];
+                        out->stats.solutions = i + 1;
+                    }
+                    out->complete = 0;
+                    break;
+                }
+            }
+        }
+        out->total_ms = now_ms() - t0;
+        return CUBICS_OK;
+    });
+}
+
+extern "C" int cubics_solve_optimize(const cubics_model* h, const cubics_search_config* cfg, int64_t* best_values,
+                                     cubics_result* out) {
+    if (!h || !cfg || !out) return CUBICS_E_INVALID;
+    return guarded([&] {
+        const double t0 = now_ms();
+        std::memset(out, 0, sizeof *out);
+        const HostModel& m = h->m;
+        if (m.goal == CUBICS_SATISFY) throw StatusError{CUBICS_E_NO_OBJECTIVE, "solve_optimize requires a minimize or maximize goal"};
+        cubics_search_config c = *cfg;
+        if (c.engine == CUBICS_ENGINE_AUTO) c.engine = CUBICS_ENGINE_PARITY;
+        const int engine = pick_engine(c, true);
+        RunOut r;
+        // parity: every incumbent is recorded in order (max_solutions bounds them); parallel: global incumbent
+        const bool parallel = engine == CUBICS_ENGINE_PARALLEL;
+        run_search(m, c, engine, !parallel, parallel ? 0 : default_sol_cap(m, c), r);
+        fill_result(r, out);
+        const int n = m.n_vars();
+        out->complete = !r.ws.limit_hit;
+        std::vector<uint16_t> best;
+        if (parallel) {
+            if (r.ws.has_bound) best = r.inc_vals;
+        } else if (r.rec.count) {
+            best.assign(r.rec.vals.end() - n, r.rec.vals.end());
+        }
+        out->has_solution = !best.empty() || (n == 0 && r.ws.stats[3] > 0);
+        if (!best.empty()) {
+            out->objective = m.offset[m.goal_var] + best[m.goal_var];
+            if (best_values)
+                for (int v = 0; v < n; ++v) best_values[v] = m.offset[v] + best[v];
+        }
+        out->total_ms = now_ms() - t0;
+        return CUBICS_OK;
+    });
+}
+
+extern "C" int cubics_solve_shard(const cubics_model* h, const cubics_search_config* cfg, int32_t shard_index,
+                                  int32_t shard_count, cubics_keyed_solution_cb cb, void* user, cubics_result* out) {
+    if (!h || !cfg || !out || shard_count < 1 || shard_index < 0 || shard_index >= shard_count) return CUBICS_E_INVALID;
+    return guarded([&]() -> int {
+        const double t0 = now_ms();
+        std::memset(out, 0, sizeof *out);
+        if (shard_count != 1) throw StatusError{CUBICS_E_UNSUPPORTED, "multi-shard search not built yet"};
+        const HostModel& m = h->m;
+        cubics_search_config c = *cfg;
+        c.engine = CUBICS_ENGINE_PARALLEL;
+        pick_engine(c, m.goal != CUBICS_SATISFY);
+        const bool record = cb && !c.count_only;
+        RunOut r;
+        run_search(m, c, CUBICS_ENGINE_PARALLEL, record, record ? default_sol_cap(m, c) : 0, r);
+        fill_result(r, out);
+        out->complete = 1;
+        out->has_solution = r.ws.stats[3] > 0;
+        const int n = m.n_vars();
+        std::vector<int64_t> vals(n);
+        for (uint64_t s = 0; s < r.rec.count; ++s) {
+            for (int v = 0; v < n; ++v) vals[v] = m.offset[v] + r.rec.vals[s * n + v];
+            if (!cb(user, r.rec.keys.data() + s * r.KW, r.KW, vals.data(), n)) break;
+        }
+        out->total_ms = now_ms() - t0;
+        return CUBICS_OK;
+    });
+}
+
+namespace {
+int run_prop(const cubics_model* h, const uint64_t* words_in, uint64_t* words_out, int32_t alldiff, int32_t max_rounds,
+             const int32_t* cons, int32_t n_cons, bool removals_only, cubics_fixpoint_result* fr) {
+    const HostModel& m = h->m;
+    const int dev = current_device(-1);
+    Prepared P;
+    // the removal subset decides which constraints are evaluated (INT64_MIN pre-check included)
+    HostModel sub;
+    const HostModel* use = &m;
+    std::vector<uint8_t> enabled;
+    if (removals_only && cons) {
+        std::vector<char> on(m.n_cons(), 0);
+        for (int i = 0; i < n_cons; ++i) {
+            if (cons[i] < 0 || cons[i] >= m.n_cons()) throw StatusError{CUBICS_E_INVALID, "constraint index out of range"};
+            on[cons[i]] = 1;
+        }
+        sub = m;
+        sub.con_kind.clear();
+        sub.con_op.clear();
+        sub.con_value.clear();
+        sub.con_start.assign(1, 0);
+        sub.term_var.clear();
+        sub.term_coeff.clear();
+        for (int c = 0; c < m.n_cons(); ++c) {
+            if (!on[c]) continue;
+            sub.con_kind.push_back(m.con_kind[c]);
+            sub.con_op.push_back(m.con_op[c]);
+            sub.con_value.push_back(m.con_value[c]);
+            for (int t = m.con_start[c]; t < m.con_start[c + 1]; ++t) {
+                sub.term_var.push_back(m.term_var[t]);
+                sub.term_coeff.push_back(m.term_coeff[t]);
+            }
+            sub.con_start.push_back(static_cast<int32_t>(sub.term_var.size()));
+        }
+        use = &sub;
+    }
+    prepare(*use, words_in, P);
+    const size_t NWP = P.NWP;
+    const int block = parity_block(P);
+    bool in_smem = true;
+    dev::SmemLayout L = dev::smem_layout(P.W, P.n, P.total_members, block / 32, 0, true);
+    if (L.total > kSmemBudget) {
+        in_smem = false;
+        L = dev::smem_layout(P.W, P.n, P.total_members, block / 32, 0, false);
+    }
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t at = (off + 255) & ~size_t(255);
+        off = at + std::max<size_t>(bytes, 16);
+        return at;
+    };
+    const size_t a_blob = take(P.blob.bytes.size());
+    const size_t a_dom = take(sizeof(uint32_t) * NWP);
+    const size_t a_out = take(sizeof(uint32_t) * NWP);
+    const size_t a_res = take(sizeof(int32_t) * 8);
+    const size_t a_scr = take(in_smem ? 0 : sizeof(uint32_t) * 2 * NWP);
+    uint8_t* base = device_arena(dev, off);
+    std::vector<uint8_t> stage(a_dom + sizeof(uint32_t) * NWP, 0);
+    std::memcpy(stage.data() + a_blob, P.blob.bytes.data(), P.blob.bytes.size());
+    std::memcpy(stage.data() + a_dom, P.blob.bytes.data() + P.o_dom, sizeof(uint32_t) * NWP);
+    cudaStream_t st = nullptr;
+    CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    CU(cudaMemcpyAsync(base, stage.data(), stage.size(), cudaMemcpyHostToDevice, st));
+    PropParams PP{};
+    PP.M = P.bind(base + a_blob);
+    PP.alldiff = alldiff == CUBICS_FORWARD_CHECKING ? 0 : 1;
+    PP.max_rounds = max_rounds;
+    PP.removals_only = removals_only ? 1 : 0;
+    PP.enabled = nullptr;
+    PP.dom = reinterpret_cast<uint32_t*>(base + a_dom);
+    PP.out = reinterpret_cast<uint32_t*>(base + a_out);
+    PP.result = reinterpret_cast<int32_t*>(base + a_res);
+    uint32_t* scr = reinterpret_cast<uint32_t*>(base + a_scr);
+#define LP(w) launch_propagate<w>(PP, block, L.total, st, scr, in_smem ? 1 : 0)
+    CUBICS_DISPATCH_W(P.W, LP)
+#undef LP
+    std::vector<uint32_t> res32(NWP);
+    int32_t res[8] = {0};
+    CU(cudaMemcpyAsync(res32.data(), removals_only ? (void*)PP.out : (void*)PP.dom, sizeof(uint32_t) * NWP,
+                       cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(res, PP.result, sizeof res, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    cudaStreamDestroy(st);
+    if (res[4] == DERR_OVERFLOW) throw StatusError{CUBICS_E_OVERFLOW, "overflow in linear propagation"};
+    // back to the u64 reference layout
+    for (int v = 0; v < m.n_vars(); ++v) {
+        const int nw64 = m.word_start[v + 1] - m.word_start[v];
+        for (int i = 0; i < nw64; ++i) {
+            uint64_t lo = 2 * i < P.W ? res32[(size_t)v * P.W + 2 * i] : 0;
+            uint64_t hi = 2 * i + 1 < P.W ? res32[(size_t)v * P.W + 2 * i + 1] : 0;
+            words_out[m.word_start[v] + i] = lo | (hi << 32);
+        }
+    }
+    if (fr) {
+        fr->failed = res[0];
+        fr->failed_var = res[1];
+        fr->rounds = res[2];
+        fr->last_status = res[3];
+    }
+    return CUBICS_OK;
+}
+} // namespace
+
+extern "C" int cubics_propagate(const cubics_model* h, uint64_t* words, int32_t alldiff, int32_t max_rounds,
+                                cubics_fixpoint_result* out) {
+    if (!h || !words || !out) return CUBICS_E_INVALID;
+    return guarded([&] { return run_prop(h, words, words, alldiff, max_rounds, nullptr, 0, false, out); });
+}
+
+extern "C" int cubics_removals(const cubics_model* h, const uint64_t* words, int32_t alldiff, const int32_t* cons,
+                               int32_t n_cons, uint64_t* removed) {
+    if (!h || !words || !removed) return CUBICS_E_INVALID;
+    return guarded([&] { return run_prop(h, words, removed, alldiff, 1, cons, n_cons, true, nullptr); });
+}
+
+#define CUBICS_STR2(x) #x
+#define CUBICS_STR(x) CUBICS_STR2(x)
+extern "C" const char* cubics_build_info(void) {
+    return "cubics-b200 abi=1 arch=sm_100a engine=persistent-dfs(parity|parallel) nvcc=" CUBICS_STR(__CUDACC_VER_MAJOR__) "." CUBICS_STR(__CUDACC_VER_MINOR__);
+}
+
+extern "C" int cubics_device_count(void) {
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) return 0;
+    return c;
+}

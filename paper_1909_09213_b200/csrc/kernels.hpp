@@ -1,0 +1,19 @@
+// Launch interface of the device kernels. Each domain word count W in {1,2,4,8,16,32} is
+// instantiated in its own translation unit (kernels_inst.cu compiled with -DCUBICS_W=W).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "device_model.hpp"
+
+namespace cubics {
+
+template <int W>
+cudaError_t launch_search(const SearchParams& P, int grid, int block, size_t smem, cudaStream_t st);
+template <int W>
+cudaError_t occupancy_search(int block, size_t smem, int* blocks_per_sm);
+template <int W>
+cudaError_t launch_propagate(const PropParams& P, int block, size_t smem, cudaStream_t st, uint32_t* scratch,
+                             int in_smem);
+
+} // namespace cubics

@@ -1,0 +1,38 @@
+// One instantiation of the search / propagation kernels for domain word count CUBICS_W.
+#include "kernels.hpp"
+#include "search.cuh"
+
+#ifndef CUBICS_W
+#error "compile with -DCUBICS_W=<1|2|4|8|16|32>"
+#endif
+
+namespace cubics {
+
+template <>
+cudaError_t launch_search<CUBICS_W>(const SearchParams& P, int grid, int block, size_t smem, cudaStream_t st) {
+    auto k = dev::search_kernel<CUBICS_W>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k<<<grid, block, smem, st>>>(P);
+    return cudaGetLastError();
+}
+
+template <>
+cudaError_t occupancy_search<CUBICS_W>(int block, size_t smem, int* out) {
+    auto k = dev::search_kernel<CUBICS_W>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, k, block, smem);
+}
+
+template <>
+cudaError_t launch_propagate<CUBICS_W>(const PropParams& P, int block, size_t smem, cudaStream_t st,
+                                       uint32_t* scratch, int in_smem) {
+    auto k = dev::propagate_kernel<CUBICS_W>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k<<<1, block, smem, st>>>(P, scratch, in_smem);
+    return cudaGetLastError();
+}
+
+} // namespace cubics

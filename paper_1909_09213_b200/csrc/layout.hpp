@@ -1,0 +1,47 @@
+// Shared-memory layout of one search context; used by the kernels and by the host launcher.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+#ifndef __CUDACC__
+#define CUBICS_HD
+#else
+#define CUBICS_HD __host__ __device__
+#endif
+
+namespace cubics {
+namespace dev {
+
+CUBICS_HD constexpr size_t round4(size_t x) { return (x + 3) & ~size_t(3); }
+
+// per-warp alldifferent scratch: BFS layers [66] + ancestor sets [64] (u64) + value owners [W*32] (u8)
+CUBICS_HD constexpr int warp_scratch_bytes(int W) { return (66 + 64) * 8 + W * 32; }
+
+struct SmemLayout {
+    size_t dom, rm, mates, scratch, path, bestkey, total;
+    int stride;
+};
+
+CUBICS_HD inline SmemLayout smem_layout(int W, int n, int total_members, int nw, int KW, bool dom_in_smem) {
+    SmemLayout L{};
+    const size_t NWP = round4((size_t)n * W);
+    size_t p = 0;
+    L.dom = p;
+    L.rm = p + (dom_in_smem ? NWP * 4 : 0);
+    p += dom_in_smem ? 2 * NWP * 4 : 0;
+    L.mates = p;
+    p += ((size_t)total_members * 2 + 15) & ~size_t(15);
+    L.stride = (warp_scratch_bytes(W) + 15) & ~15;
+    L.scratch = p;
+    p += (size_t)nw * L.stride;
+    L.path = p;
+    p += ((size_t)KW * 4 + 15) & ~size_t(15);
+    L.bestkey = p;
+    p += ((size_t)KW * 4 + 15) & ~size_t(15);
+    L.total = p;
+    return L;
+}
+
+} // namespace dev
+} // namespace cubics

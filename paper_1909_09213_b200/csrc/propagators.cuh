@@ -1,0 +1,644 @@
+// Device propagators and the bulk-synchronous round, sm_100a.
+//
+// One search context = one thread block. Its domains live in shared memory (or in a per-context
+// HBM/L2 slab when they do not fit) as W u32 words per variable. A round follows the
+// reference's snapshot semantics exactly (propagation.cpp:480-514): every propagator reads the
+// frozen domains and ORs its removals into a removal buffer `rm` with atomics (the RemovalSet
+// union, :26-99, without materialising per-call sets); after a barrier, the apply step does
+// dom &= ~rm, detects "changed" and emptiness with __syncthreads_or, and clears rm.
+//
+// Removal masks may contain bits of values that are absent: the apply step ANDs them with the
+// domain, which is exactly the reference's "only values present in the snapshot are recorded"
+// rule (add_value, propagation.cpp:42-48).
+#pragma once
+
+#include <cstdint>
+
+#include "device_model.hpp"
+#include "layout.hpp"
+
+namespace cubics {
+namespace dev {
+
+constexpr unsigned FULL = 0xffffffffu;
+typedef __int128 i128;
+
+enum RoundStatus : int { R_CHANGED = 0, R_STABLE = 1, R_FAILED = 2, R_ERROR = 3 };
+
+// ------------------------------------------------------------------ bitset helpers
+template <int W>
+__device__ __forceinline__ bool dom_empty(const uint32_t* d) {
+    uint32_t o = 0;
+#pragma unroll
+    for (int i = 0; i < W; ++i) o |= d[i];
+    return o == 0;
+}
+
+template <int W>
+__device__ __forceinline__ int dom_size(const uint32_t* d) {
+    int s = 0;
+#pragma unroll
+    for (int i = 0; i < W; ++i) s += __popc(d[i]);
+    return s;
+}
+
+template <int W>
+__device__ __forceinline__ int dom_first(const uint32_t* d) { // -1 when empty
+    int r = -1;
+#pragma unroll
+    for (int i = W - 1; i >= 0; --i)
+        if (d[i]) r = i * 32 + __ffs(d[i]) - 1;
+    return r;
+}
+
+template <int W>
+__device__ __forceinline__ int dom_last(const uint32_t* d) {
+    int r = -1;
+#pragma unroll
+    for (int i = 0; i < W; ++i)
+        if (d[i]) r = i * 32 + 31 - __clz(d[i]);
+    return r;
+}
+
+__device__ __forceinline__ long long clampbit(i128 x, int nb) {
+    return x < -1 ? -1LL : (x > (i128)nb ? (long long)nb : (long long)x);
+}
+
+// bits of [lo, hi] (global bit indices, may lie outside the word) inside word w
+__device__ __forceinline__ uint32_t range_word(int w, long long lo, long long hi) {
+    long long a = lo - (long long)w * 32, b = hi - (long long)w * 32;
+    if (b < 0 || a > 31 || a > b) return 0u;
+    int aa = a < 0 ? 0 : (int)a;
+    int bb = b > 31 ? 31 : (int)b;
+    uint32_t hiMask = bb == 31 ? 0xffffffffu : ((1u << (bb + 1)) - 1u);
+    return hiMask & ~((1u << aa) - 1u);
+}
+
+// word i of (src << s): out bit j = src bit (j - s); s may be negative; out-of-range bits are 0
+template <int W>
+__device__ __forceinline__ uint32_t shifted_word(const uint32_t* src, int i, long long s) {
+    long long b = (long long)i * 32 - s;
+    long long q = b >> 5;
+    int r = (int)(b & 31);
+    uint32_t lo = (q >= 0 && q < W) ? src[q] : 0u;
+    uint32_t hi = (q + 1 >= 0 && q + 1 < W) ? src[q + 1] : 0u;
+    return r ? ((lo >> r) | (hi << (32 - r))) : lo;
+}
+
+template <int W>
+__device__ __forceinline__ void or_range(uint32_t* rmv, const uint32_t* dv, long long lo, long long hi) {
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        uint32_t m = range_word(w, lo, hi) & dv[w];
+        if (m) atomicOr(rmv + w, m);
+    }
+}
+
+__device__ __forceinline__ void or_bit(uint32_t* rmv, const uint32_t* dv, i128 bit, int nb) {
+    if (bit < 0 || bit >= (i128)nb) return;
+    int b = (int)bit;
+    uint32_t m = (1u << (b & 31)) & dv[b >> 5];
+    if (m) atomicOr(rmv + (b >> 5), m);
+}
+
+__device__ __forceinline__ long long wrap_add(long long a, long long b) {
+    return (long long)((unsigned long long)a + (unsigned long long)b);
+}
+
+// ------------------------------------------------------------------ RelBin (propagation.cpp:120-194)
+template <int W>
+__device__ __forceinline__ void prop_relbin(const DevModel& M, int c, const uint32_t* dom, uint32_t* rm) {
+    constexpr int NB = W * 32;
+    const RelBinRec r = M.rb[c];
+    const int x = r.x, op = r.yop & 7, y = (r.yop >> 3) - 1;
+    const uint32_t* dx = dom + (size_t)x * W;
+    uint32_t* rx = rm + (size_t)x * W;
+    const long long offx = M.off[x];
+    if (y < 0) { // x op literal (:126-141); absent values are masked by dx
+        const i128 lit = r.k;
+        switch (op) {
+        case 0: or_range<W>(rx, dx, clampbit(lit - offx, NB), NB); break;                          // <
+        case 1: or_range<W>(rx, dx, clampbit((i128)wrap_add(r.k, 1) - offx, NB), NB); break;        // <=
+        case 2: or_range<W>(rx, dx, -1, clampbit(lit - offx, NB)); break;                           // >
+        case 3: or_range<W>(rx, dx, -1, clampbit((i128)wrap_add(r.k, -1) - offx, NB)); break;       // >=
+        case 4: {                                                                                   // =
+            i128 b = lit - offx;
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                uint32_t keep = (b >= (i128)w * 32 && b < (i128)w * 32 + 32) ? (1u << (int)(b - w * 32)) : 0u;
+                uint32_t m = dx[w] & ~keep;
+                if (m) atomicOr(rx + w, m);
+            }
+            break;
+        }
+        default: or_bit(rx, dx, lit - offx, NB); break;                                             // !=
+        }
+        return;
+    }
+    const uint32_t* dy = dom + (size_t)y * W;
+    uint32_t* ry = rm + (size_t)y * W;
+    const long long offy = M.off[y];
+    const i128 k = r.k;
+    if (op == 5) { // x != y + k: value consistency from singletons (:180-191)
+        int sy = dom_size<W>(dy), sx = dom_size<W>(dx);
+        if (sy == 1) or_bit(rx, dx, (i128)offy + dom_first<W>(dy) + k - offx, NB);
+        if (sx == 1) or_bit(ry, dy, (i128)offx + dom_first<W>(dx) - k - offy, NB);
+        return;
+    }
+    if (dom_empty<W>(dx) || dom_empty<W>(dy)) return;
+    switch (op) {
+    case 0: // x < y + k : x keeps v < max(y)+k ; y keeps w > min(x)-k
+        or_range<W>(rx, dx, clampbit((i128)offy + dom_last<W>(dy) + k - offx, NB), NB);
+        or_range<W>(ry, dy, -1, clampbit((i128)offx + dom_first<W>(dx) - k - offy, NB));
+        break;
+    case 1: // x <= y + k
+        or_range<W>(rx, dx, clampbit((i128)offy + dom_last<W>(dy) + k + 1 - offx, NB), NB);
+        or_range<W>(ry, dy, -1, clampbit((i128)offx + dom_first<W>(dx) - k - 1 - offy, NB));
+        break;
+    case 2: // x > y + k : x keeps v > min(y)+k ; y keeps w < max(x)-k
+        or_range<W>(rx, dx, -1, clampbit((i128)offy + dom_first<W>(dy) + k - offx, NB));
+        or_range<W>(ry, dy, clampbit((i128)offx + dom_last<W>(dx) - k - offy, NB), NB);
+        break;
+    case 3: // x >= y + k
+        or_range<W>(rx, dx, -1, clampbit((i128)offy + dom_first<W>(dy) + k - 1 - offx, NB));
+        or_range<W>(ry, dy, clampbit((i128)offx + dom_last<W>(dx) - k + 1 - offy, NB), NB);
+        break;
+    default: { // x = y + k, domain consistent: keep_x = D(y) << s, keep_y = D(x) >> s
+        i128 s128 = (i128)offy + k - offx;
+        long long s = s128 > (i128)(NB + 64) ? (long long)(NB + 64)
+                                             : (s128 < -(i128)(NB + 64) ? -(long long)(NB + 64) : (long long)s128);
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            uint32_t mx = dx[w] & ~shifted_word<W>(dy, w, s);
+            if (mx) atomicOr(rx + w, mx);
+            uint32_t my = dy[w] & ~shifted_word<W>(dx, w, -s);
+            if (my) atomicOr(ry + w, my);
+        }
+        break;
+    }
+    }
+}
+
+// ------------------------------------------------------------------ Linear (propagation.cpp:196-252)
+__device__ __forceinline__ bool fits64(i128 v) {
+    return v >= (i128)(-9223372036854775807LL - 1) && v <= (i128)9223372036854775807LL;
+}
+
+__device__ __forceinline__ i128 floor_div(i128 a, long long b) {
+    i128 q = a / b;
+    if ((a % b != 0) && ((a < 0) != (b < 0))) q -= 1;
+    return q;
+}
+__device__ __forceinline__ i128 ceil_div(i128 a, long long b) {
+    i128 q = a / b;
+    if ((a % b != 0) && ((a < 0) == (b < 0))) q += 1;
+    return q;
+}
+
+// filter_linear_le over terms [b, e) with coefficients sign*coeff; false on int64 overflow
+template <int W>
+__device__ bool filter_le(const DevModel& M, int b, int e, long long sign, long long bound,
+                          const uint32_t* dom, uint32_t* rm) {
+    constexpr int NB = W * 32;
+    long long total = 0;
+    for (int t = b; t < e; ++t) { // :217-224
+        const int v = M.lin_var[t];
+        const uint32_t* d = dom + (size_t)v * W;
+        if (dom_empty<W>(d)) return true;
+        const long long a = sign * M.lin_coeff[t];
+        const long long val = M.off[v] + (a > 0 ? dom_first<W>(d) : dom_last<W>(d));
+        i128 tm = (i128)a * val;
+        if (!fits64(tm)) return false;
+        i128 s = (i128)total + tm;
+        if (!fits64(s)) return false;
+        total = (long long)s;
+    }
+    for (int t = b; t < e; ++t) { // :225-235
+        const int v = M.lin_var[t];
+        const uint32_t* d = dom + (size_t)v * W;
+        const long long a = sign * M.lin_coeff[t];
+        const long long offv = M.off[v];
+        const long long tm = a * (offv + (a > 0 ? dom_first<W>(d) : dom_last<W>(d)));
+        i128 rest = (i128)total + (i128)wrap_add(0, -tm); // checked_add(total, -term_min)
+        if (!fits64(rest)) return false;
+        const i128 budget = (i128)bound - rest;
+        uint32_t* rv = rm + (size_t)v * W;
+        if (a > 0) { // remove v > floor(budget / a)
+            i128 thr = a == 1 ? budget : floor_div(budget, a);
+            or_range<W>(rv, d, clampbit(thr + 1 - offv, NB), NB);
+        } else {     // remove v < budget / a, i.e. v <= ceil(budget / a) - 1
+            i128 thr = a == -1 ? -budget - 1 : ceil_div(budget, a) - 1;
+            or_range<W>(rv, d, -1, clampbit(thr - offv, NB));
+        }
+    }
+    return true;
+}
+
+template <int W>
+__device__ __forceinline__ bool prop_linear(const DevModel& M, int c, const uint32_t* dom, uint32_t* rm) {
+    const int b = M.lin_start[c], e = M.lin_start[c + 1];
+    const long long bound = M.lin_bound[c];
+    if (!filter_le<W>(M, b, e, 1, bound, dom, rm)) return false;
+    // Eq: the >= direction as sum(-a x) <= -bound (:243-250); INT64_MIN coefficients / bounds
+    // (whose negation overflows) are rejected on the host before launch.
+    if (M.lin_op[c] == 1 && !filter_le<W>(M, b, e, -1, -bound, dom, rm)) return false;
+    return true;
+}
+
+// ------------------------------------------------------------------ AllDifferent (warp per constraint)
+// Members are spread over the 32 lanes, two slots per lane (member l and l+32), so one warp
+// handles up to 64 members. Member domains are loaded into a common value universe (W words).
+
+struct WarpScratch {
+    unsigned long long* layers; // [66] BFS frontier member sets
+    unsigned long long* anc;    // [64] ancestor sets (Warshall closure)
+    uint8_t* owner;             // [W*32] universe value -> matched member
+};
+
+template <int W>
+__device__ __forceinline__ bool testbit_r(const uint32_t (&a)[W], int bit) {
+    bool t = false;
+#pragma unroll
+    for (int w = 0; w < W; ++w) t |= (w == (bit >> 5)) && ((a[w] >> (bit & 31)) & 1u);
+    return t;
+}
+
+__device__ __forceinline__ uint32_t bitword(int bit, int w) { // word w of the singleton {bit}; bit < 0 -> 0
+    return (bit >= 0 && (bit >> 5) == w) ? (1u << (bit & 31)) : 0u;
+}
+
+__device__ __forceinline__ unsigned long long ballot64(bool a, bool b) {
+    return (unsigned long long)__ballot_sync(FULL, a) | ((unsigned long long)__ballot_sync(FULL, b) << 32);
+}
+
+// Bit-parallel BFS augmenting path from member r (uniform). Updates mate[], MV. true on success.
+template <int W>
+__device__ bool gac_augment(int r, const uint32_t (&D0)[W], const uint32_t (&D1)[W], bool h0, bool h1,
+                            int& m0, int& m1, uint32_t (&MV)[W], const WarpScratch& ws, int lane) {
+    uint32_t vis[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) vis[w] = 0;
+    unsigned long long front = 1ull << r;
+    if (lane == 0) ws.layers[0] = front;
+    int L = 0;
+    for (;;) {
+        const bool f0 = h0 && ((front >> lane) & 1ull), f1 = h1 && ((front >> (lane + 32)) & 1ull);
+        uint32_t nv[W];
+        uint32_t any = 0;
+        int found = -1;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            uint32_t c = (f0 ? D0[w] : 0u) | (f1 ? D1[w] : 0u);
+            nv[w] = __reduce_or_sync(FULL, c) & ~vis[w];
+            vis[w] |= nv[w];
+            any |= nv[w];
+            uint32_t fr = nv[w] & ~MV[w];
+            if (fr && found < 0) found = w * 32 + __ffs(fr) - 1;
+        }
+        if (!any) return false;
+        if (found >= 0) { // walk back through the layers, re-matching along the path
+            int j = found;
+            for (int l = L;; --l) {
+                __syncwarp();
+                const unsigned long long lay = ws.layers[l];
+                const bool c0 = h0 && ((lay >> lane) & 1ull) && testbit_r<W>(D0, j);
+                const bool c1 = h1 && ((lay >> (lane + 32)) & 1ull) && testbit_r<W>(D1, j);
+                const unsigned long long bal = ballot64(c0, c1);
+                const int k = __ffsll((long long)bal) - 1;
+                const int kl = k & 31, ks = k >> 5;
+                const int old = __shfl_sync(FULL, ks ? m1 : m0, kl);
+                if (lane == kl) {
+                    if (ks) m1 = j;
+                    else m0 = j;
+                }
+                if (l == 0) break;
+                j = old;
+            }
+#pragma unroll
+            for (int w = 0; w < W; ++w) MV[w] |= bitword(found, w);
+            __syncwarp();
+            return true;
+        }
+        const bool t0 = h0 && m0 >= 0 && testbit_r<W>(nv, m0);
+        const bool t1 = h1 && m1 >= 0 && testbit_r<W>(nv, m1);
+        front = ballot64(t0, t1);
+        ++L;
+        __syncwarp();
+        if (lane == 0) ws.layers[L] = front;
+    }
+}
+
+// prop_alldiff_gac (propagation.cpp:348-433): removes exactly the values in no maximum matching;
+// the result is unique, so this bit-parallel formulation (warm-started matching, Warshall
+// closure of the member graph m -> k iff mate(m) in D(k)) equals the reference's Kuhn + Tarjan.
+// On infeasibility the reference wipes the first member Kuhn leaves unmatched (:379-386); with
+// exact_wipe we recompute the matching greedily in member order, which leaves the same first
+// member unmatched (transversal-matroid greedy basis), and wipe it.
+template <int W>
+__device__ void prop_alldiff_gac(const DevModel& M, int a, const uint32_t* dom, uint32_t* rm, int16_t* mates,
+                                 const WarpScratch& ws, int lane, int exact_wipe) {
+    const int b = M.ad_start[a], n = M.ad_start[a + 1] - b;
+    const bool h0 = lane < n, h1 = lane + 32 < n;
+    uint32_t D0[W], D1[W];
+    int v0 = -1, v1 = -1, s0 = 0, s1 = 0;
+    if (h0) {
+        v0 = M.ad_var[b + lane];
+        s0 = M.ad_shift[b + lane];
+    }
+    if (h1) {
+        v1 = M.ad_var[b + lane + 32];
+        s1 = M.ad_shift[b + lane + 32];
+    }
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        D0[w] = h0 ? (s0 ? shifted_word<W>(dom + (size_t)v0 * W, w, s0) : dom[(size_t)v0 * W + w]) : 0u;
+        D1[w] = h1 ? (s1 ? shifted_word<W>(dom + (size_t)v1 * W, w, s1) : dom[(size_t)v1 * W + w]) : 0u;
+    }
+    int m0 = h0 ? mates[lane] : -1, m1 = h1 ? mates[lane + 32] : -1;
+    if (m0 >= 0 && !testbit_r<W>(D0, m0)) m0 = -1; // warm start: keep still-valid edges
+    if (m1 >= 0 && !testbit_r<W>(D1, m1)) m1 = -1;
+    uint32_t MV[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) MV[w] = __reduce_or_sync(FULL, bitword(m0, w) | bitword(m1, w));
+
+    unsigned long long unm = ballot64(h0 && m0 < 0, h1 && m1 < 0);
+    int fail = -1;
+    while (unm) {
+        const int r = __ffsll((long long)unm) - 1;
+        unm &= unm - 1;
+        if (!gac_augment<W>(r, D0, D1, h0, h1, m0, m1, MV, ws, lane)) {
+            fail = r;
+            break;
+        }
+    }
+    if (fail >= 0) {
+        if (exact_wipe) { // greedy matching in member order: its first failure is Kuhn's
+            m0 = m1 = -1;
+#pragma unroll
+            for (int w = 0; w < W; ++w) MV[w] = 0;
+            for (int r = 0; r < n; ++r)
+                if (!gac_augment<W>(r, D0, D1, h0, h1, m0, m1, MV, ws, lane)) {
+                    fail = r;
+                    break;
+                }
+        }
+        if (lane == (fail & 31)) {
+            const int v = (fail >> 5) ? v1 : v0;
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                uint32_t d = dom[(size_t)v * W + w];
+                if (d) atomicOr(rm + (size_t)v * W + w, d);
+            }
+        }
+        if (h0) mates[lane] = (int16_t)m0;
+        if (h1) mates[lane + 32] = (int16_t)m1;
+        __syncwarp();
+        return;
+    }
+    if (h0) {
+        mates[lane] = (int16_t)m0;
+        ws.owner[m0] = (uint8_t)lane;
+    }
+    if (h1) {
+        mates[lane + 32] = (int16_t)m1;
+        ws.owner[m1] = (uint8_t)(lane + 32);
+    }
+    __syncwarp();
+    // free values F = U & ~MV ; pred(k) = { m : mate(m) in D(k) }
+    uint32_t F[W];
+    unsigned long long p0 = 0, p1 = 0;
+    bool sd0 = false, sd1 = false;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        F[w] = __reduce_or_sync(FULL, D0[w] | D1[w]) & ~MV[w];
+        sd0 |= (D0[w] & F[w]) != 0;
+        sd1 |= (D1[w] & F[w]) != 0;
+        uint32_t x0 = D0[w] & MV[w], x1 = D1[w] & MV[w];
+        while (x0) {
+            p0 |= 1ull << ws.owner[w * 32 + __ffs(x0) - 1];
+            x0 &= x0 - 1;
+        }
+        while (x1) {
+            p1 |= 1ull << ws.owner[w * 32 + __ffs(x1) - 1];
+            x1 &= x1 - 1;
+        }
+    }
+    // Warshall: anc(k) = members that reach k
+    for (int p = 0; p < n; ++p) {
+        const unsigned long long ap = __shfl_sync(FULL, (p >> 5) ? p1 : p0, p & 31);
+        if ((p0 >> p) & 1ull) p0 |= ap;
+        if ((p1 >> p) & 1ull) p1 |= ap;
+    }
+    // members reached from free values (seeds: D(k) meets F)
+    const unsigned long long S = ballot64(h0 && sd0, h1 && sd1);
+    const bool r0 = h0 && (p0 & S), r1 = h1 && (p1 & S);
+    uint32_t KEEP[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) KEEP[w] = F[w] | __reduce_or_sync(FULL, (r0 ? bitword(m0, w) : 0u) | (r1 ? bitword(m1, w) : 0u));
+    ws.anc[lane] = p0;
+    ws.anc[lane + 32] = p1;
+    __syncwarp();
+    // an unmatched edge (k, j) survives iff j is kept above or owner(j) is in k's SCC
+#pragma unroll
+    for (int sl = 0; sl < 2; ++sl) {
+        const bool h = sl ? h1 : h0;
+        if (!h) continue;
+        const int k = lane + 32 * sl, mk = sl ? m1 : m0, v = sl ? v1 : v0, sh = sl ? s1 : s0;
+        const unsigned long long ak = sl ? p1 : p0;
+        uint32_t rem[W];
+        bool anyr = false;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            uint32_t cand = (sl ? D1[w] : D0[w]) & ~KEEP[w] & ~bitword(mk, w);
+            uint32_t x = cand;
+            while (x) {
+                const int bit = __ffs(x) - 1;
+                x &= x - 1;
+                const int m = ws.owner[w * 32 + bit];
+                if (((ak >> m) & 1ull) && ((ws.anc[m] >> k) & 1ull)) cand &= ~(1u << bit);
+            }
+            rem[w] = cand;
+            anyr |= cand != 0;
+        }
+        if (anyr) {
+#pragma unroll
+            for (int w = 0; w < W; ++w) { // back to the member's own bit positions
+                uint32_t mword = sh ? shifted_word<W>(rem, w, -sh) : rem[w];
+                if (mword) atomicOr(rm + (size_t)v * W + w, mword);
+            }
+        }
+    }
+    __syncwarp();
+}
+
+// prop_alldiff_fc (propagation.cpp:254-268): singleton values are removed from the other members
+template <int W>
+__device__ void prop_alldiff_fc(const DevModel& M, int a, const uint32_t* dom, uint32_t* rm, int lane) {
+    const int b = M.ad_start[a], n = M.ad_start[a + 1] - b;
+    const bool h0 = lane < n, h1 = lane + 32 < n;
+    uint32_t D0[W], D1[W];
+    int v0 = -1, v1 = -1, s0 = 0, s1 = 0;
+    if (h0) {
+        v0 = M.ad_var[b + lane];
+        s0 = M.ad_shift[b + lane];
+    }
+    if (h1) {
+        v1 = M.ad_var[b + lane + 32];
+        s1 = M.ad_shift[b + lane + 32];
+    }
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        D0[w] = h0 ? (s0 ? shifted_word<W>(dom + (size_t)v0 * W, w, s0) : dom[(size_t)v0 * W + w]) : 0u;
+        D1[w] = h1 ? (s1 ? shifted_word<W>(dom + (size_t)v1 * W, w, s1) : dom[(size_t)v1 * W + w]) : 0u;
+    }
+    const bool g0 = h0 && dom_size<W>(D0) == 1, g1 = h1 && dom_size<W>(D1) == 1;
+    const int x0 = g0 ? dom_first<W>(D0) : -1, x1 = g1 ? dom_first<W>(D1) : -1;
+    uint32_t once0[W], once1[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        once0[w] = __reduce_or_sync(FULL, bitword(x0, w));
+        once1[w] = __reduce_or_sync(FULL, bitword(x1, w));
+    }
+    const unsigned q0 = __match_any_sync(FULL, g0 ? x0 : -(lane + 1));
+    const unsigned q1 = __match_any_sync(FULL, g1 ? x1 : -(lane + 33));
+    const bool dup0 = g0 && (__popc(q0) > 1 || testbit_r<W>(once1, x0));
+    const bool dup1 = g1 && (__popc(q1) > 1 || testbit_r<W>(once0, x1));
+#pragma unroll
+    for (int sl = 0; sl < 2; ++sl) {
+        const bool h = sl ? h1 : h0;
+        if (!h) continue;
+        const bool g = sl ? g1 : g0, dup = sl ? dup1 : dup0;
+        const int x = sl ? x1 : x0, v = sl ? v1 : v0, sh = sl ? s1 : s0;
+        uint32_t rem[W];
+        bool anyr = false;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            uint32_t once = once0[w] | once1[w];
+            uint32_t r = g ? ((once & ~bitword(x, w)) | (dup ? bitword(x, w) : 0u)) : once;
+            rem[w] = r & (sl ? D1[w] : D0[w]);
+            anyr |= rem[w] != 0;
+        }
+        if (anyr) {
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                uint32_t mword = sh ? shifted_word<W>(rem, w, -sh) : rem[w];
+                if (mword) atomicOr(rm + (size_t)v * W + w, mword);
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ one bulk-synchronous round
+struct RoundCtx {
+    uint32_t* dom;
+    uint32_t* rm;
+    int16_t* mates;     // [total_members] persistent warm-start matchings
+    uint8_t* scratch;   // per-warp GAC scratch
+    int scratch_stride; // bytes per warp
+    const uint8_t* enabled;
+    int alldiff;
+    int exact_wipe;
+};
+
+template <int W>
+__device__ __forceinline__ WarpScratch warp_scratch(const RoundCtx& R, int warp) {
+    WarpScratch ws;
+    uint8_t* base = R.scratch + (size_t)warp * R.scratch_stride;
+    ws.layers = reinterpret_cast<unsigned long long*>(base);
+    ws.anc = ws.layers + 66;
+    ws.owner = reinterpret_cast<uint8_t*>(ws.anc + 64);
+    return ws;
+}
+
+
+// Phase A: every propagator against the frozen domains. *s_err receives DERR_OVERFLOW.
+template <int W>
+__device__ __forceinline__ void run_propagators(const DevModel& M, const RoundCtx& R, int* s_err) {
+    const int tid = threadIdx.x, T = blockDim.x, nw = T >> 5, warp = tid >> 5, lane = tid & 31;
+    const int ad_warps = M.na < nw ? M.na : nw;
+    const int prop_threads = nw > ad_warps ? (nw - ad_warps) * 32 : T;
+    if (tid < prop_threads) {
+        for (int c = tid; c < M.nr; c += prop_threads)
+            if (!R.enabled || R.enabled[c]) prop_relbin<W>(M, c, R.dom, R.rm);
+        for (int c = tid; c < M.nl; c += prop_threads)
+            if (!R.enabled || R.enabled[M.nr + c])
+                if (!prop_linear<W>(M, c, R.dom, R.rm)) *s_err = DERR_OVERFLOW;
+    }
+    if (warp >= nw - ad_warps) {
+        const WarpScratch ws = warp_scratch<W>(R, warp);
+        for (int a = warp - (nw - ad_warps); a < M.na; a += ad_warps) {
+            if (R.enabled && !R.enabled[M.nr + M.nl + a]) continue;
+            if (R.alldiff) prop_alldiff_gac<W>(M, a, R.dom, R.rm, R.mates + M.ad_start[a], ws, lane, R.exact_wipe);
+            else prop_alldiff_fc<W>(M, a, R.dom, R.rm, lane);
+        }
+    }
+}
+
+// Phase B: dom &= ~rm. Returns R_CHANGED / R_STABLE / R_FAILED / R_ERROR.
+// failed_var (when non-null) receives the lowest empty var id on failure.
+template <int W>
+__device__ __forceinline__ int apply_removals(const DevModel& M, const RoundCtx& R, int* s_err, int* s_min,
+                                              int* failed_var) {
+    const int tid = threadIdx.x, T = blockDim.x;
+    int changed = 0, empty_min = 0x7fffffff;
+    for (int v = tid; v < M.n; v += T) {
+        uint32_t* d = R.dom + (size_t)v * W;
+        uint32_t* r = R.rm + (size_t)v * W;
+        uint32_t any = 0;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            uint32_t rw = r[w], dw = d[w];
+            if (rw) {
+                if (dw & rw) {
+                    changed = 1;
+                    dw &= ~rw;
+                    d[w] = dw;
+                }
+                r[w] = 0;
+            }
+            any |= dw;
+        }
+        if (!any && v < empty_min) empty_min = v;
+    }
+    const int ch = __syncthreads_or(changed);
+    const int err = *s_err;
+    if (err) return R_ERROR;
+    if (!ch) return R_STABLE;
+    const int em = __syncthreads_or(empty_min != 0x7fffffff);
+    if (!em) return R_CHANGED;
+    if (failed_var) {
+        if (tid == 0) *s_min = 0x7fffffff;
+        __syncthreads();
+        if (empty_min != 0x7fffffff) atomicMin(s_min, empty_min);
+        __syncthreads();
+        *failed_var = *s_min;
+        __syncthreads();
+    }
+    return R_FAILED;
+}
+
+template <int W>
+__device__ __forceinline__ int block_round(const DevModel& M, const RoundCtx& R, int* s_err, int* s_min,
+                                           int* failed_var) {
+    run_propagators<W>(M, R, s_err);
+    __syncthreads();
+    return apply_removals<W>(M, R, s_err, s_min, failed_var);
+}
+
+// propagate_fixpoint (propagation.cpp:516-532); *rounds counts every round including the last
+template <int W>
+__device__ int block_fixpoint(const DevModel& M, const RoundCtx& R, int* s_err, int* s_min, int max_rounds,
+                              int* rounds, int* failed_var) {
+    int r = 0;
+    for (;;) {
+        const int st = block_round<W>(M, R, s_err, s_min, failed_var);
+        ++r;
+        if (st != R_CHANGED || (max_rounds > 0 && r >= max_rounds)) {
+            *rounds = r;
+            return st;
+        }
+    }
+}
+
+} // namespace dev
+} // namespace cubics

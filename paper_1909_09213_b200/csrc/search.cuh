@@ -1,0 +1,449 @@
+// Persistent search kernel, sm_100a: the reference's Dfs::descend (search.cpp:80-132) as an
+// iterative loop in one thread block per search context.
+//
+// * Labeling: first-fail / input-order selection is a block argmin over (popc, var id)
+//   (select_variable, search.cpp:13-28); the value is the domain minimum (__ffs, :30-32).
+// * Propagation: block_fixpoint (propagators.cuh) - all constraints in parallel per round.
+// * Backtracking: every left branch pushes a copy of the parent's post-propagation domains
+//   into a per-context decision stack in HBM (vectorised uint4 copies); the right branch
+//   restores it and removes the value. This is observationally identical to SearchStore's
+//   save-on-modify trail (state.cpp:12-36): both reinstate the state on entering the level.
+//   At most one frame per variable is live (each left branch fixes one more variable).
+// * Parallel engine: many contexts per GPU. A busy context donates its shallowest pending right
+//   branch to an idle one through a spin-locked queue in HBM; nodes are visited exactly once,
+//   so nodes/failures/rounds/solutions of a complete enumeration are exact sums. Each subtree
+//   carries its DFS path bits, the key that restores the reference's solution order.
+#pragma once
+
+#include "layout.hpp"
+#include "propagators.cuh"
+
+namespace cubics {
+namespace dev {
+
+__device__ __forceinline__ int ld_volatile(const int32_t* p) { return *reinterpret_cast<const volatile int32_t*>(p); }
+
+__device__ __forceinline__ void spin_lock(int32_t* l) {
+    int ns = 16;
+    while (atomicCAS(l, 0, 1) != 0) {
+        __nanosleep(ns);
+        ns = ns < 512 ? ns * 2 : ns;
+    }
+    __threadfence();
+}
+
+__device__ __forceinline__ void spin_unlock(int32_t* l) {
+    __threadfence();
+    atomicExch(l, 0);
+}
+
+// block-wide copy of nw4 uint4 words
+__device__ __forceinline__ void copy4(uint32_t* dst, const uint32_t* src, size_t nwords) {
+    uint4* d = reinterpret_cast<uint4*>(dst);
+    const uint4* s = reinterpret_cast<const uint4*>(src);
+    for (size_t i = threadIdx.x; i < nwords / 4; i += blockDim.x) d[i] = s[i];
+}
+
+__device__ __forceinline__ void copy4_cg(uint32_t* dst, const uint32_t* src, size_t nwords) {
+    uint4* d = reinterpret_cast<uint4*>(dst);
+    const uint4* s = reinterpret_cast<const uint4*>(src);
+    for (size_t i = threadIdx.x; i < nwords / 4; i += blockDim.x) d[i] = __ldcg(s + i);
+}
+
+// block argmin of (size, id) over unbound vars; -1 when every domain is a singleton
+template <int W>
+__device__ __forceinline__ int select_var(const DevModel& M, const uint32_t* dom, int first_fail, unsigned* s_red) {
+    const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = T >> 5;
+    unsigned best = 0xffffffffu;
+    for (int v = tid; v < M.n; v += T) {
+        const int sz = dom_size<W>(dom + (size_t)v * W);
+        if (sz > 1) {
+            const unsigned key = first_fail ? ((unsigned)sz << 21) | (unsigned)v : (unsigned)v;
+            best = key < best ? key : best;
+        }
+    }
+    best = __reduce_min_sync(FULL, best);
+    if (nw > 1) {
+        if (lane == 0) s_red[warp] = best;
+        __syncthreads();
+        unsigned x = lane < nw ? s_red[lane] : 0xffffffffu;
+        best = __reduce_min_sync(FULL, x);
+        __syncthreads();
+    }
+    return best == 0xffffffffu ? -1 : (int)(best & 0x1fffffu);
+}
+
+template <int W>
+__global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ int s_err, s_min, s_flag, s_src;
+    __shared__ unsigned s_red[32];
+    __shared__ long long s_ll;
+
+    const DevModel& M = P.M;
+    const int ctx = blockIdx.x, tid = threadIdx.x, T = blockDim.x, nw = T >> 5;
+    const bool parallel = P.mode == MODE_PARALLEL;
+    const int n = M.n;
+    const size_t NW = (size_t)n * W, NWP = round4(NW);
+    const int KW = P.KW;
+    const SmemLayout L = smem_layout(W, n, M.total_members, nw, KW, P.dom_in_smem);
+    uint32_t* dom = P.dom_in_smem ? reinterpret_cast<uint32_t*>(smem + L.dom) : P.gdom + (size_t)ctx * 2 * NWP;
+    uint32_t* rm = P.dom_in_smem ? reinterpret_cast<uint32_t*>(smem + L.rm) : dom + NWP;
+    int16_t* mates = reinterpret_cast<int16_t*>(smem + L.mates);
+    uint32_t* path = reinterpret_cast<uint32_t*>(smem + L.path);
+    uint32_t* bestkey = reinterpret_cast<uint32_t*>(smem + L.bestkey);
+    RoundCtx R{dom, rm, mates, smem + L.scratch, L.stride, nullptr, P.alldiff, P.exact_wipe};
+    uint32_t* frames = P.frames + (size_t)ctx * P.frame_cap * NWP;
+    int32_t* meta = P.frame_meta + (size_t)ctx * P.frame_cap * 4;
+    WorkState* ws = P.ws;
+    const size_t OS = NWP + round4((size_t)KW + 1);
+
+    for (size_t i = tid; i < NWP; i += T) rm[i] = 0;
+    for (int i = tid; i < M.total_members; i += T) mates[i] = -1;
+    for (int i = tid; i < KW; i += T) {
+        path[i] = 0;
+        bestkey[i] = 0xffffffffu;
+    }
+    if (tid == 0) s_err = 0;
+
+    unsigned long long nodes = 0, failures = 0, rounds = 0, sols = 0;
+    int sp = 0, base = 0, depth = 0;
+    bool has_bound = P.has_init_bound != 0;
+    long long bound = P.init_bound;
+    bool has_first = false;
+    const bool optimizing = M.goal != 0, minimizing = M.goal == 1;
+    const int obj = M.goal_var;
+
+    // ---- acquire the first subtree: the root for context 0, a donated one for the rest
+    auto get_work = [&]() -> bool {
+        if (tid == 0) {
+            atomicSub(&ws->outstanding, 1);
+            atomicAdd(&ws->n_idle, 1);
+            int got = -1, ns = 64;
+            for (;;) {
+                if (ld_volatile(&ws->stop)) break;
+                if (ld_volatile(&ws->q_count) > 0) {
+                    spin_lock(&ws->lock);
+                    volatile int32_t* qc = &ws->q_count;
+                    if (*qc > 0) {
+                        const int k = *qc - 1;
+                        got = reinterpret_cast<volatile int32_t*>(P.queue)[k];
+                        *qc = k;
+                    }
+                    spin_unlock(&ws->lock);
+                    if (got >= 0) break;
+                }
+                if (ld_volatile(&ws->outstanding) == 0) break;
+                __nanosleep(ns);
+                ns = ns < 2048 ? ns * 2 : ns;
+            }
+            if (got >= 0) {
+                atomicSub(&ws->n_idle, 1);
+                __threadfence();
+            }
+            s_src = got;
+        }
+        __syncthreads();
+        const int got = s_src;
+        if (got < 0) return false;
+        const uint32_t* ob = P.outbox + (size_t)got * OS;
+        copy4_cg(dom, ob, NWP);
+        for (int i = tid; i < KW; i += T) path[i] = __ldcg(ob + NWP + i);
+        depth = (int)__ldcg(ob + NWP + KW);
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            atomicExch(&P.outbox_busy[got], 0);
+        }
+        sp = base = 0;
+        return true;
+    };
+
+    bool have_work;
+    if (!parallel || ctx == 0) {
+        copy4(dom, M.init_dom, NWP);
+        have_work = true;
+    } else {
+        have_work = get_work();
+    }
+    __syncthreads();
+
+    while (have_work) {
+        // ================= node entry (descend, search.cpp:80-111)
+        ++nodes;
+        if (P.node_limit && nodes > P.node_limit) {
+            if (tid == 0) {
+                ws->limit_hit = 1;
+                ws->stop = 1;
+            }
+            break;
+        }
+        bool backtrack = false;
+        if (optimizing) { // branch-and-bound shrink (:87-101), done by thread 0
+            if (tid == 0) {
+                int empty = 0;
+                long long bnd = bound;
+                bool hb = has_bound;
+                if (parallel) {
+                    hb = ld_volatile(&ws->has_bound) != 0;
+                    bnd = *reinterpret_cast<volatile long long*>(&ws->bound);
+                }
+                if (hb) {
+                    uint32_t* d = dom + (size_t)obj * W;
+                    const long long off = M.off[obj];
+                    const int lo = dom_first<W>(d), hi = dom_last<W>(d);
+                    const bool shrink = minimizing ? (off + hi >= bnd) : (off + lo <= bnd);
+                    if (shrink) {
+                        // minimise: remove_above(bound-1) ; maximise: remove_below(bound+1)
+                        const long long cut = minimizing ? clampbit((i128)bnd - off, W * 32)
+                                                         : clampbit((i128)bnd - off, W * 32);
+                        uint32_t any = 0;
+#pragma unroll
+                        for (int w = 0; w < W; ++w) {
+                            uint32_t m = minimizing ? range_word(w, cut, W * 32) : range_word(w, -1, cut);
+                            d[w] &= ~m;
+                            any |= d[w];
+                        }
+                        empty = any == 0;
+                    }
+                }
+                s_flag = empty;
+            }
+            __syncthreads();
+            backtrack = s_flag != 0;
+            if (backtrack) ++failures;
+        }
+        if (!backtrack) {
+            int r = 0;
+            const int st = block_fixpoint<W>(M, R, &s_err, &s_min, 0, &r, nullptr);
+            rounds += (unsigned long long)r;
+            if (st == R_ERROR) {
+                if (tid == 0) {
+                    ws->error = DERR_OVERFLOW;
+                    ws->stop = 1;
+                }
+                break;
+            }
+            if (st == R_FAILED) {
+                ++failures;
+                backtrack = true;
+            }
+        }
+        if (!backtrack) {
+            const int sel = select_var<W>(M, dom, P.var_heuristic, s_red);
+            if (sel < 0) {
+                // ============ solution leaf (emit_solution, search.cpp:134-156)
+                if (tid == 0) s_ll = parallel ? (long long)atomicAdd((unsigned long long*)&ws->sol_count, 1ull) : (long long)sols;
+                __syncthreads();
+                const unsigned long long idx = (unsigned long long)s_ll;
+                ++sols;
+                if (P.record && idx < P.sol_cap) {
+                    for (int v = tid; v < n; v += T) P.sol_vals[idx * n + v] = (uint16_t)dom_first<W>(dom + (size_t)v * W);
+                    for (int i = tid; i < KW; i += T) P.sol_keys[idx * KW + i] = path[i];
+                    if (tid == 0 && !parallel) {
+                        P.sol_stats[idx * 3 + 0] = nodes;
+                        P.sol_stats[idx * 3 + 1] = failures;
+                        P.sol_stats[idx * 3 + 2] = rounds;
+                    }
+                }
+                if (parallel && KW > 0) { // per-context DFS-first solution
+                    if (tid == 0) {
+                        int less = 0;
+                        for (int i = 0; i < KW; ++i)
+                            if (path[i] != bestkey[i]) {
+                                less = path[i] < bestkey[i];
+                                break;
+                            }
+                        s_flag = less || !has_first;
+                    }
+                    __syncthreads();
+                    if (s_flag) {
+                        has_first = true;
+                        for (int i = tid; i < KW; i += T) {
+                            bestkey[i] = path[i];
+                            P.ctx_first_key[(size_t)ctx * KW + i] = path[i];
+                        }
+                        for (int v = tid; v < n; v += T)
+                            P.ctx_first_vals[(size_t)ctx * n + v] = (uint16_t)dom_first<W>(dom + (size_t)v * W);
+                        if (tid == 0) P.ctx_has_first[ctx] = 1;
+                    }
+                }
+                if (optimizing) {
+                    const long long val = M.off[obj] + dom_first<W>(dom + (size_t)obj * W);
+                    has_bound = true;
+                    bound = val;
+                    if (parallel && tid == 0) {
+                        spin_lock(&ws->inc_lock);
+                        volatile long long* gb = reinterpret_cast<volatile long long*>(&ws->bound);
+                        volatile int32_t* ghb = &ws->has_bound;
+                        if (!*ghb || (minimizing ? val < *gb : val > *gb)) {
+                            for (int v = 0; v < n; ++v) P.inc_vals[v] = (uint16_t)dom_first<W>(dom + (size_t)v * W);
+                            *gb = val;
+                            __threadfence();
+                            *ghb = 1;
+                        }
+                        spin_unlock(&ws->inc_lock);
+                    }
+                }
+                __syncthreads();
+                if (!parallel && sols >= P.max_solutions) {
+                    if (tid == 0) {
+                        ws->user_stop = 1;
+                        ws->stop = 1;
+                    }
+                    break;
+                }
+                backtrack = true;
+            } else {
+                // ============ left branch: push the frame, assign x = min(x) (:116-121)
+                if (sp >= P.frame_cap) {
+                    if (tid == 0) {
+                        ws->error = DERR_CAPACITY;
+                        ws->stop = 1;
+                    }
+                    break;
+                }
+                const int bit = dom_first<W>(dom + (size_t)sel * W);
+                copy4(frames + (size_t)sp * NWP, dom, NWP);
+                if (tid == 0) {
+                    meta[sp * 4 + 0] = sel;
+                    meta[sp * 4 + 1] = bit;
+                    meta[sp * 4 + 2] = depth;
+                }
+                __syncthreads();
+                if (tid < W) dom[(size_t)sel * W + tid] = (tid == (bit >> 5)) ? (1u << (bit & 31)) : 0u;
+                ++sp;
+                ++depth;
+                if (parallel) {
+                    // donate the shallowest pending right branch when someone is idle
+                    if (tid == 0) {
+                        int want = ld_volatile(&ws->stop) ? 2 : 0;
+                        if (!want && sp > base && !ld_volatile(&P.outbox_busy[ctx]) &&
+                            ld_volatile(&ws->n_idle) > ld_volatile(&ws->q_count))
+                            want = 1;
+                        s_flag = want;
+                    }
+                    __syncthreads();
+                    const int want = s_flag;
+                    if (want == 2) break;
+                    if (want == 1) {
+                        const int f = base++;
+                        const int fvar = meta[f * 4 + 0], fbit = meta[f * 4 + 1], fdepth = meta[f * 4 + 2];
+                        uint32_t* ob = P.outbox + (size_t)ctx * OS;
+                        const uint32_t* fr = frames + (size_t)f * NWP;
+                        const size_t clr = (size_t)fvar * W + (fbit >> 5);
+                        for (size_t i = tid; i < NWP; i += T) {
+                            uint32_t x = fr[i];
+                            if (i == clr) x &= ~(1u << (fbit & 31));
+                            ob[i] = x;
+                        }
+                        for (int i = tid; i < KW; i += T) {
+                            const int lo = i * 32;
+                            uint32_t x = path[i];
+                            uint32_t keep = fdepth >= lo + 32 ? 0xffffffffu : (fdepth <= lo ? 0u : ((1u << (fdepth - lo)) - 1u));
+                            x &= keep;
+                            if (fdepth >= lo && fdepth < lo + 32) x |= 1u << (fdepth - lo);
+                            ob[NWP + i] = x;
+                        }
+                        if (tid == 0) ob[NWP + KW] = (uint32_t)(fdepth + 1);
+                        __syncthreads();
+                        if (tid == 0) {
+                            __threadfence();
+                            P.outbox_busy[ctx] = 1;
+                            atomicAdd(&ws->outstanding, 1);
+                            spin_lock(&ws->lock);
+                            volatile int32_t* qc = &ws->q_count;
+                            const int k = *qc;
+                            reinterpret_cast<volatile int32_t*>(P.queue)[k] = ctx;
+                            *qc = k + 1;
+                            spin_unlock(&ws->lock);
+                            atomicAdd((unsigned long long*)&ws->donations, 1ull);
+                        }
+                    }
+                }
+                __syncthreads();
+                continue;
+            }
+        }
+        // ================= backtrack: right branch of the deepest pending frame (:122-131)
+        if (sp == base) {
+            if (!parallel) break;
+            __syncthreads();
+            have_work = get_work();
+            __syncthreads();
+            continue;
+        }
+        --sp;
+        copy4(dom, frames + (size_t)sp * NWP, NWP);
+        const int var = meta[sp * 4 + 0], bit = meta[sp * 4 + 1], d = meta[sp * 4 + 2];
+        __syncthreads();
+        if (tid == 0) {
+            dom[(size_t)var * W + (bit >> 5)] &= ~(1u << (bit & 31));
+            if (KW > 0) { // path: bit d = 1, everything deeper cleared
+                const int last = depth < KW * 32 ? depth : KW * 32 - 1;
+                for (int i = d >> 5; i <= (last >> 5); ++i) {
+                    const int lo = i * 32;
+                    uint32_t keep = d >= lo + 32 ? 0xffffffffu : (d <= lo ? 0u : ((1u << (d - lo)) - 1u));
+                    uint32_t x = path[i] & keep;
+                    if (d >= lo && d < lo + 32) x |= 1u << (d - lo);
+                    path[i] = x;
+                }
+            }
+        }
+        depth = d + 1;
+        __syncthreads();
+    }
+    __syncthreads();
+    if (parallel && tid == 0 && have_work) {
+        // unwound by stop: this context no longer counts as outstanding
+        atomicSub(&ws->outstanding, 1);
+    }
+    if (tid == 0) {
+        atomicAdd((unsigned long long*)&ws->stats[0], nodes);
+        atomicAdd((unsigned long long*)&ws->stats[1], failures);
+        atomicAdd((unsigned long long*)&ws->stats[2], rounds);
+        atomicAdd((unsigned long long*)&ws->stats[3], sols);
+    }
+}
+
+// cubics_propagate / cubics_removals: one block over caller-provided domains
+template <int W>
+__global__ void __launch_bounds__(1024) propagate_kernel(const PropParams P, uint32_t* gscratch, int dom_in_smem) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ int s_err, s_min;
+    const DevModel& M = P.M;
+    const int tid = threadIdx.x, T = blockDim.x, nw = T >> 5;
+    const size_t NW = (size_t)M.n * W, NWP = round4(NW);
+    const SmemLayout L = smem_layout(W, M.n, M.total_members, nw, 0, dom_in_smem);
+    uint32_t* dom = dom_in_smem ? reinterpret_cast<uint32_t*>(smem + L.dom) : gscratch;
+    uint32_t* rm = dom_in_smem ? reinterpret_cast<uint32_t*>(smem + L.rm) : gscratch + NWP;
+    int16_t* mates = reinterpret_cast<int16_t*>(smem + L.mates);
+    RoundCtx R{dom, rm, mates, smem + L.scratch, L.stride, P.enabled, P.alldiff, 1};
+    for (size_t i = tid; i < NWP; i += T) {
+        dom[i] = P.dom[i];
+        rm[i] = 0;
+    }
+    for (int i = tid; i < M.total_members; i += T) mates[i] = -1;
+    if (tid == 0) s_err = 0;
+    __syncthreads();
+    if (P.removals_only) {
+        run_propagators<W>(M, R, &s_err);
+        __syncthreads();
+        for (size_t i = tid; i < NWP; i += T) P.out[i] = rm[i] & dom[i];
+        if (tid == 0) P.result[4] = s_err;
+        return;
+    }
+    int rounds = 0, fv = -1;
+    const int st = block_fixpoint<W>(M, R, &s_err, &s_min, P.max_rounds, &rounds, &fv);
+    for (size_t i = tid; i < NWP; i += T) P.dom[i] = dom[i];
+    if (tid == 0) {
+        P.result[0] = st == R_FAILED;
+        P.result[1] = st == R_FAILED ? fv : -1;
+        P.result[2] = rounds;
+        P.result[3] = st == R_ERROR ? 0 : st;
+        P.result[4] = s_err;
+    }
+}
+
+} // namespace dev
+} // namespace cubics

@@ -1,0 +1,447 @@
+"""Python mirror of the reference solver interface (proj/include/fd/*.hpp) over libcubics.so.
+
+Names, argument meaning and error behaviour follow the reference so the parity tests read like
+the reference's own tests:
+
+    fd::parse_model          -> parse_model(text)               (parser.hpp:38)
+    fd::model_validate       -> Model.validate()                (model.hpp:93)
+    fd::solve_satisfy        -> solve_satisfy(model, cfg, cb)   (search.hpp:62)
+    fd::enumerate_solutions  -> enumerate_solutions(model, cfg) (search.hpp:65)
+    fd::solve_optimize       -> solve_optimize(model, cfg)      (search.hpp:77)
+    fd::propagate_fixpoint   -> propagate_fixpoint(model, doms) (propagation.hpp:114)
+    fd::propagate_round      -> propagate_round(model, doms)    (propagation.hpp:102)
+    fd::run_batch / prop_*   -> removals(model, doms, cons)     (propagation.hpp:78-89)
+
+Errors are raised as the reference's exception types: ArithmeticOverflowError
+(model.hpp:99-101), ValueError for a parse error, LogicError (std::logic_error) when optimising
+without an objective. The CUDA engine is the only implementation: if libcubics.so is missing or
+no B200 is present, calls raise EngineUnavailable - there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+from . import _abi as A
+
+
+class EngineUnavailable(RuntimeError):
+    """libcubics.so is not built or no usable sm_100 device is present."""
+
+
+class ArithmeticOverflowError(RuntimeError):
+    """fd::ArithmeticOverflowError (model.hpp:99-101)."""
+
+
+class LogicError(RuntimeError):
+    """std::logic_error raised by fd::solve_optimize without an objective (search.cpp:192)."""
+
+
+class CapacityError(RuntimeError):
+    pass
+
+
+class UnsupportedInstance(RuntimeError):
+    pass
+
+
+_LIB = None
+
+
+def lib():
+    """Load the in-tree libcubics.so (built by __graft_entry__.build())."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(A.LIB_PATH):
+            raise EngineUnavailable(f"{A.LIB_PATH} is not built; run __graft_entry__.build()")
+        _LIB = A.declare(C.CDLL(A.LIB_PATH))
+    return _LIB
+
+
+def _check(rc, what=""):
+    if rc == A.OK:
+        return
+    msg = (lib().cubics_last_error() or b"").decode()
+    if rc == A.E_OVERFLOW:
+        raise ArithmeticOverflowError(msg)
+    if rc == A.E_NO_OBJECTIVE:
+        raise LogicError(msg)
+    if rc == A.E_CUDA:
+        raise EngineUnavailable(msg)
+    if rc == A.E_CAPACITY:
+        raise CapacityError(msg)
+    if rc == A.E_UNSUPPORTED:
+        raise UnsupportedInstance(msg)
+    raise ValueError(f"{what}: {A.STATUS_NAMES.get(rc, rc)}: {msg}")
+
+
+# ------------------------------------------------------------------ configuration / results
+@dataclass
+class SearchConfig:
+    """fd::SearchConfig (search.hpp:19-27) plus the engine selector."""
+    var_heuristic: int = A.FIRST_FAIL
+    value_heuristic: int = 0
+    max_solutions: int = A.UINT64_MAX
+    thread_count: int = 1
+    seed: int = 0
+    alldiff: int = A.ARC_CONSISTENT
+    node_limit: int = 0
+    engine: int = A.ENGINE_AUTO
+    device: int = -1
+    contexts: int = 0
+    block_threads: int = 0
+    count_only: bool = False
+
+    def to_c(self) -> A.SearchConfig:
+        c = A.SearchConfig()
+        for f in ("var_heuristic", "value_heuristic", "max_solutions", "thread_count", "seed", "alldiff",
+                  "node_limit", "engine", "device", "contexts", "block_threads"):
+            setattr(c, f, getattr(self, f))
+        c.count_only = 1 if self.count_only else 0
+        return c
+
+
+@dataclass
+class SearchStats:
+    nodes: int = 0
+    failures: int = 0
+    rounds: int = 0
+    solutions: int = 0
+
+    def as_tuple(self):
+        return (self.nodes, self.failures, self.rounds, self.solutions)
+
+
+@dataclass
+class SatisfyResult:
+    stats: SearchStats
+    complete: bool
+    engine: int = 0
+    contexts: int = 1
+    device_ms: float = 0.0
+    total_ms: float = 0.0
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
+    kernel_launches: int = 0
+
+
+@dataclass
+class Solution:
+    values: list
+    objective: int | None = None
+
+
+@dataclass
+class OptimizeResult:
+    best: Solution | None
+    complete: bool
+    stats: SearchStats
+    engine: int = 0
+    contexts: int = 1
+    device_ms: float = 0.0
+    total_ms: float = 0.0
+
+
+@dataclass
+class FixpointResult:
+    failed: bool
+    failed_var: int
+    rounds: int
+    last_status: int = 1  # fd::RoundResult::Status: 0 Changed, 1 Stable, 2 Failed
+
+
+def _stats(r: A.Result) -> SearchStats:
+    return SearchStats(r.stats.nodes, r.stats.failures, r.stats.rounds, r.stats.solutions)
+
+
+# ------------------------------------------------------------------ model
+class Domain:
+    """A value set [offset, offset+width) as a Python int bitmask (bit i = offset + i)."""
+
+    __slots__ = ("offset", "width", "bits")
+
+    def __init__(self, lo: int, hi: int | None = None, bits: int | None = None, width: int | None = None):
+        if hi is not None:
+            if lo > hi:
+                raise ValueError("empty range")
+            if hi - lo >= 1024:
+                raise ValueError("width exceeded")
+            self.offset, self.width = lo, hi - lo + 1
+            self.bits = (1 << self.width) - 1
+        else:
+            self.offset, self.width = lo, width
+            self.bits = bits & ((1 << width) - 1)
+
+    def values(self):
+        b, out, i = self.bits, [], 0
+        while b:
+            if b & 1:
+                out.append(self.offset + i)
+            b >>= 1
+            i += 1
+        return out
+
+    def size(self):
+        return bin(self.bits).count("1")
+
+    def empty(self):
+        return self.bits == 0
+
+    def contains(self, v):
+        i = v - self.offset
+        return 0 <= i < self.width and (self.bits >> i) & 1 == 1
+
+    def remove(self, v):
+        if self.contains(v):
+            self.bits &= ~(1 << (v - self.offset))
+
+    def copy(self):
+        return Domain(self.offset, bits=self.bits, width=self.width)
+
+    def __eq__(self, o):
+        return (self.offset, self.width, self.bits) == (o.offset, o.width, o.bits)
+
+    def __repr__(self):
+        return f"Domain({self.values()})"
+
+    def words(self):
+        nw = (self.width + 63) // 64
+        return [(self.bits >> (64 * i)) & ((1 << 64) - 1) for i in range(nw)]
+
+
+class Model:
+    """Owning handle of a cubics_model (fd::Model)."""
+
+    def __init__(self, handle):
+        self._h = handle
+        d = A.ModelDesc()
+        _check(lib().cubics_model_describe(self._h, C.byref(d)), "describe")
+        self.n_vars = d.n_vars
+        self.n_cons = d.n_cons
+        self.goal = d.goal
+        self.goal_var = d.goal_var
+        self.offsets = [d.var_offset[i] for i in range(self.n_vars)]
+        self.widths = [d.var_width[i] for i in range(self.n_vars)]
+        self.word_start = [0]
+        for w in self.widths:
+            self.word_start.append(self.word_start[-1] + (w + 63) // 64)
+        words = [d.var_words[i] for i in range(self.word_start[-1])]
+        self.domains = []
+        for v in range(self.n_vars):
+            bits = 0
+            for i, x in enumerate(words[self.word_start[v]:self.word_start[v + 1]]):
+                bits |= x << (64 * i)
+            self.domains.append(Domain(self.offsets[v], bits=bits, width=self.widths[v]))
+        self.con_kind = [d.con_kind[i] for i in range(self.n_cons)]
+        self.con_op = [d.con_op[i] for i in range(self.n_cons)]
+        self.con_value = [d.con_value[i] for i in range(self.n_cons)]
+        self.con_start = [d.con_start[i] for i in range(self.n_cons + 1)]
+        nt = self.con_start[-1] if self.n_cons else 0
+        self.term_var = [d.term_var[i] for i in range(nt)]
+        self.term_coeff = [d.term_coeff[i] for i in range(nt)] if nt else []
+        self.names = [lib().cubics_model_var_name(self._h, i).decode() for i in range(self.n_vars)]
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h and _LIB is not None:
+            _LIB.cubics_model_free(h)
+
+    def validate(self):
+        """fd::model_validate: list of (kind, constraint_index); empty = valid."""
+        cnt = C.c_int32(0)
+        buf = (A.Diagnostic * 256)()
+        _check(lib().cubics_model_validate(self._h, buf, 256, C.byref(cnt)), "validate")
+        return [(buf[i].kind, buf[i].constraint_index) for i in range(min(cnt.value, 256))]
+
+    def desc_arrays(self):
+        """Flat arrays for building a cubics_model_desc (keeps them alive in the returned dict)."""
+        return build_desc(self.offsets, self.widths, self.domains, self.con_kind, self.con_op, self.con_value,
+                          self.con_start, self.term_var, self.term_coeff, self.goal, self.goal_var)
+
+    def words_of(self, domains):
+        out = (C.c_uint64 * max(1, self.word_start[-1]))()
+        for v, d in enumerate(domains):
+            for i, x in enumerate(d.words()):
+                out[self.word_start[v] + i] = x
+        return out
+
+    def domains_of(self, words):
+        doms = []
+        for v in range(self.n_vars):
+            bits = 0
+            for i in range(self.word_start[v + 1] - self.word_start[v]):
+                bits |= int(words[self.word_start[v] + i]) << (64 * i)
+            doms.append(Domain(self.offsets[v], bits=bits, width=self.widths[v]))
+        return doms
+
+    def with_goal(self, goal, var):
+        arr = self.desc_arrays()
+        arr["desc"].goal = goal
+        arr["desc"].goal_var = var
+        return model_from_desc(arr["desc"])
+
+    def with_domains(self, domains):
+        arr = build_desc(self.offsets, self.widths, domains, self.con_kind, self.con_op, self.con_value,
+                         self.con_start, self.term_var, self.term_coeff, self.goal, self.goal_var)
+        return model_from_desc(arr["desc"])
+
+
+def build_desc(offsets, widths, domains, kinds, ops, values, starts, tvars, tcoeffs, goal=A.SATISFY, goal_var=0):
+    n, m = len(offsets), len(kinds)
+    nt = starts[-1] if m else 0
+    ws = [0]
+    for w in widths:
+        ws.append(ws[-1] + (w + 63) // 64)
+    keep = {
+        "off": (C.c_int64 * max(1, n))(*offsets),
+        "width": (C.c_int32 * max(1, n))(*widths),
+        "words": (C.c_uint64 * max(1, ws[-1]))(),
+        "kind": (C.c_int32 * max(1, m))(*kinds),
+        "op": (C.c_int32 * max(1, m))(*ops),
+        "value": (C.c_int64 * max(1, m))(*values),
+        "start": (C.c_int32 * (m + 1))(*(starts if m else [0])),
+        "tvar": (C.c_int32 * max(1, nt))(*tvars),
+        "tcoeff": (C.c_int64 * max(1, nt))(*(tcoeffs or [1] * nt)),
+    }
+    for v, d in enumerate(domains):
+        for i, x in enumerate(d.words()):
+            keep["words"][ws[v] + i] = x
+    d = A.ModelDesc()
+    d.n_vars = n
+    d.var_offset = keep["off"]
+    d.var_width = keep["width"]
+    d.var_words = keep["words"]
+    d.n_cons = m
+    d.con_kind = keep["kind"]
+    d.con_op = keep["op"]
+    d.con_value = keep["value"]
+    d.con_start = keep["start"]
+    d.term_var = keep["tvar"]
+    d.term_coeff = keep["tcoeff"]
+    d.goal = goal
+    d.goal_var = goal_var
+    keep["desc"] = d
+    return keep
+
+
+def model_from_desc(desc: A.ModelDesc) -> Model:
+    h = C.c_void_p()
+    _check(lib().cubics_model_create(C.byref(desc), C.byref(h)), "model_create")
+    return Model(h.value)
+
+
+def parse_model(text: str) -> Model:
+    """fd::parse_model; raises ValueError(message) with the reference's line/column format."""
+    h = C.c_void_p()
+    err = A.ParseError()
+    raw = text.encode()
+    rc = lib().cubics_model_parse(raw, len(raw), C.byref(h), C.byref(err))
+    if rc == A.E_PARSE:
+        e = ValueError(err.message.decode())
+        e.kind, e.line, e.column = err.kind, err.line, err.column
+        raise e
+    _check(rc, "parse")
+    return Model(h.value)
+
+
+# ------------------------------------------------------------------ search
+def solve_satisfy(model: Model, cfg: SearchConfig | None = None, cb=None) -> SatisfyResult:
+    """fd::solve_satisfy: cb(Solution) -> bool is called per solution in the reference's DFS order."""
+    cfg = cfg or SearchConfig()
+    user_err = []
+
+    def trampoline(_user, vals, n):
+        try:
+            keep = cb(Solution([vals[i] for i in range(n)]))
+            return 1 if keep else 0
+        except BaseException as e:  # noqa: BLE001 - re-raised below
+            user_err.append(e)
+            return 0
+
+    cfun = A.SOLUTION_CB(trampoline) if cb else A.SOLUTION_CB()
+    res = A.Result()
+    c = cfg.to_c()
+    _check(lib().cubics_solve_satisfy(model.handle, C.byref(c), cfun, None, C.byref(res)), "solve_satisfy")
+    if user_err:
+        raise user_err[0]
+    return SatisfyResult(_stats(res), bool(res.complete), res.engine, res.contexts, res.device_ms, res.total_ms,
+                         res.h2d_bytes, res.d2h_bytes, res.kernel_launches)
+
+
+def enumerate_solutions(model: Model, cfg: SearchConfig | None = None, stats: SearchStats | None = None):
+    """fd::enumerate_solutions: every solution (values lists) in DFS order."""
+    out = []
+    r = solve_satisfy(model, cfg, lambda s: out.append(s) or True)
+    if stats is not None:
+        stats.nodes, stats.failures, stats.rounds, stats.solutions = r.stats.as_tuple()
+    return out
+
+
+def solve_optimize(model: Model, cfg: SearchConfig | None = None) -> OptimizeResult:
+    """fd::solve_optimize (branch and bound)."""
+    cfg = cfg or SearchConfig()
+    res = A.Result()
+    best = (C.c_int64 * max(1, model.n_vars))()
+    c = cfg.to_c()
+    _check(lib().cubics_solve_optimize(model.handle, C.byref(c), best, C.byref(res)), "solve_optimize")
+    sol = None
+    if res.has_solution:
+        sol = Solution([best[i] for i in range(model.n_vars)], res.objective)
+    return OptimizeResult(sol, bool(res.complete), _stats(res), res.engine, res.contexts, res.device_ms, res.total_ms)
+
+
+def solve_shard(model: Model, cfg: SearchConfig, shard_index: int, shard_count: int, cb=None):
+    """One rank's share of a multi-GPU search (cubics_solve_shard); cb(key_words, values)."""
+    def trampoline(_u, key, kw, vals, n):
+        return 1 if cb([key[i] for i in range(kw)], [vals[i] for i in range(n)]) else 0
+
+    cfun = A.KEYED_SOLUTION_CB(trampoline) if cb else A.KEYED_SOLUTION_CB()
+    res = A.Result()
+    c = cfg.to_c()
+    _check(lib().cubics_solve_shard(model.handle, C.byref(c), shard_index, shard_count, cfun, None, C.byref(res)),
+           "solve_shard")
+    return SatisfyResult(_stats(res), bool(res.complete), res.engine, res.contexts, res.device_ms, res.total_ms,
+                         res.h2d_bytes, res.d2h_bytes, res.kernel_launches)
+
+
+# ------------------------------------------------------------------ propagation
+def propagate_fixpoint(model: Model, domains=None, alldiff=A.ARC_CONSISTENT, max_rounds=0):
+    """fd::propagate_fixpoint over `domains` (default: the model's); returns (domains, FixpointResult)."""
+    doms = domains if domains is not None else model.domains
+    words = model.words_of(doms)
+    fr = A.FixpointResult()
+    _check(lib().cubics_propagate(model.handle, words, alldiff, max_rounds, C.byref(fr)), "propagate")
+    return model.domains_of(words), FixpointResult(bool(fr.failed), fr.failed_var, fr.rounds, fr.last_status)
+
+
+def propagate_round(model: Model, domains=None, alldiff=A.ARC_CONSISTENT):
+    """fd::propagate_round: one bulk-synchronous round; returns (domains, status, failed_var)."""
+    doms, fr = propagate_fixpoint(model, domains, alldiff, max_rounds=1)
+    return doms, fr.last_status, fr.failed_var
+
+
+def removals(model: Model, domains=None, cons=None, alldiff=A.ARC_CONSISTENT):
+    """fd::run_batch / propagate_one: per-var removed value lists against the snapshot."""
+    doms = domains if domains is not None else model.domains
+    words = model.words_of(doms)
+    out = (C.c_uint64 * max(1, model.word_start[-1]))()
+    if cons is None:
+        rc = lib().cubics_removals(model.handle, words, alldiff, None, 0, out)
+    else:
+        arr = (C.c_int32 * max(1, len(cons)))(*cons)
+        rc = lib().cubics_removals(model.handle, words, alldiff, arr, len(cons), out)
+    _check(rc, "removals")
+    return [d.values() for d in model.domains_of(out)]
+
+
+def device_count() -> int:
+    return lib().cubics_device_count()
+
+
+def build_info() -> str:
+    return lib().cubics_build_info().decode()
