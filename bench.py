@@ -1,0 +1,272 @@
+"""Benchmark: search nodes/s and time-to-all-solutions, N-Queens n=14 all solutions (BASELINE.json
+configs[1]), on B200 through the C ABI, beside the reference CPU solver.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--instance nq14]
+
+One step = one complete all-solutions search of the instance (4,864,749 nodes for nq14).
+value   = nodes / device time of the search kernel (CUDA events on the launching stream),
+          max over ranks for N > 1, whole-job aggregate.
+e2e     = the same metric through cubics_solve_satisfy with host buffers: model upload, search,
+          and the download of every solution (365,596 x 14 values) inside the timed region.
+Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+METRIC = "search nodes/sec and time-to-all-solutions at 1/2/4/8 B200 vs CPU ref"
+REF_DRIVER = os.path.join(ROOT, "oracle", "_ref", "fdref_driver")
+MODELS = os.path.join(ROOT, "tests", "golden", "models")
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback"
+
+
+def algorithmic_bytes(model, stats):
+    """A = rounds*(4*S + 8*V) + nodes*(4*V), W_v = ceil(width_v/32) u32 words."""
+    wv = [(w + 31) // 32 for w in model.widths]
+    V = sum(wv)
+    S_ = 0
+    for c in range(model.n_cons):
+        scope = set(model.term_var[model.con_start[c]:model.con_start[c + 1]])
+        S_ += sum(wv[v] for v in scope)
+    return stats.rounds * (4 * S_ + 8 * V) + stats.nodes * (4 * V), S_, V
+
+
+class ClockSampler:
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, gpu):
+        self.gpu, self.samples, self.proc = gpu, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(int(float(s[0])) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max(int(float(s[1])) for s in self.samples if s[1].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i] == "Active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def run_reference(path, flags, threads=1, timeout=3600):
+    import resource
+
+    def lim():
+        resource.setrlimit(resource.RLIMIT_STACK, (resource.RLIM_INFINITY, resource.RLIM_INFINITY))
+
+    r = subprocess.run([REF_DRIVER, "solve", path, "--threads", str(threads)] + flags, capture_output=True,
+                       text=True, timeout=timeout, preexec_fn=lim)
+    if r.returncode != 0:
+        raise RuntimeError(r.stderr)
+    return json.loads(r.stdout)
+
+
+def cpu_sample(instance, node_limit, threads):
+    out = run_reference(os.path.join(MODELS, instance + ".fd"), ["--all", "--node-limit", str(node_limit)], threads)
+    return out["nodes"] / (out["time_ms"] / 1e3), out
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def impl_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    if not os.path.exists(REF_DRIVER):
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/fdref_driver not built"}))
+        return 0
+    nproc = os.cpu_count() or 1
+    # bounded sample of the same workload: the first N nodes of the nq14 all-solutions DFS
+    limit = args.ref_node_limit
+    # the reference's only parallel knob (OpenMP propagation) slows this workload down
+    # (SURVEY.md 2.3); pick whichever of 1 / nproc threads is faster on a short probe
+    probe = {t: cpu_sample(args.instance, 20000, t)[0] for t in sorted({1, nproc})}
+    threads = max(probe, key=probe.get)
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, out = cpu_sample(args.instance, limit, threads)
+        if i >= args.warmup:
+            vals.append(v)
+    value = sum(vals) / len(vals)
+    line = {
+        "metric": METRIC, "impl": "reference", "value": value, "unit": "nodes/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": limit / value * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic", "config": {"workload": f"{args.instance} all solutions", "sample": f"first {limit} DFS nodes"},
+        "cpu_baseline": {"value": value, "unit": "nodes/s", "cores": threads, "kind": "reference",
+                         "sample": f"first {limit} nodes of the {args.instance} all-solutions DFS, threads={threads}",
+                         "probe_nodes_per_s": probe},
+        "e2e": {"value": value, "unit": "nodes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def impl_ours(args):
+    from paper_1909_09213_b200 import _abi as A
+    from paper_1909_09213_b200 import solver as S
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    device = local if world > 1 else 0
+    text = open(os.path.join(MODELS, args.instance + ".fd")).read()
+    model = S.parse_model(text)
+    cfg = S.SearchConfig(engine=A.ENGINE_PARALLEL, device=device, count_only=True, contexts=args.contexts,
+                         block_threads=args.block)
+
+    def one_step(count_only=True):
+        c = S.SearchConfig(**{**cfg.__dict__, "count_only": count_only})
+        if world > 1:
+            return S.solve_shard(model, c, rank, world)
+        return S.solve_satisfy(model, c, (lambda s: True) if not count_only else None)
+
+    for _ in range(args.warmup):
+        one_step()
+    if world > 1:
+        dist.barrier()
+    stats0 = None
+    dev_ms = []
+    with ClockSampler(device) as clk:
+        for _ in range(args.steps):
+            r = one_step()
+            dev_ms.append(r.device_ms)
+            stats0 = r.stats
+    # e2e: through the public C ABI with host buffers; every solution is copied back and
+    # delivered to the callback in DFS order
+    e2e_ms, h2d, d2h = [], 0, 0
+    for _ in range(max(1, min(args.steps, 3))):
+        t0 = time.perf_counter()
+        cnt = [0]
+
+        def cb(_s, cnt=cnt):
+            cnt[0] += 1
+            return True
+
+        r2 = S.solve_satisfy(model, S.SearchConfig(**{**cfg.__dict__, "count_only": False}), cb)
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        h2d, d2h = r2.h2d_bytes, r2.d2h_bytes
+        assert cnt[0] == r2.stats.solutions
+    ms = max(dev_ms) if dev_ms else 0.0
+    nodes = stats0.nodes
+    if world > 1:
+        t = torch.tensor([ms, nodes], dtype=torch.float64, device=f"cuda:{local}")
+        mx = t.clone()
+        dist.all_reduce(mx[0:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(t[1:2], op=dist.ReduceOp.SUM)
+        ms, nodes = float(mx[0]), int(t[1])
+    if rank != 0:
+        return 0
+    mean_ms = sum(dev_ms) / len(dev_ms)
+    value = nodes / (mean_ms / 1e3)
+    A_bytes, S_, V = algorithmic_bytes(model, stats0)
+    peak, peak_kind = load_peaks()
+    achieved = A_bytes / (mean_ms / 1e3) / 1e9
+    # CPU baseline: the unmodified reference on this host, bounded sample
+    cpu = None
+    if os.path.exists(REF_DRIVER) and not args.no_cpu:
+        v, out = cpu_sample(args.instance, args.cpu_node_limit, 1)
+        cpu = {"value": v, "unit": "nodes/s", "cores": 1, "kind": "reference",
+               "sample": f"first {args.cpu_node_limit} nodes of the {args.instance} all-solutions DFS "
+                         f"(oracle/_ref/fdref_driver, thread_count=1, {out['time_ms']:.0f} ms)"}
+    e2e_best = min(e2e_ms)
+    line = {
+        "metric": METRIC, "value": value, "unit": "nodes/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": mean_ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": f"{args.instance} all solutions (N-Queens n=14, BASELINE configs[1])",
+                   "engine": "parallel", "contexts": r.contexts, "l2": "working set < L2; no flush needed"
+                   " (each step is a full search, the state is re-uploaded)",
+                   "stats": {"nodes": stats0.nodes, "failures": stats0.failures, "rounds": stats0.rounds,
+                             "solutions": stats0.solutions}},
+        "time_to_all_solutions_ms": mean_ms,
+        "e2e": {"value": nodes / (e2e_best / 1e3), "unit": "nodes/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "time_to_all_solutions_ms": e2e_best},
+        "gpu_launches": r.kernel_launches,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                     "algorithmic_bytes": A_bytes, "S_words": S_, "V_words": V,
+                     "note": "latency/barrier-bound search; A from SURVEY 8(d)"},
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--instance", default="nq14")
+    ap.add_argument("--contexts", type=int, default=0)
+    ap.add_argument("--block", type=int, default=0)
+    ap.add_argument("--cpu-node-limit", type=int, default=400000)
+    ap.add_argument("--ref-node-limit", type=int, default=200000)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return impl_reference(args)
+    return impl_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -50,6 +50,18 @@ __device__ __forceinline__ void copy4_cg(uint32_t* dst, const uint32_t* src, siz
     for (size_t i = threadIdx.x; i < nwords / 4; i += blockDim.x) d[i] = __ldcg(s + i);
 }
 
+// DFS path key: decision at depth d is bit (31 - d%32) of word d/32, so comparing the words as
+// unsigned integers, most significant first, is the reference's DFS (preorder) order.
+// path_right_word: word i of the key of the right child taken at depth d (prefix [0,d) kept,
+// bit d set, deeper bits cleared).
+__device__ __forceinline__ uint32_t path_right_word(uint32_t word, int i, int d) {
+    const int c = d - i * 32; // prefix bits of this word that are kept
+    uint32_t keep = c <= 0 ? 0u : (c >= 32 ? 0xffffffffu : ~(0xffffffffu >> c));
+    uint32_t x = word & keep;
+    if (c >= 0 && c < 32) x |= 0x80000000u >> c;
+    return x;
+}
+
 // block argmin of (size, id) over unbound vars; -1 when every domain is a singleton
 template <int W>
 __device__ __forceinline__ int select_var(const DevModel& M, const uint32_t* dom, int first_fail, unsigned* s_red) {
@@ -337,14 +349,7 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
                             if (i == clr) x &= ~(1u << (fbit & 31));
                             ob[i] = x;
                         }
-                        for (int i = tid; i < KW; i += T) {
-                            const int lo = i * 32;
-                            uint32_t x = path[i];
-                            uint32_t keep = fdepth >= lo + 32 ? 0xffffffffu : (fdepth <= lo ? 0u : ((1u << (fdepth - lo)) - 1u));
-                            x &= keep;
-                            if (fdepth >= lo && fdepth < lo + 32) x |= 1u << (fdepth - lo);
-                            ob[NWP + i] = x;
-                        }
+                        for (int i = tid; i < KW; i += T) ob[NWP + i] = path_right_word(path[i], i, fdepth);
                         if (tid == 0) ob[NWP + KW] = (uint32_t)(fdepth + 1);
                         __syncthreads();
                         if (tid == 0) {
@@ -381,13 +386,7 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
             dom[(size_t)var * W + (bit >> 5)] &= ~(1u << (bit & 31));
             if (KW > 0) { // path: bit d = 1, everything deeper cleared
                 const int last = depth < KW * 32 ? depth : KW * 32 - 1;
-                for (int i = d >> 5; i <= (last >> 5); ++i) {
-                    const int lo = i * 32;
-                    uint32_t keep = d >= lo + 32 ? 0xffffffffu : (d <= lo ? 0u : ((1u << (d - lo)) - 1u));
-                    uint32_t x = path[i] & keep;
-                    if (d >= lo && d < lo + 32) x |= 1u << (d - lo);
-                    path[i] = x;
-                }
+                for (int i = d >> 5; i <= (last >> 5); ++i) path[i] = path_right_word(path[i], i, d);
             }
         }
         depth = d + 1;

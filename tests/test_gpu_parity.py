@@ -1,0 +1,215 @@
+"""Parity of the CUDA engine (through the C ABI) with the reference / the pinned oracle.
+
+Expectations come from the unmodified reference (tests/golden/*.json) or from the oracle port
+that tests/test_oracle.py pins to it. Bit-exact: stats, solutions, solution order, domains.
+"""
+import itertools
+
+import pytest
+
+import golden_cases as G
+import oracle_binding as O
+from paper_1909_09213_b200 import _abi as A
+from paper_1909_09213_b200 import models
+from paper_1909_09213_b200 import solver as S
+
+pytestmark = pytest.mark.gpu
+
+PARITY = A.ENGINE_PARITY
+PARALLEL = A.ENGINE_PARALLEL
+
+
+@pytest.fixture(scope="module", autouse=True)
+def engine_present():
+    # fail loudly (never skip) when the native engine is absent on a GPU box
+    assert S.device_count() >= 1, "no CUDA device visible to libcubics"
+
+
+def gpu_case(key, engine):
+    inst, flags = G.split_key(key)
+    m = S.parse_model(G.model_text(inst))
+    cfg = G.cfg_from_flags(flags)
+    cfg.engine = engine
+    if m.goal != 0:
+        r = S.solve_optimize(m, cfg)
+        return r.stats.as_tuple(), (r.best.values if r.best else None)
+    first = []
+    r = S.solve_satisfy(m, cfg, lambda s: (first.append(s.values) if not first else None) or True)
+    return r.stats.as_tuple(), (first[0] if first else None)
+
+
+@pytest.mark.parametrize("key", G.FAST_CASES + ["nq10|--all", "nq12|--all", "golomb9",
+                                                 "magic4|--all --node-limit 20000",
+                                                 "rcsp_100000|--max 1 --node-limit 200"])
+def test_parity_engine_matches_reference(key):
+    g = G.goldens()[key]
+    stats, sol = gpu_case(key, PARITY)
+    assert stats == G.expected_tuple(g)
+    assert sol == (g.get("best") if "best" in g else g.get("first"))
+
+
+@pytest.mark.parametrize("key", ["nq4|--all", "nq6|--all", "nq8|--all", "nq8|--all --fc", "nq8|--all --input",
+                                 "nq10|--all", "nq12|--all", "magic3|--all"])
+def test_parallel_engine_exact_on_complete_enumerations(key):
+    g = G.goldens()[key]
+    stats, sol = gpu_case(key, PARALLEL)
+    assert stats == G.expected_tuple(g)
+    assert sol == g["first"]
+
+
+def test_parallel_solution_stream_in_reference_order():
+    m = S.parse_model(G.model_text("nq8"))
+    expect = [s.values for s in O.enumerate_solutions(m)]
+    for eng in (PARITY, PARALLEL):
+        got = [s.values for s in S.enumerate_solutions(m, S.SearchConfig(engine=eng))]
+        assert got == expect
+
+
+def test_corpus_solutions_fixpoints_and_first():
+    c = G.corpus()["corpus"]
+    for seed in range(200):
+        rec = c[str(seed)]
+        m = S.parse_model(models.corpus_instance(seed))
+        for eng in (PARITY, PARALLEL):
+            st = S.SearchStats()
+            sols = S.enumerate_solutions(m, S.SearchConfig(engine=eng), st)
+            assert [s.values for s in sols] == rec["all"]["all"], (seed, eng)
+            assert st.as_tuple() == G.expected_tuple(rec["all"]), (seed, eng)
+        for name, cfg in (("all_fc", S.SearchConfig(alldiff=0)), ("all_input", S.SearchConfig(var_heuristic=0)),
+                          ("first", S.SearchConfig(max_solutions=1))):
+            st = S.SearchStats()
+            S.enumerate_solutions(m, cfg, st)
+            assert st.as_tuple() == G.expected_tuple(rec[name]), (seed, name)
+        for name, level in (("fix_gac", 1), ("fix_fc", 0)):
+            doms, fr = S.propagate_fixpoint(m, alldiff=level)
+            exp = rec[name]
+            assert (fr.failed, fr.rounds, fr.failed_var) == (exp["failed"], exp["rounds"], exp["failed_var"]), (seed, name)
+            assert [d.values() for d in doms] == exp["domains"], (seed, name)
+
+
+def test_corpus_removals_per_constraint():
+    for seed in range(200):
+        m = S.parse_model(models.corpus_instance(seed))
+        for level in (0, 1):
+            for c in range(m.n_cons):
+                assert S.removals(m, cons=[c], alldiff=level) == O.removals(m, cons=[c], alldiff=level), (seed, c)
+            assert S.removals(m, alldiff=level) == O.removals(m, alldiff=level), seed
+
+
+def test_optimization_corpus():
+    c = G.corpus()["optimization"]
+    for seed in range(50):
+        text, goal = models.optimization_instance(seed)
+        m = S.parse_model(models.with_goal(text, goal))
+        exp = c[str(seed)]
+        r = S.solve_optimize(m, S.SearchConfig(engine=PARITY))
+        assert r.stats.as_tuple() == G.expected_tuple(exp), seed
+        assert (r.best.values if r.best else None) == exp.get("best"), seed
+        rp = S.solve_optimize(m, S.SearchConfig(engine=PARALLEL))
+        assert (rp.best is None) == (r.best is None), seed
+        if r.best:
+            assert rp.best.objective == r.best.objective, seed
+
+
+def test_random_instances():
+    c = G.corpus()["random"]
+    for seed in range(100, 140):
+        text, _ = models.random_instance(seed)
+        m = S.parse_model(text)
+        st = S.SearchStats()
+        sols = S.enumerate_solutions(m, S.SearchConfig(), st)
+        assert [s.values for s in sols] == c[str(seed)]["all"], seed
+        assert st.as_tuple() == G.expected_tuple(c[str(seed)]), seed
+
+
+# ---- acceptance.cpp:184-301 (criterion 5) inputs: per-propagator removals vs the oracle
+def _subset_domains(lo, hi, bits_list):
+    doms = []
+    for bits in bits_list:
+        d = S.Domain(lo, hi)
+        for b in range(hi - lo + 1):
+            if not (bits >> b) & 1:
+                d.remove(lo + b)
+        doms.append(d)
+    return doms
+
+
+def test_relbin_exhaustive_small_domains():
+    texts = []
+    for op in ["<", "<=", ">", ">=", "=", "!="]:
+        for off in (-1, 0, 2):
+            rhs = "y" if off == 0 else (f"y + {off}" if off > 0 else f"y - {-off}")
+            texts.append(f"var x in 1..4; var y in 1..4; constraint x {op} {rhs}; solve satisfy;")
+        texts.append(f"var x in 1..4; var y in 1..4; constraint x {op} 2; solve satisfy;")
+    for t in texts:
+        m = S.parse_model(t)
+        for bx in range(1, 16):
+            for by in range(1, 16):
+                doms = _subset_domains(1, 4, [bx, by])
+                assert S.removals(m, doms) == O.removals(m, doms), (t, bx, by)
+
+
+def test_alldiff_exhaustive_triples():
+    m = S.parse_model("var x in 1..3; var y in 1..3; var z in 1..3; constraint alldifferent(x, y, z); solve satisfy;")
+    for bx, by, bz in itertools.product(range(1, 8), repeat=3):
+        doms = _subset_domains(1, 3, [bx, by, bz])
+        for level in (0, 1):
+            assert S.removals(m, doms, alldiff=level) == O.removals(m, doms, alldiff=level), (bx, by, bz, level)
+            gd, gf = S.propagate_fixpoint(m, doms, alldiff=level)
+            od, of = O.propagate_fixpoint(m, doms, alldiff=level)
+            assert gd == od and gf == of, (bx, by, bz, level)
+
+
+def test_random_linear_and_alldiff4():
+    rng = models.Rng(5150)
+    for trial in range(400):
+        doms = []
+        for v in range(4):
+            d = S.Domain(1, 8)
+            for x in range(1, 9):
+                if d.size() > 1 and rng.below(2) == 0:
+                    d.remove(x)
+            doms.append(d)
+        a0, a1, a2 = rng.range(-3, 3), rng.range(1, 3), rng.range(-2, 2)
+        op = "<=" if rng.below(2) else "="
+        bound = rng.range(-10, 25)
+        a0, a2 = a0 or 1, a2 or 1
+        t = (f"var a in 1..8; var b in 1..8; var c in 1..8; var d in 1..8; "
+             f"constraint {a0}*a + {a1}*b + {a2}*c {op} {bound}; constraint alldifferent(a, b, c, d); solve satisfy;")
+        t = t.replace("+ -", "- ")
+        m = S.parse_model(t)
+        for level in (0, 1):
+            assert S.removals(m, doms, alldiff=level) == O.removals(m, doms, alldiff=level), (trial, t)
+
+
+def test_pigeonhole_fails_at_root():
+    m = S.parse_model("var a in 1..2;\nvar b in 1..2;\nvar c in 1..2;\nconstraint alldifferent(a, b, c);\nsolve satisfy;")
+    st = S.SearchStats()
+    assert S.enumerate_solutions(m, S.SearchConfig(), st) == []
+    assert (st.nodes, st.failures) == (1, 1)
+
+
+def test_overflow_raises_reference_exception():
+    m = S.parse_model("var x in 1..5; var y in 1..5; constraint 4611686018427387904*x + 4611686018427387904*y <= 3; "
+                      "solve satisfy;")
+    with pytest.raises(S.ArithmeticOverflowError):
+        S.solve_satisfy(m, S.SearchConfig())
+    with pytest.raises(S.ArithmeticOverflowError):
+        O.solve_satisfy(m, S.SearchConfig())
+
+
+def test_optimize_without_objective_is_logic_error():
+    m = S.parse_model("var x in 1..3; solve satisfy;")
+    with pytest.raises(S.LogicError):
+        S.solve_optimize(m, S.SearchConfig())
+
+
+def test_callback_stop_truncates_stats_like_reference():
+    # reference search.cpp:147-149: a callback returning false stops the search right there
+    m = S.parse_model(G.model_text("nq8"))
+    for k in (1, 5, 40):
+        seen = []
+        r = S.solve_satisfy(m, S.SearchConfig(engine=PARITY), lambda s: seen.append(s) or len(seen) < k)
+        ro = O.solve_satisfy(m, S.SearchConfig(), (lambda acc: (lambda s: acc.append(s) or len(acc) < k))([]))
+        assert r.stats.as_tuple() == ro.stats.as_tuple()
+        assert r.complete is False and len(seen) == k
