@@ -51,22 +51,33 @@ enum DeviceError : int32_t {
 };
 
 // Global coordination state for the parallel engine (one per launch, in HBM).
-struct WorkState {
-    int32_t lock;         // queue spin-lock
-    int32_t q_count;      // tasks waiting in queue[]
-    int32_t n_idle;       // contexts waiting for work
-    int32_t outstanding;  // busy contexts + queued tasks; 0 => search finished
+// `hot` is read by every busy context once per node (one 16-byte load, issued early and consumed
+// late so its L2 latency hides behind the propagation rounds); the counters that take heavy
+// atomic traffic live on other 128-byte lines.
+struct alignas(16) HotState {
+    uint32_t push_ticket; // tasks published into the ring
+    uint32_t pop_ticket;  // idle contexts that took a ticket
     int32_t stop;         // 1 => every context unwinds (error / limit / solution cap)
+    int32_t has_bound;    // branch-and-bound incumbent present (parallel)
+};
+
+struct WorkState {
+    HotState hot;
+    int64_t bound;        // branch-and-bound incumbent objective (parallel)
+    int32_t inc_lock;
+    int32_t pad0[25];     // -> 128 bytes
+    int32_t outstanding;  // busy contexts + published tasks; 0 => search finished
     int32_t error;        // DeviceError
     int32_t limit_hit;
     int32_t user_stop;
     uint64_t sol_count;   // solutions recorded (parallel: atomic slot allocator)
-    int64_t bound;        // branch-and-bound incumbent objective (parallel)
-    int32_t has_bound;
-    int32_t inc_lock;
+    int32_t pad1[26];     // -> 256 bytes
     uint64_t stats[4];    // nodes, failures, rounds, solutions
     uint64_t donations;
     uint64_t steals;
+    uint64_t busy_cycles;  // sum over contexts of clock64 cycles with work
+    uint64_t idle_cycles;  // sum over contexts of clock64 cycles waiting for work
+    uint64_t lock_fails;   // unused (kept for the debug line)
 };
 
 struct SearchParams {
@@ -88,7 +99,8 @@ struct SearchParams {
     uint32_t* gdom;        // [n_ctx][2*NW] when domains do not fit in shared memory
     // work sharing
     WorkState* ws;
-    int32_t* queue;        // [n_ctx]
+    unsigned long long* ring; // [ring_cap] published tasks: ((ticket + 1) << 32) | donor ctx
+    uint32_t ring_cap;
     int32_t* outbox_busy;  // [n_ctx]
     uint32_t* outbox;      // [n_ctx][NW + KW + 4]
     // solutions

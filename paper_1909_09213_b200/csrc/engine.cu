@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <mutex>
@@ -305,14 +306,16 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
     out.KW = KW;
     // launch geometry
     int block = cfg.block_threads > 0 ? ((cfg.block_threads + 31) / 32) * 32 : 0;
-    if (!block) block = parallel ? (P.na > 0 && P.nr + P.nl > 0 ? 64 : 32) : parity_block(P);
+    if (!block) // parallel: one warp per context maximises resident contexts (32 per SM) for small models
+        block = parallel ? (P.nr + P.nl > 1024 || P.n > 1024 ? 128 : (P.W >= 8 || P.nr + P.nl > 256 ? 64 : 32))
+                         : parity_block(P);
     block = std::min(std::max(block, 32), 1024);
     const int nw = block / 32;
     bool in_smem = true;
-    dev::SmemLayout L = dev::smem_layout(P.W, n, P.total_members, nw, KW, true);
+    dev::SmemLayout L = dev::smem_layout(P.W, n, P.total_members, nw, KW, true, P.na);
     if (L.total > kSmemBudget) {
         in_smem = false;
-        L = dev::smem_layout(P.W, n, P.total_members, nw, KW, false);
+        L = dev::smem_layout(P.W, n, P.total_members, nw, KW, false, P.na);
         if (L.total > kSmemBudget) throw StatusError{CUBICS_E_UNSUPPORTED, "search context does not fit in shared memory"};
     }
     int n_ctx = 1;
@@ -345,7 +348,8 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
     };
     const size_t a_blob = take(P.blob.bytes.size());
     const size_t a_ws = take(sizeof(WorkState));
-    const size_t a_queue = take(sizeof(int32_t) * n_ctx);
+    const uint32_t ring_cap = 2u * (uint32_t)n_ctx;
+    const size_t a_queue = take(sizeof(unsigned long long) * ring_cap);
     const size_t a_busy = take(sizeof(int32_t) * n_ctx);
     const size_t a_hf = take(sizeof(int32_t) * n_ctx);
     const size_t zero_end = off;
@@ -398,7 +402,8 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
         S.frame_meta = reinterpret_cast<int32_t*>(base + a_meta);
         S.gdom = reinterpret_cast<uint32_t*>(base + a_gdom);
         S.ws = reinterpret_cast<WorkState*>(base + a_ws);
-        S.queue = reinterpret_cast<int32_t*>(base + a_queue);
+        S.ring = reinterpret_cast<unsigned long long*>(base + a_queue);
+        S.ring_cap = ring_cap;
         S.outbox_busy = reinterpret_cast<int32_t*>(base + a_busy);
         S.outbox = reinterpret_cast<uint32_t*>(base + a_outbox);
         S.sol_cap = sol_cap;
@@ -482,6 +487,16 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     cudaStreamDestroy(st);
+    if (std::getenv("CUBICS_DEBUG")) {
+        const WorkState& w = out.ws;
+        const double tot = (double)w.busy_cycles + (double)w.idle_cycles;
+        std::fprintf(stderr,
+                     "[cubics] engine=%s ctx=%d block=%d W=%d smem=%zu KW=%d ms=%.3f nodes=%llu donations=%llu "
+                     "steals=%llu busy=%.3f\n",
+                     parallel ? "parallel" : "parity", n_ctx, block, P.W, L.total, KW, out.device_ms,
+                     (unsigned long long)w.stats[0], (unsigned long long)w.donations, (unsigned long long)w.steals,
+                     tot > 0 ? w.busy_cycles / tot : 0.0);
+    }
     if (out.ws.error == DERR_OVERFLOW) throw StatusError{CUBICS_E_OVERFLOW, "overflow in linear propagation"};
     if (out.ws.error == DERR_CAPACITY) throw StatusError{CUBICS_E_CAPACITY, "device decision stack capacity exceeded"};
 }
@@ -635,7 +650,7 @@ extern "C" int cubics_solve_optimize(const cubics_model* h, const cubics_search_
         out->complete = !r.ws.limit_hit;
         std::vector<uint16_t> best;
         if (parallel) {
-            if (r.ws.has_bound) best = r.inc_vals;
+            if (r.ws.hot.has_bound) best = r.inc_vals;
         } else if (r.rec.count) {
             best.assign(r.rec.vals.end() - n, r.rec.vals.end());
         }

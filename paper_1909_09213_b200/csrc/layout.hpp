@@ -19,11 +19,16 @@ CUBICS_HD constexpr size_t round4(size_t x) { return (x + 3) & ~size_t(3); }
 CUBICS_HD constexpr int warp_scratch_bytes(int W) { return (66 + 64) * 8 + W * 32; }
 
 struct SmemLayout {
-    size_t dom, rm, mates, scratch, path, bestkey, total;
+    size_t dom, rm, mates, scratch, path, bestkey, post, post_ok, total;
     int stride;
+    bool has_post;
 };
 
-CUBICS_HD inline SmemLayout smem_layout(int W, int n, int total_members, int nw, int KW, bool dom_in_smem) {
+// GAC post-states are kept when they cost at most this many bytes of shared memory
+constexpr size_t kPostBudget = 16384;
+
+CUBICS_HD inline SmemLayout smem_layout(int W, int n, int total_members, int nw, int KW, bool dom_in_smem,
+                                        int na = 0) {
     SmemLayout L{};
     const size_t NWP = round4((size_t)n * W);
     size_t p = 0;
@@ -39,6 +44,12 @@ CUBICS_HD inline SmemLayout smem_layout(int W, int n, int total_members, int nw,
     p += ((size_t)KW * 4 + 15) & ~size_t(15);
     L.bestkey = p;
     p += ((size_t)KW * 4 + 15) & ~size_t(15);
+    const size_t post_bytes = (size_t)total_members * W * 4;
+    L.has_post = na > 0 && post_bytes <= kPostBudget;
+    L.post = p;
+    p += L.has_post ? post_bytes : 0;
+    L.post_ok = p;
+    p += L.has_post ? (((size_t)na + 15) & ~size_t(15)) : 0;
     L.total = p;
     return L;
 }

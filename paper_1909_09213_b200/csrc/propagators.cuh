@@ -336,7 +336,7 @@ __device__ bool gac_augment(int r, const uint32_t (&D0)[W], const uint32_t (&D1)
 // member unmatched (transversal-matroid greedy basis), and wipe it.
 template <int W>
 __device__ void prop_alldiff_gac(const DevModel& M, int a, const uint32_t* dom, uint32_t* rm, int16_t* mates,
-                                 const WarpScratch& ws, int lane, int exact_wipe) {
+                                 const WarpScratch& ws, int lane, int exact_wipe, uint32_t* post, int8_t* post_ok) {
     const int b = M.ad_start[a], n = M.ad_start[a + 1] - b;
     const bool h0 = lane < n, h1 = lane + 32 < n;
     uint32_t D0[W], D1[W];
@@ -353,6 +353,15 @@ __device__ void prop_alldiff_gac(const DevModel& M, int a, const uint32_t* dom, 
     for (int w = 0; w < W; ++w) {
         D0[w] = h0 ? (s0 ? shifted_word<W>(dom + (size_t)v0 * W, w, s0) : dom[(size_t)v0 * W + w]) : 0u;
         D1[w] = h1 ? (s1 ? shifted_word<W>(dom + (size_t)v1 * W, w, s1) : dom[(size_t)v1 * W + w]) : 0u;
+    }
+    if (post) { // idempotence: the post-state of the last evaluation is GAC-consistent
+        bool same = true;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            if (h0) same &= dom[(size_t)v0 * W + w] == post[(size_t)lane * W + w];
+            if (h1) same &= dom[(size_t)v1 * W + w] == post[(size_t)(lane + 32) * W + w];
+        }
+        if (__all_sync(FULL, same) && *post_ok) return;
     }
     int m0 = h0 ? mates[lane] : -1, m1 = h1 ? mates[lane + 32] : -1;
     if (m0 >= 0 && !testbit_r<W>(D0, m0)) m0 = -1; // warm start: keep still-valid edges
@@ -392,6 +401,7 @@ __device__ void prop_alldiff_gac(const DevModel& M, int a, const uint32_t* dom, 
         }
         if (h0) mates[lane] = (int16_t)m0;
         if (h1) mates[lane + 32] = (int16_t)m1;
+        if (post && lane == 0) *post_ok = 0;
         __syncwarp();
         return;
     }
@@ -423,8 +433,11 @@ __device__ void prop_alldiff_gac(const DevModel& M, int a, const uint32_t* dom, 
             x1 &= x1 - 1;
         }
     }
-    // Warshall: anc(k) = members that reach k
-    for (int p = 0; p < n; ++p) {
+    // Warshall: anc(k) = members that reach k. A singleton member has no in-edge (its only value
+    // is its own mate), so it is never interior to a path: only non-singletons serve as pivots.
+    const unsigned long long pivots = ballot64(h0 && dom_size<W>(D0) > 1, h1 && dom_size<W>(D1) > 1);
+    for (unsigned long long q = pivots; q; q &= q - 1) {
+        const int p = __ffsll((long long)q) - 1;
         const unsigned long long ap = __shfl_sync(FULL, (p >> 5) ? p1 : p0, p & 31);
         if ((p0 >> p) & 1ull) p0 |= ap;
         if ((p1 >> p) & 1ull) p1 |= ap;
@@ -465,9 +478,14 @@ __device__ void prop_alldiff_gac(const DevModel& M, int a, const uint32_t* dom, 
             for (int w = 0; w < W; ++w) { // back to the member's own bit positions
                 uint32_t mword = sh ? shifted_word<W>(rem, w, -sh) : rem[w];
                 if (mword) atomicOr(rm + (size_t)v * W + w, mword);
+                if (post) post[(size_t)k * W + w] = dom[(size_t)v * W + w] & ~mword;
             }
+        } else if (post) {
+#pragma unroll
+            for (int w = 0; w < W; ++w) post[(size_t)k * W + w] = dom[(size_t)v * W + w];
         }
     }
+    if (post && lane == 0) *post_ok = 1;
     __syncwarp();
 }
 
@@ -533,6 +551,8 @@ struct RoundCtx {
     uint32_t* dom;
     uint32_t* rm;
     int16_t* mates;     // [total_members] persistent warm-start matchings
+    uint32_t* post;     // [total_members * W] GAC post-states (null: skip test disabled)
+    int8_t* post_ok;    // [na]
     uint8_t* scratch;   // per-warp GAC scratch
     int scratch_stride; // bytes per warp
     const uint8_t* enabled;
@@ -568,7 +588,9 @@ __device__ __forceinline__ void run_propagators(const DevModel& M, const RoundCt
         const WarpScratch ws = warp_scratch<W>(R, warp);
         for (int a = warp - (nw - ad_warps); a < M.na; a += ad_warps) {
             if (R.enabled && !R.enabled[M.nr + M.nl + a]) continue;
-            if (R.alldiff) prop_alldiff_gac<W>(M, a, R.dom, R.rm, R.mates + M.ad_start[a], ws, lane, R.exact_wipe);
+            if (R.alldiff)
+                prop_alldiff_gac<W>(M, a, R.dom, R.rm, R.mates + M.ad_start[a], ws, lane, R.exact_wipe,
+                                    R.post ? R.post + (size_t)M.ad_start[a] * W : nullptr, R.post_ok + a);
             else prop_alldiff_fc<W>(M, a, R.dom, R.rm, lane);
         }
     }

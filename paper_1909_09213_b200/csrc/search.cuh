@@ -23,13 +23,36 @@ namespace dev {
 
 __device__ __forceinline__ int ld_volatile(const int32_t* p) { return *reinterpret_cast<const volatile int32_t*>(p); }
 
-__device__ __forceinline__ void spin_lock(int32_t* l) {
-    int ns = 16;
+__device__ __forceinline__ long long ld_volatile_s64(const int64_t* p) {
+    return *reinterpret_cast<const volatile long long*>(p);
+}
+
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
+    return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+
+__device__ __forceinline__ void st_volatile_u64(unsigned long long* p, unsigned long long v) {
+    *reinterpret_cast<volatile unsigned long long*>(p) = v;
+}
+
+// one 16-byte L1-bypassing load of {push_ticket, pop_ticket, stop, has_bound}
+__device__ __forceinline__ uint4 ld_volatile_v4(const uint4* p) {
+    uint4 r;
+    asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ int spin_lock(int32_t* l) {
+    int ns = 16, fails = 0;
     while (atomicCAS(l, 0, 1) != 0) {
+        ++fails;
         __nanosleep(ns);
         ns = ns < 512 ? ns * 2 : ns;
     }
     __threadfence();
+    return fails;
 }
 
 __device__ __forceinline__ void spin_unlock(int32_t* l) {
@@ -98,13 +121,15 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
     const int n = M.n;
     const size_t NW = (size_t)n * W, NWP = round4(NW);
     const int KW = P.KW;
-    const SmemLayout L = smem_layout(W, n, M.total_members, nw, KW, P.dom_in_smem);
+    const SmemLayout L = smem_layout(W, n, M.total_members, nw, KW, P.dom_in_smem, M.na);
     uint32_t* dom = P.dom_in_smem ? reinterpret_cast<uint32_t*>(smem + L.dom) : P.gdom + (size_t)ctx * 2 * NWP;
     uint32_t* rm = P.dom_in_smem ? reinterpret_cast<uint32_t*>(smem + L.rm) : dom + NWP;
     int16_t* mates = reinterpret_cast<int16_t*>(smem + L.mates);
     uint32_t* path = reinterpret_cast<uint32_t*>(smem + L.path);
     uint32_t* bestkey = reinterpret_cast<uint32_t*>(smem + L.bestkey);
-    RoundCtx R{dom, rm, mates, smem + L.scratch, L.stride, nullptr, P.alldiff, P.exact_wipe};
+    uint32_t* post = L.has_post ? reinterpret_cast<uint32_t*>(smem + L.post) : nullptr;
+    int8_t* post_ok = reinterpret_cast<int8_t*>(smem + L.post_ok);
+    RoundCtx R{dom, rm, mates, post, post_ok, smem + L.scratch, L.stride, nullptr, P.alldiff, P.exact_wipe};
     uint32_t* frames = P.frames + (size_t)ctx * P.frame_cap * NWP;
     int32_t* meta = P.frame_meta + (size_t)ctx * P.frame_cap * 4;
     WorkState* ws = P.ws;
@@ -112,6 +137,8 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
 
     for (size_t i = tid; i < NWP; i += T) rm[i] = 0;
     for (int i = tid; i < M.total_members; i += T) mates[i] = -1;
+    if (L.has_post)
+        for (int i = tid; i < M.na; i += T) post_ok[i] = 0;
     for (int i = tid; i < KW; i += T) {
         path[i] = 0;
         bestkey[i] = 0xffffffffu;
@@ -125,34 +152,39 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
     bool has_first = false;
     const bool optimizing = M.goal != 0, minimizing = M.goal == 1;
     const int obj = M.goal_var;
+    // thread 0's view of the shared coordination state (parallel engine)
+    uint4 hot = make_uint4(0, 0, 0, 0);
+    long long g_bound = P.init_bound;
+    int g_has_bound = P.has_init_bound;
+    int my_busy = 0;
 
-    // ---- acquire the first subtree: the root for context 0, a donated one for the rest
+    long long idle_cyc = 0, steals = 0, donations = 0;
+    const long long t_start = clock64();
+
+    // Idle: take a ticket and wait for the task published under it (lock-free ticket queue:
+    // each waiter spins on its own ring slot, so there is no shared hot spot to contend on).
     auto get_work = [&]() -> bool {
         if (tid == 0) {
+            const long long t0 = clock64();
             atomicSub(&ws->outstanding, 1);
-            atomicAdd(&ws->n_idle, 1);
-            int got = -1, ns = 64;
-            for (;;) {
-                if (ld_volatile(&ws->stop)) break;
-                if (ld_volatile(&ws->q_count) > 0) {
-                    spin_lock(&ws->lock);
-                    volatile int32_t* qc = &ws->q_count;
-                    if (*qc > 0) {
-                        const int k = *qc - 1;
-                        got = reinterpret_cast<volatile int32_t*>(P.queue)[k];
-                        *qc = k;
-                    }
-                    spin_unlock(&ws->lock);
-                    if (got >= 0) break;
+            const uint32_t t = atomicAdd(&ws->hot.pop_ticket, 1u);
+            const unsigned long long* slot = P.ring + (t % P.ring_cap);
+            int got = -1, ns = 32;
+            for (int it = 0;; ++it) {
+                const unsigned long long v = ld_volatile_u64(slot);
+                if ((uint32_t)(v >> 32) == t + 1u) {
+                    got = (int)(v & 0xffffffffu);
+                    break;
                 }
-                if (ld_volatile(&ws->outstanding) == 0) break;
+                if ((it & 7) == 7 && (ld_volatile(&ws->hot.stop) || ld_volatile(&ws->outstanding) == 0)) break;
                 __nanosleep(ns);
-                ns = ns < 2048 ? ns * 2 : ns;
+                ns = ns < 1024 ? ns * 2 : ns;
             }
             if (got >= 0) {
-                atomicSub(&ws->n_idle, 1);
                 __threadfence();
+                ++steals;
             }
+            idle_cyc += clock64() - t0;
             s_src = got;
         }
         __syncthreads();
@@ -186,20 +218,21 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
         if (P.node_limit && nodes > P.node_limit) {
             if (tid == 0) {
                 ws->limit_hit = 1;
-                ws->stop = 1;
+                ws->hot.stop = 1;
             }
             break;
+        }
+        if (parallel && tid == 0) { // prefetch; consumed after the fixpoint
+            hot = ld_volatile_v4(reinterpret_cast<const uint4*>(&ws->hot));
+            if (optimizing) g_bound = ld_volatile_s64(&ws->bound);
+            my_busy = ld_volatile(&P.outbox_busy[ctx]);
         }
         bool backtrack = false;
         if (optimizing) { // branch-and-bound shrink (:87-101), done by thread 0
             if (tid == 0) {
                 int empty = 0;
-                long long bnd = bound;
-                bool hb = has_bound;
-                if (parallel) {
-                    hb = ld_volatile(&ws->has_bound) != 0;
-                    bnd = *reinterpret_cast<volatile long long*>(&ws->bound);
-                }
+                const long long bnd = parallel ? g_bound : bound;
+                const bool hb = parallel ? g_has_bound != 0 : has_bound;
                 if (hb) {
                     uint32_t* d = dom + (size_t)obj * W;
                     const long long off = M.off[obj];
@@ -207,8 +240,7 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
                     const bool shrink = minimizing ? (off + hi >= bnd) : (off + lo <= bnd);
                     if (shrink) {
                         // minimise: remove_above(bound-1) ; maximise: remove_below(bound+1)
-                        const long long cut = minimizing ? clampbit((i128)bnd - off, W * 32)
-                                                         : clampbit((i128)bnd - off, W * 32);
+                        const long long cut = clampbit((i128)bnd - off, W * 32);
                         uint32_t any = 0;
 #pragma unroll
                         for (int w = 0; w < W; ++w) {
@@ -232,7 +264,7 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
             if (st == R_ERROR) {
                 if (tid == 0) {
                     ws->error = DERR_OVERFLOW;
-                    ws->stop = 1;
+                    ws->hot.stop = 1;
                 }
                 break;
             }
@@ -241,6 +273,7 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
                 backtrack = true;
             }
         }
+        if (parallel && tid == 0) g_has_bound = (int)hot.w; // the prefetched bound pairs with this flag
         if (!backtrack) {
             const int sel = select_var<W>(M, dom, P.var_heuristic, s_red);
             if (sel < 0) {
@@ -287,7 +320,7 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
                     if (parallel && tid == 0) {
                         spin_lock(&ws->inc_lock);
                         volatile long long* gb = reinterpret_cast<volatile long long*>(&ws->bound);
-                        volatile int32_t* ghb = &ws->has_bound;
+                        volatile int32_t* ghb = &ws->hot.has_bound;
                         if (!*ghb || (minimizing ? val < *gb : val > *gb)) {
                             for (int v = 0; v < n; ++v) P.inc_vals[v] = (uint16_t)dom_first<W>(dom + (size_t)v * W);
                             *gb = val;
@@ -295,13 +328,15 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
                             *ghb = 1;
                         }
                         spin_unlock(&ws->inc_lock);
+                        g_bound = *gb; // our own incumbent is visible to us at once
+                        g_has_bound = 1;
                     }
                 }
                 __syncthreads();
                 if (!parallel && sols >= P.max_solutions) {
                     if (tid == 0) {
                         ws->user_stop = 1;
-                        ws->stop = 1;
+                        ws->hot.stop = 1;
                     }
                     break;
                 }
@@ -311,7 +346,7 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
                 if (sp >= P.frame_cap) {
                     if (tid == 0) {
                         ws->error = DERR_CAPACITY;
-                        ws->stop = 1;
+                        ws->hot.stop = 1;
                     }
                     break;
                 }
@@ -321,49 +356,38 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
                     meta[sp * 4 + 0] = sel;
                     meta[sp * 4 + 1] = bit;
                     meta[sp * 4 + 2] = depth;
+                    // donate the shallowest pending right branch when someone waits for work
+                    int want = hot.z ? 2 : 0;
+                    if (parallel && !want && sp + 1 > base && !my_busy && hot.y > hot.x) want = 1;
+                    s_flag = want;
                 }
                 __syncthreads();
                 if (tid < W) dom[(size_t)sel * W + tid] = (tid == (bit >> 5)) ? (1u << (bit & 31)) : 0u;
                 ++sp;
                 ++depth;
-                if (parallel) {
-                    // donate the shallowest pending right branch when someone is idle
-                    if (tid == 0) {
-                        int want = ld_volatile(&ws->stop) ? 2 : 0;
-                        if (!want && sp > base && !ld_volatile(&P.outbox_busy[ctx]) &&
-                            ld_volatile(&ws->n_idle) > ld_volatile(&ws->q_count))
-                            want = 1;
-                        s_flag = want;
+                const int want = s_flag;
+                if (want == 2) break;
+                if (want == 1) {
+                    const int f = base++;
+                    const int fvar = meta[f * 4 + 0], fbit = meta[f * 4 + 1], fdepth = meta[f * 4 + 2];
+                    uint32_t* ob = P.outbox + (size_t)ctx * OS;
+                    const uint32_t* fr = frames + (size_t)f * NWP;
+                    const size_t clr = (size_t)fvar * W + (fbit >> 5);
+                    for (size_t i = tid; i < NWP; i += T) {
+                        uint32_t x = fr[i];
+                        if (i == clr) x &= ~(1u << (fbit & 31));
+                        ob[i] = x;
                     }
+                    for (int i = tid; i < KW; i += T) ob[NWP + i] = path_right_word(path[i], i, fdepth);
+                    if (tid == 0) ob[NWP + KW] = (uint32_t)(fdepth + 1);
                     __syncthreads();
-                    const int want = s_flag;
-                    if (want == 2) break;
-                    if (want == 1) {
-                        const int f = base++;
-                        const int fvar = meta[f * 4 + 0], fbit = meta[f * 4 + 1], fdepth = meta[f * 4 + 2];
-                        uint32_t* ob = P.outbox + (size_t)ctx * OS;
-                        const uint32_t* fr = frames + (size_t)f * NWP;
-                        const size_t clr = (size_t)fvar * W + (fbit >> 5);
-                        for (size_t i = tid; i < NWP; i += T) {
-                            uint32_t x = fr[i];
-                            if (i == clr) x &= ~(1u << (fbit & 31));
-                            ob[i] = x;
-                        }
-                        for (int i = tid; i < KW; i += T) ob[NWP + i] = path_right_word(path[i], i, fdepth);
-                        if (tid == 0) ob[NWP + KW] = (uint32_t)(fdepth + 1);
-                        __syncthreads();
-                        if (tid == 0) {
-                            __threadfence();
-                            P.outbox_busy[ctx] = 1;
-                            atomicAdd(&ws->outstanding, 1);
-                            spin_lock(&ws->lock);
-                            volatile int32_t* qc = &ws->q_count;
-                            const int k = *qc;
-                            reinterpret_cast<volatile int32_t*>(P.queue)[k] = ctx;
-                            *qc = k + 1;
-                            spin_unlock(&ws->lock);
-                            atomicAdd((unsigned long long*)&ws->donations, 1ull);
-                        }
+                    if (tid == 0) {
+                        P.outbox_busy[ctx] = 1;
+                        atomicAdd(&ws->outstanding, 1);
+                        const uint32_t s = atomicAdd(&ws->hot.push_ticket, 1u);
+                        __threadfence();
+                        st_volatile_u64(P.ring + (s % P.ring_cap), ((unsigned long long)(s + 1u) << 32) | (unsigned)ctx);
+                        ++donations;
                     }
                 }
                 __syncthreads();
@@ -371,9 +395,13 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
             }
         }
         // ================= backtrack: right branch of the deepest pending frame (:122-131)
+        if (parallel) {
+            if (tid == 0) s_flag = hot.z;
+            __syncthreads();
+            if (s_flag) break;
+        }
         if (sp == base) {
             if (!parallel) break;
-            __syncthreads();
             have_work = get_work();
             __syncthreads();
             continue;
@@ -398,6 +426,11 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
         atomicSub(&ws->outstanding, 1);
     }
     if (tid == 0) {
+        const long long total = clock64() - t_start;
+        atomicAdd((unsigned long long*)&ws->busy_cycles, (unsigned long long)(total - idle_cyc));
+        atomicAdd((unsigned long long*)&ws->idle_cycles, (unsigned long long)idle_cyc);
+        atomicAdd((unsigned long long*)&ws->steals, (unsigned long long)steals);
+        atomicAdd((unsigned long long*)&ws->donations, (unsigned long long)donations);
         atomicAdd((unsigned long long*)&ws->stats[0], nodes);
         atomicAdd((unsigned long long*)&ws->stats[1], failures);
         atomicAdd((unsigned long long*)&ws->stats[2], rounds);
@@ -417,7 +450,7 @@ __global__ void __launch_bounds__(1024) propagate_kernel(const PropParams P, uin
     uint32_t* dom = dom_in_smem ? reinterpret_cast<uint32_t*>(smem + L.dom) : gscratch;
     uint32_t* rm = dom_in_smem ? reinterpret_cast<uint32_t*>(smem + L.rm) : gscratch + NWP;
     int16_t* mates = reinterpret_cast<int16_t*>(smem + L.mates);
-    RoundCtx R{dom, rm, mates, smem + L.scratch, L.stride, P.enabled, P.alldiff, 1};
+    RoundCtx R{dom, rm, mates, nullptr, nullptr, smem + L.scratch, L.stride, P.enabled, P.alldiff, 1};
     for (size_t i = tid; i < NWP; i += T) {
         dom[i] = P.dom[i];
         rm[i] = 0;
