@@ -4,7 +4,9 @@
 // HBM / shared-memory layout:
 //   domains  : n x W u32 words, var v at [v*W, v*W+W); bit i = value off[v] + i. W is a power of
 //              two >= every domain's and every alldifferent universe's word count (u32 words).
-//   RelBin   : one 16-byte record per constraint {x, (y+1)<<3 | op, k}      (model.hpp:26-32)
+//   RelBin   : one 16-byte record per constraint {x, y, op, s} with every 64-bit offset folded
+//              on the host into a 32-bit bit offset s (model.hpp:26-32): var form x op y + k has
+//              s = off[y] + k - off[x]; the literal form carries its threshold bit index in s.
 //   Linear   : CSR {start[], op[], bound[]} over terms {var[], coeff[]}     (model.hpp:42-46)
 //   AllDiff  : CSR over members {var[], shift[]}; shift = off[var] - universe_offset, so a
 //              member's domain shifted left by `shift` bits lands in the common value universe.
@@ -14,10 +16,11 @@
 
 namespace cubics {
 
-struct RelBinRec {
+struct alignas(16) RelBinRec {
     int32_t x;
-    int32_t yop;  // ((y + 1) << 3) | op ; y = -1 for the literal form
-    int64_t k;    // literal, or the offset added to y
+    int32_t y;   // -1 for the literal form
+    int32_t op;  // fd::RelOp
+    int32_t s;   // var form: off[y] + k - off[x]; literal form: threshold bit (see engine.cu)
 };
 
 struct DevModel {

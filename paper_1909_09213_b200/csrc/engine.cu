@@ -153,11 +153,26 @@ void prepare(const HostModel& m, const uint64_t* words, Prepared& P) {
         const int b = m.con_start[c], e = m.con_start[c + 1];
         switch (m.con_kind[c]) {
         case CUBICS_RELBIN: {
+            // fold the int64 arithmetic of prop_rel_bin (propagation.cpp:126-192) into one clamped
+            // bit offset; any value beyond +-4096 bits behaves identically on <= 1024-bit domains
+            auto clampi = [](__int128 v, long lo, long hi) {
+                return static_cast<int32_t>(v < lo ? lo : (v > hi ? hi : v));
+            };
+            auto wrap = [](int64_t a, int64_t b) { return (int64_t)((uint64_t)a + (uint64_t)b); };
             RelBinRec r{};
             r.x = m.term_var[b];
-            const int y = e - b == 2 ? m.term_var[b + 1] : -1;
-            r.yop = ((y + 1) << 3) | m.con_op[c];
-            r.k = m.con_value[c];
+            r.y = e - b == 2 ? m.term_var[b + 1] : -1;
+            r.op = m.con_op[c];
+            const int64_t k = m.con_value[c];
+            const __int128 offx = m.offset[r.x];
+            if (r.y >= 0) {
+                r.s = clampi((__int128)m.offset[r.y] + k - offx, -4096, 4096);
+            } else {
+                __int128 lit = k;
+                if (r.op == CUBICS_LE) lit = wrap(k, 1);  // remove [lit+1, max]
+                if (r.op == CUBICS_GE) lit = wrap(k, -1); // remove [min, lit-1]
+                r.s = clampi(lit - offx, -1, 2048);
+            }
             P.kind_index[c] = static_cast<int>(rb.size());
             rb.push_back(r);
             break;
@@ -335,7 +350,7 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
     if (cfg.node_limit && cfg.node_limit + 1 < (uint64_t)frame_cap) frame_cap = static_cast<int>(cfg.node_limit + 1);
     frame_cap = std::max(frame_cap, 1);
     const size_t NWP = P.NWP;
-    const size_t OS = NWP + dev::round4((size_t)KW + 1);
+    const size_t OS = NWP + dev::round4((size_t)KW + 2);
     if (!record) sol_cap = 0;
 
     // one device allocation: [model blob | ws | queue | busy | has_first | frames | meta | gdom | outbox |
@@ -733,10 +748,10 @@ int run_prop(const cubics_model* h, const uint64_t* words_in, uint64_t* words_ou
     const size_t NWP = P.NWP;
     const int block = parity_block(P);
     bool in_smem = true;
-    dev::SmemLayout L = dev::smem_layout(P.W, P.n, P.total_members, block / 32, 0, true);
+    dev::SmemLayout L = dev::smem_layout(P.W, P.n, P.total_members, block / 32, 0, true, P.na);
     if (L.total > kSmemBudget) {
         in_smem = false;
-        L = dev::smem_layout(P.W, P.n, P.total_members, block / 32, 0, false);
+        L = dev::smem_layout(P.W, P.n, P.total_members, block / 32, 0, false, P.na);
     }
     size_t off = 0;
     auto take = [&](size_t bytes) {

@@ -19,13 +19,15 @@ CUBICS_HD constexpr size_t round4(size_t x) { return (x + 3) & ~size_t(3); }
 CUBICS_HD constexpr int warp_scratch_bytes(int W) { return (66 + 64) * 8 + W * 32; }
 
 struct SmemLayout {
-    size_t dom, rm, mates, scratch, path, bestkey, post, post_ok, total;
+    size_t dom, rm, mates, scratch, path, bestkey, post, post_ok, chg, total;
     int stride;
-    bool has_post;
+    bool has_post, has_chg;
 };
 
 // GAC post-states are kept when they cost at most this many bytes of shared memory
 constexpr size_t kPostBudget = 16384;
+// changed-variable trigger bitmaps (two buffers of n bits) are kept up to this size
+constexpr size_t kChgBudget = 65536;
 
 CUBICS_HD inline SmemLayout smem_layout(int W, int n, int total_members, int nw, int KW, bool dom_in_smem,
                                         int na = 0) {
@@ -50,6 +52,10 @@ CUBICS_HD inline SmemLayout smem_layout(int W, int n, int total_members, int nw,
     p += L.has_post ? post_bytes : 0;
     L.post_ok = p;
     p += L.has_post ? (((size_t)na + 15) & ~size_t(15)) : 0;
+    const size_t chg_bytes = (((size_t)n + 31) / 32) * 4;
+    L.has_chg = 2 * chg_bytes <= kChgBudget;
+    L.chg = p;
+    p += L.has_chg ? ((2 * chg_bytes + 15) & ~size_t(15)) : 0;
     L.total = p;
     return L;
 }

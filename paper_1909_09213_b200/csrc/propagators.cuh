@@ -94,9 +94,9 @@ __device__ __forceinline__ void or_range(uint32_t* rmv, const uint32_t* dv, long
     }
 }
 
-__device__ __forceinline__ void or_bit(uint32_t* rmv, const uint32_t* dv, i128 bit, int nb) {
-    if (bit < 0 || bit >= (i128)nb) return;
-    int b = (int)bit;
+__device__ __forceinline__ void or_bit(uint32_t* rmv, const uint32_t* dv, int bit, int nb) {
+    if (bit < 0 || bit >= nb) return;
+    const int b = bit;
     uint32_t m = (1u << (b & 31)) & dv[b >> 5];
     if (m) atomicOr(rmv + (b >> 5), m);
 }
@@ -106,76 +106,87 @@ __device__ __forceinline__ long long wrap_add(long long a, long long b) {
 }
 
 // ------------------------------------------------------------------ RelBin (propagation.cpp:120-194)
+// All offsets are pre-folded into r.s (engine.cu), so every case is 32-bit bit arithmetic:
+//   x <  y+k : x loses bits >= last(y)+s      y loses bits <= first(x)-s
+//   x <= y+k : x loses bits >= last(y)+s+1    y loses bits <= first(x)-s-1
+//   x >  y+k : x loses bits <= first(y)+s     y loses bits >= last(x)-s
+//   x >= y+k : x loses bits <= first(y)+s-1   y loses bits >= last(x)-s+1
+//   x =  y+k : x keeps D(y) << s, y keeps D(x) >> s      (domain consistency)
+//   x != y+k : singleton y removes bit first(y)+s from x, singleton x removes first(x)-s from y
+// Literal forms carry the threshold bit in s (x < lit: bits >= s; x <= lit: bits >= s with
+// s = lit+1-off; x > lit: bits <= s; x >= lit: bits <= s with s = lit-1-off; = / != : bit s).
 template <int W>
 __device__ __forceinline__ void prop_relbin(const DevModel& M, int c, const uint32_t* dom, uint32_t* rm) {
     constexpr int NB = W * 32;
     const RelBinRec r = M.rb[c];
-    const int x = r.x, op = r.yop & 7, y = (r.yop >> 3) - 1;
-    const uint32_t* dx = dom + (size_t)x * W;
-    uint32_t* rx = rm + (size_t)x * W;
-    const long long offx = M.off[x];
-    if (y < 0) { // x op literal (:126-141); absent values are masked by dx
-        const i128 lit = r.k;
-        switch (op) {
-        case 0: or_range<W>(rx, dx, clampbit(lit - offx, NB), NB); break;                          // <
-        case 1: or_range<W>(rx, dx, clampbit((i128)wrap_add(r.k, 1) - offx, NB), NB); break;        // <=
-        case 2: or_range<W>(rx, dx, -1, clampbit(lit - offx, NB)); break;                           // >
-        case 3: or_range<W>(rx, dx, -1, clampbit((i128)wrap_add(r.k, -1) - offx, NB)); break;       // >=
-        case 4: {                                                                                   // =
-            i128 b = lit - offx;
+    const uint32_t* dx = dom + (size_t)r.x * W;
+    uint32_t* rx = rm + (size_t)r.x * W;
+    const int s = r.s;
+    if (r.y < 0) {
+        switch (r.op) {
+        case 0:
+        case 1: or_range<W>(rx, dx, s, NB); break;
+        case 2:
+        case 3: or_range<W>(rx, dx, -1, s); break;
+        case 4: {
 #pragma unroll
             for (int w = 0; w < W; ++w) {
-                uint32_t keep = (b >= (i128)w * 32 && b < (i128)w * 32 + 32) ? (1u << (int)(b - w * 32)) : 0u;
-                uint32_t m = dx[w] & ~keep;
+                const uint32_t keep = (s >= w * 32 && s < w * 32 + 32) ? (1u << (s - w * 32)) : 0u;
+                const uint32_t m = dx[w] & ~keep;
                 if (m) atomicOr(rx + w, m);
             }
             break;
         }
-        default: or_bit(rx, dx, lit - offx, NB); break;                                             // !=
+        default: or_bit(rx, dx, s, NB); break;
         }
         return;
     }
-    const uint32_t* dy = dom + (size_t)y * W;
-    uint32_t* ry = rm + (size_t)y * W;
-    const long long offy = M.off[y];
-    const i128 k = r.k;
-    if (op == 5) { // x != y + k: value consistency from singletons (:180-191)
-        int sy = dom_size<W>(dy), sx = dom_size<W>(dx);
-        if (sy == 1) or_bit(rx, dx, (i128)offy + dom_first<W>(dy) + k - offx, NB);
-        if (sx == 1) or_bit(ry, dy, (i128)offx + dom_first<W>(dx) - k - offy, NB);
+    const uint32_t* dy = dom + (size_t)r.y * W;
+    uint32_t* ry = rm + (size_t)r.y * W;
+    if (r.op == 5) {
+        if (W == 1) {
+            const uint32_t ax = dx[0], ay = dy[0];
+            if (ay && !(ay & (ay - 1))) { // y singleton
+                const int bit = __ffs(ay) - 1 + s;
+                if (bit >= 0 && bit < 32 && ((ax >> bit) & 1u)) atomicOr(rx, 1u << bit);
+            }
+            if (ax && !(ax & (ax - 1))) {
+                const int bit = __ffs(ax) - 1 - s;
+                if (bit >= 0 && bit < 32 && ((ay >> bit) & 1u)) atomicOr(ry, 1u << bit);
+            }
+            return;
+        }
+        if (dom_size<W>(dy) == 1) or_bit(rx, dx, dom_first<W>(dy) + s, NB);
+        if (dom_size<W>(dx) == 1) or_bit(ry, dy, dom_first<W>(dx) - s, NB);
         return;
     }
     if (dom_empty<W>(dx) || dom_empty<W>(dy)) return;
-    switch (op) {
-    case 0: // x < y + k : x keeps v < max(y)+k ; y keeps w > min(x)-k
-        or_range<W>(rx, dx, clampbit((i128)offy + dom_last<W>(dy) + k - offx, NB), NB);
-        or_range<W>(ry, dy, -1, clampbit((i128)offx + dom_first<W>(dx) - k - offy, NB));
+    switch (r.op) {
+    case 0:
+        or_range<W>(rx, dx, dom_last<W>(dy) + s, NB);
+        or_range<W>(ry, dy, -1, dom_first<W>(dx) - s);
         break;
-    case 1: // x <= y + k
-        or_range<W>(rx, dx, clampbit((i128)offy + dom_last<W>(dy) + k + 1 - offx, NB), NB);
-        or_range<W>(ry, dy, -1, clampbit((i128)offx + dom_first<W>(dx) - k - 1 - offy, NB));
+    case 1:
+        or_range<W>(rx, dx, dom_last<W>(dy) + s + 1, NB);
+        or_range<W>(ry, dy, -1, dom_first<W>(dx) - s - 1);
         break;
-    case 2: // x > y + k : x keeps v > min(y)+k ; y keeps w < max(x)-k
-        or_range<W>(rx, dx, -1, clampbit((i128)offy + dom_first<W>(dy) + k - offx, NB));
-        or_range<W>(ry, dy, clampbit((i128)offx + dom_last<W>(dx) - k - offy, NB), NB);
+    case 2:
+        or_range<W>(rx, dx, -1, dom_first<W>(dy) + s);
+        or_range<W>(ry, dy, dom_last<W>(dx) - s, NB);
         break;
-    case 3: // x >= y + k
-        or_range<W>(rx, dx, -1, clampbit((i128)offy + dom_first<W>(dy) + k - 1 - offx, NB));
-        or_range<W>(ry, dy, clampbit((i128)offx + dom_last<W>(dx) - k + 1 - offy, NB), NB);
+    case 3:
+        or_range<W>(rx, dx, -1, dom_first<W>(dy) + s - 1);
+        or_range<W>(ry, dy, dom_last<W>(dx) - s + 1, NB);
         break;
-    default: { // x = y + k, domain consistent: keep_x = D(y) << s, keep_y = D(x) >> s
-        i128 s128 = (i128)offy + k - offx;
-        long long s = s128 > (i128)(NB + 64) ? (long long)(NB + 64)
-                                             : (s128 < -(i128)(NB + 64) ? -(long long)(NB + 64) : (long long)s128);
+    default:
 #pragma unroll
         for (int w = 0; w < W; ++w) {
-            uint32_t mx = dx[w] & ~shifted_word<W>(dy, w, s);
+            const uint32_t mx = dx[w] & ~shifted_word<W>(dy, w, s);
             if (mx) atomicOr(rx + w, mx);
-            uint32_t my = dy[w] & ~shifted_word<W>(dx, w, -s);
+            const uint32_t my = dy[w] & ~shifted_word<W>(dx, w, -s);
             if (my) atomicOr(ry + w, my);
         }
         break;
-    }
     }
 }
 
@@ -553,6 +564,8 @@ struct RoundCtx {
     int16_t* mates;     // [total_members] persistent warm-start matchings
     uint32_t* post;     // [total_members * W] GAC post-states (null: skip test disabled)
     int8_t* post_ok;    // [na]
+    uint32_t* chg0;     // [ceil(n/32)] vars changed since the last fixpoint (round-1 triggers)
+    uint32_t* chg1;     // [ceil(n/32)] second buffer (null: triggers disabled, full sweeps)
     uint8_t* scratch;   // per-warp GAC scratch
     int scratch_stride; // bytes per warp
     const uint8_t* enabled;
@@ -571,23 +584,48 @@ __device__ __forceinline__ WarpScratch warp_scratch(const RoundCtx& R, int warp)
 }
 
 
-// Phase A: every propagator against the frozen domains. *s_err receives DERR_OVERFLOW.
+__device__ __forceinline__ bool trig_bit(const uint32_t* t, int v) { return (t[v >> 5] >> (v & 31)) & 1u; }
+
+// Phase A: every triggered propagator against the frozen domains (trig == null: all of them).
+// A propagator is triggered when a variable of its scope changed in the previous apply. An
+// untriggered propagator sees exactly the domains of its last evaluation, whose removals are
+// already applied, so skipping it changes no domain, no "changed" flag and no round count.
+// *s_err receives DERR_OVERFLOW.
 template <int W>
-__device__ __forceinline__ void run_propagators(const DevModel& M, const RoundCtx& R, int* s_err) {
+__device__ __forceinline__ void run_propagators(const DevModel& M, const RoundCtx& R, int* s_err,
+                                                const uint32_t* trig) {
     const int tid = threadIdx.x, T = blockDim.x, nw = T >> 5, warp = tid >> 5, lane = tid & 31;
     const int ad_warps = M.na < nw ? M.na : nw;
     const int prop_threads = nw > ad_warps ? (nw - ad_warps) * 32 : T;
     if (tid < prop_threads) {
-        for (int c = tid; c < M.nr; c += prop_threads)
-            if (!R.enabled || R.enabled[c]) prop_relbin<W>(M, c, R.dom, R.rm);
-        for (int c = tid; c < M.nl; c += prop_threads)
-            if (!R.enabled || R.enabled[M.nr + c])
-                if (!prop_linear<W>(M, c, R.dom, R.rm)) *s_err = DERR_OVERFLOW;
+        for (int c = tid; c < M.nr; c += prop_threads) {
+            if (R.enabled && !R.enabled[c]) continue;
+            if (trig) {
+                const int2 xy = *reinterpret_cast<const int2*>(M.rb + c);
+                if (!trig_bit(trig, xy.x) && (xy.y < 0 || !trig_bit(trig, xy.y))) continue;
+            }
+            prop_relbin<W>(M, c, R.dom, R.rm);
+        }
+        for (int c = tid; c < M.nl; c += prop_threads) {
+            if (R.enabled && !R.enabled[M.nr + c]) continue;
+            if (trig) {
+                bool hit = false;
+                for (int t = M.lin_start[c]; t < M.lin_start[c + 1] && !hit; ++t) hit = trig_bit(trig, M.lin_var[t]);
+                if (!hit) continue;
+            }
+            if (!prop_linear<W>(M, c, R.dom, R.rm)) *s_err = DERR_OVERFLOW;
+        }
     }
     if (warp >= nw - ad_warps) {
         const WarpScratch ws = warp_scratch<W>(R, warp);
         for (int a = warp - (nw - ad_warps); a < M.na; a += ad_warps) {
             if (R.enabled && !R.enabled[M.nr + M.nl + a]) continue;
+            if (trig) {
+                const int b = M.ad_start[a], e = M.ad_start[a + 1];
+                bool hit = false;
+                for (int t = b + lane; t < e; t += 32) hit |= trig_bit(trig, M.ad_var[t]);
+                if (!__any_sync(FULL, hit)) continue;
+            }
             if (R.alldiff)
                 prop_alldiff_gac<W>(M, a, R.dom, R.rm, R.mates + M.ad_start[a], ws, lane, R.exact_wipe,
                                     R.post ? R.post + (size_t)M.ad_start[a] * W : nullptr, R.post_ok + a);
@@ -600,25 +638,30 @@ __device__ __forceinline__ void run_propagators(const DevModel& M, const RoundCt
 // failed_var (when non-null) receives the lowest empty var id on failure.
 template <int W>
 __device__ __forceinline__ int apply_removals(const DevModel& M, const RoundCtx& R, int* s_err, int* s_min,
-                                              int* failed_var) {
+                                              int* failed_var, uint32_t* chg_out) {
     const int tid = threadIdx.x, T = blockDim.x;
     int changed = 0, empty_min = 0x7fffffff;
     for (int v = tid; v < M.n; v += T) {
         uint32_t* d = R.dom + (size_t)v * W;
         uint32_t* r = R.rm + (size_t)v * W;
         uint32_t any = 0;
+        bool vch = false;
 #pragma unroll
         for (int w = 0; w < W; ++w) {
             uint32_t rw = r[w], dw = d[w];
             if (rw) {
                 if (dw & rw) {
-                    changed = 1;
+                    vch = true;
                     dw &= ~rw;
                     d[w] = dw;
                 }
                 r[w] = 0;
             }
             any |= dw;
+        }
+        if (vch) {
+            changed = 1;
+            if (chg_out) atomicOr(chg_out + (v >> 5), 1u << (v & 31));
         }
         if (!any && v < empty_min) empty_min = v;
     }
@@ -639,26 +682,33 @@ __device__ __forceinline__ int apply_removals(const DevModel& M, const RoundCtx&
     return R_FAILED;
 }
 
-template <int W>
-__device__ __forceinline__ int block_round(const DevModel& M, const RoundCtx& R, int* s_err, int* s_min,
-                                           int* failed_var) {
-    run_propagators<W>(M, R, s_err);
-    __syncthreads();
-    return apply_removals<W>(M, R, s_err, s_min, failed_var);
-}
-
-// propagate_fixpoint (propagation.cpp:516-532); *rounds counts every round including the last
+// propagate_fixpoint (propagation.cpp:516-532); *rounds counts every round including the last.
+// first_all: evaluate every propagator in round 1; otherwise round 1 is triggered by the vars
+// set in R.chg0 (the caller's branch decision). Both trigger buffers are left dirty.
 template <int W>
 __device__ int block_fixpoint(const DevModel& M, const RoundCtx& R, int* s_err, int* s_min, int max_rounds,
-                              int* rounds, int* failed_var) {
+                              int* rounds, int* failed_var, bool first_all) {
+    const int tid = threadIdx.x, T = blockDim.x;
+    const int nb = (M.n + 31) >> 5;
+    uint32_t* cur = R.chg0;
+    uint32_t* nxt = R.chg1;
+    bool all = first_all || !R.chg1;
     int r = 0;
     for (;;) {
-        const int st = block_round<W>(M, R, s_err, s_min, failed_var);
+        if (nxt)
+            for (int i = tid; i < nb; i += T) nxt[i] = 0;
+        run_propagators<W>(M, R, s_err, all ? nullptr : cur);
+        __syncthreads();
+        const int st = apply_removals<W>(M, R, s_err, s_min, failed_var, nxt);
         ++r;
         if (st != R_CHANGED || (max_rounds > 0 && r >= max_rounds)) {
             *rounds = r;
             return st;
         }
+        uint32_t* t = cur;
+        cur = nxt;
+        nxt = t;
+        all = false;
     }
 }
 

@@ -129,11 +129,16 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
     uint32_t* bestkey = reinterpret_cast<uint32_t*>(smem + L.bestkey);
     uint32_t* post = L.has_post ? reinterpret_cast<uint32_t*>(smem + L.post) : nullptr;
     int8_t* post_ok = reinterpret_cast<int8_t*>(smem + L.post_ok);
-    RoundCtx R{dom, rm, mates, post, post_ok, smem + L.scratch, L.stride, nullptr, P.alldiff, P.exact_wipe};
+    uint32_t* chg0 = L.has_chg ? reinterpret_cast<uint32_t*>(smem + L.chg) : nullptr;
+    uint32_t* chg1 = L.has_chg ? chg0 + ((n + 31) >> 5) : nullptr;
+    const int nbw = (n + 31) >> 5;
+    RoundCtx R{dom, rm, mates, post, post_ok, chg0, chg1, smem + L.scratch, L.stride, nullptr, P.alldiff,
+               P.exact_wipe};
+    bool first_all = true; // the root's first round evaluates every propagator
     uint32_t* frames = P.frames + (size_t)ctx * P.frame_cap * NWP;
     int32_t* meta = P.frame_meta + (size_t)ctx * P.frame_cap * 4;
     WorkState* ws = P.ws;
-    const size_t OS = NWP + round4((size_t)KW + 1);
+    const size_t OS = NWP + round4((size_t)KW + 2); // outbox: domains | path key | depth | branch var
 
     for (size_t i = tid; i < NWP; i += T) rm[i] = 0;
     for (int i = tid; i < M.total_members; i += T) mates[i] = -1;
@@ -194,12 +199,17 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
         copy4_cg(dom, ob, NWP);
         for (int i = tid; i < KW; i += T) path[i] = __ldcg(ob + NWP + i);
         depth = (int)__ldcg(ob + NWP + KW);
+        const int tvar = (int)__ldcg(ob + NWP + KW + 1);
+        if (chg0)
+            for (int i = tid; i < 2 * nbw; i += T) chg0[i] = 0;
         __syncthreads();
         if (tid == 0) {
+            if (chg0) chg0[tvar >> 5] |= 1u << (tvar & 31);
             __threadfence();
             atomicExch(&P.outbox_busy[got], 0);
         }
         sp = base = 0;
+        first_all = false;
         return true;
     };
 
@@ -249,6 +259,7 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
                             any |= d[w];
                         }
                         empty = any == 0;
+                        if (chg0) chg0[obj >> 5] |= 1u << (obj & 31);
                     }
                 }
                 s_flag = empty;
@@ -259,7 +270,8 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
         }
         if (!backtrack) {
             int r = 0;
-            const int st = block_fixpoint<W>(M, R, &s_err, &s_min, 0, &r, nullptr);
+            const int st = block_fixpoint<W>(M, R, &s_err, &s_min, 0, &r, nullptr, first_all);
+            first_all = false;
             rounds += (unsigned long long)r;
             if (st == R_ERROR) {
                 if (tid == 0) {
@@ -352,6 +364,8 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
                 }
                 const int bit = dom_first<W>(dom + (size_t)sel * W);
                 copy4(frames + (size_t)sp * NWP, dom, NWP);
+                if (chg0)
+                    for (int i = tid; i < 2 * nbw; i += T) chg0[i] = 0;
                 if (tid == 0) {
                     meta[sp * 4 + 0] = sel;
                     meta[sp * 4 + 1] = bit;
@@ -363,6 +377,7 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
                 }
                 __syncthreads();
                 if (tid < W) dom[(size_t)sel * W + tid] = (tid == (bit >> 5)) ? (1u << (bit & 31)) : 0u;
+                if (tid == 0 && chg0) chg0[sel >> 5] |= 1u << (sel & 31);
                 ++sp;
                 ++depth;
                 const int want = s_flag;
@@ -379,7 +394,10 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
                         ob[i] = x;
                     }
                     for (int i = tid; i < KW; i += T) ob[NWP + i] = path_right_word(path[i], i, fdepth);
-                    if (tid == 0) ob[NWP + KW] = (uint32_t)(fdepth + 1);
+                    if (tid == 0) {
+                        ob[NWP + KW] = (uint32_t)(fdepth + 1);
+                        ob[NWP + KW + 1] = (uint32_t)fvar;
+                    }
                     __syncthreads();
                     if (tid == 0) {
                         P.outbox_busy[ctx] = 1;
@@ -408,10 +426,13 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
         }
         --sp;
         copy4(dom, frames + (size_t)sp * NWP, NWP);
+        if (chg0)
+            for (int i = tid; i < 2 * nbw; i += T) chg0[i] = 0;
         const int var = meta[sp * 4 + 0], bit = meta[sp * 4 + 1], d = meta[sp * 4 + 2];
         __syncthreads();
         if (tid == 0) {
             dom[(size_t)var * W + (bit >> 5)] &= ~(1u << (bit & 31));
+            if (chg0) chg0[var >> 5] |= 1u << (var & 31);
             if (KW > 0) { // path: bit d = 1, everything deeper cleared
                 const int last = depth < KW * 32 ? depth : KW * 32 - 1;
                 for (int i = d >> 5; i <= (last >> 5); ++i) path[i] = path_right_word(path[i], i, d);
@@ -446,11 +467,13 @@ __global__ void __launch_bounds__(1024) propagate_kernel(const PropParams P, uin
     const DevModel& M = P.M;
     const int tid = threadIdx.x, T = blockDim.x, nw = T >> 5;
     const size_t NW = (size_t)M.n * W, NWP = round4(NW);
-    const SmemLayout L = smem_layout(W, M.n, M.total_members, nw, 0, dom_in_smem);
+    const SmemLayout L = smem_layout(W, M.n, M.total_members, nw, 0, dom_in_smem, M.na);
     uint32_t* dom = dom_in_smem ? reinterpret_cast<uint32_t*>(smem + L.dom) : gscratch;
     uint32_t* rm = dom_in_smem ? reinterpret_cast<uint32_t*>(smem + L.rm) : gscratch + NWP;
     int16_t* mates = reinterpret_cast<int16_t*>(smem + L.mates);
-    RoundCtx R{dom, rm, mates, nullptr, nullptr, smem + L.scratch, L.stride, P.enabled, P.alldiff, 1};
+    uint32_t* chg0 = L.has_chg ? reinterpret_cast<uint32_t*>(smem + L.chg) : nullptr;
+    RoundCtx R{dom, rm, mates, nullptr, nullptr, chg0, L.has_chg ? chg0 + ((M.n + 31) >> 5) : nullptr,
+               smem + L.scratch, L.stride, P.enabled, P.alldiff, 1};
     for (size_t i = tid; i < NWP; i += T) {
         dom[i] = P.dom[i];
         rm[i] = 0;
@@ -459,14 +482,14 @@ __global__ void __launch_bounds__(1024) propagate_kernel(const PropParams P, uin
     if (tid == 0) s_err = 0;
     __syncthreads();
     if (P.removals_only) {
-        run_propagators<W>(M, R, &s_err);
+        run_propagators<W>(M, R, &s_err, nullptr);
         __syncthreads();
         for (size_t i = tid; i < NWP; i += T) P.out[i] = rm[i] & dom[i];
         if (tid == 0) P.result[4] = s_err;
         return;
     }
     int rounds = 0, fv = -1;
-    const int st = block_fixpoint<W>(M, R, &s_err, &s_min, P.max_rounds, &rounds, &fv);
+    const int st = block_fixpoint<W>(M, R, &s_err, &s_min, P.max_rounds, &rounds, &fv, true);
     for (size_t i = tid; i < NWP; i += T) P.dom[i] = dom[i];
     if (tid == 0) {
         P.result[0] = st == R_FAILED;
