@@ -166,6 +166,18 @@ typedef int32_t (*cubics_solution_cb)(void* user, const int64_t* values, int32_t
 int cubics_solve_satisfy(const cubics_model* m, const cubics_search_config* cfg,
                          cubics_solution_cb cb, void* user, cubics_result* out);
 
+/* fd::enumerate_solutions (search.hpp:65-66) in one call: every solution, in the reference's DFS
+ * order, as one row-major int64 array (count x n_vars) owned by the library; free it with
+ * cubics_solutions_free. No per-solution callback crosses the ABI. */
+typedef struct cubics_solutions {
+    uint64_t count;
+    int32_t n_vars;
+    int64_t* values;
+} cubics_solutions;
+int cubics_enumerate(const cubics_model* m, const cubics_search_config* cfg, cubics_solutions** out_solutions,
+                     cubics_result* out);
+void cubics_solutions_free(cubics_solutions* s);
+
 /* best_values (n_vars entries, may be NULL) receives the optimal / last incumbent. */
 int cubics_solve_optimize(const cubics_model* m, const cubics_search_config* cfg,
                           int64_t* best_values, cubics_result* out);

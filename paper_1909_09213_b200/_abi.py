@@ -89,6 +89,10 @@ class Result(C.Structure):
     ]
 
 
+class Solutions(C.Structure):
+    _fields_ = [("count", C.c_uint64), ("n_vars", C.c_int32), ("values", C.POINTER(C.c_int64))]
+
+
 class FixpointResult(C.Structure):
     _fields_ = [("failed", C.c_int32), ("failed_var", C.c_int32), ("rounds", C.c_int32), ("last_status", C.c_int32)]
 
@@ -101,7 +105,8 @@ KEYED_SOLUTION_CB = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.POINTER(C.c_uint32), C.
 EXPORTED = [
     "cubics_model_create", "cubics_model_parse", "cubics_model_free", "cubics_model_describe",
     "cubics_model_var_name", "cubics_model_validate", "cubics_search_config_init",
-    "cubics_solve_satisfy", "cubics_solve_optimize", "cubics_solve_shard", "cubics_propagate",
+    "cubics_solve_satisfy", "cubics_enumerate", "cubics_solutions_free", "cubics_solve_optimize",
+    "cubics_solve_shard", "cubics_propagate",
     "cubics_removals", "cubics_last_error", "cubics_build_info", "cubics_device_count",
 ]
 
@@ -125,6 +130,10 @@ def declare(lib):
     lib.cubics_search_config_init.restype = None
     lib.cubics_solve_satisfy.argtypes = [C.c_void_p, P(SearchConfig), SOLUTION_CB, C.c_void_p, P(Result)]
     lib.cubics_solve_satisfy.restype = C.c_int
+    lib.cubics_enumerate.argtypes = [C.c_void_p, P(SearchConfig), P(P(Solutions)), P(Result)]
+    lib.cubics_enumerate.restype = C.c_int
+    lib.cubics_solutions_free.argtypes = [P(Solutions)]
+    lib.cubics_solutions_free.restype = None
     lib.cubics_solve_optimize.argtypes = [C.c_void_p, P(SearchConfig), P(C.c_int64), P(Result)]
     lib.cubics_solve_optimize.restype = C.c_int
     lib.cubics_solve_shard.argtypes = [C.c_void_p, P(SearchConfig), C.c_int32, C.c_int32, KEYED_SOLUTION_CB,

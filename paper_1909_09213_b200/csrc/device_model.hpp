@@ -81,6 +81,8 @@ struct WorkState {
     uint64_t busy_cycles;  // sum over contexts of clock64 cycles with work
     uint64_t idle_cycles;  // sum over contexts of clock64 cycles waiting for work
     uint64_t lock_fails;   // unused (kept for the debug line)
+    int32_t max_depth;     // deepest solution leaf (parallel): key words that can differ
+    int64_t n_tasks;       // frontier expansion: open nodes emitted at split_depth
 };
 
 struct SearchParams {
@@ -119,6 +121,12 @@ struct SearchParams {
     uint16_t* inc_vals;       // [n]
     int64_t init_bound;
     int32_t has_init_bound;
+    // frontier expansion (parity mode): open nodes at binary depth split_depth become tasks
+    int32_t split_depth;      // -1: off
+    int64_t task_cap;
+    uint32_t* tasks;          // [task_cap][OS] same layout as an outbox slot
+    // seeded parallel run: outbox slots [n_ctx, n_ctx + n_seed) hold pre-published tasks
+    int32_t n_seed;
 };
 
 struct PropParams {

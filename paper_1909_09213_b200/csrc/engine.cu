@@ -18,6 +18,8 @@
 #include <string>
 #include <vector>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "cubics.h"
 #include "device_model.hpp"
 #include "model.hpp"
@@ -56,11 +58,13 @@ struct Arena {
     size_t cap = 0;
 };
 std::mutex g_arena_mu;
-Arena g_arena[64];
+Arena g_arena[2][64];
 Arena g_pinned[64];
 
-uint8_t* device_arena(int dev, size_t bytes) {
-    Arena& a = g_arena[dev];
+// slot 0: per-call search state; slot 1: solution-ordering scratch (kept apart so growing one
+// never invalidates the other while both are live)
+uint8_t* device_arena(int dev, size_t bytes, int slot = 0) {
+    Arena& a = g_arena[slot][dev];
     if (a.cap < bytes) {
         if (a.ptr) cudaFree(a.ptr);
         a.ptr = nullptr;
@@ -287,8 +291,63 @@ int parity_block(const Prepared& P) {
     return std::min(1024, 32 * warps);
 }
 
+// ------------------------------------------------------------------ solution ordering on the device
+__global__ void iota_kernel(uint32_t* p, uint64_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        p[i] = (uint32_t)i;
+}
+
+__global__ void gather_key_word(const uint32_t* keys, int KW, int w, const uint32_t* perm, uint32_t* out, uint64_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = keys[(uint64_t)perm[i] * KW + w];
+}
+
+__global__ void permute_rows(const uint16_t* in, const uint32_t* perm, int nv, uint64_t n, uint16_t* out) {
+    const uint64_t total = n * (uint64_t)nv;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t r = i / nv, c = i % nv;
+        out[i] = in[(uint64_t)perm[r] * nv + c];
+    }
+}
+
+// LSD radix sort of the path keys (only the words that can differ), then one gather of the
+// solution rows: the reference's DFS order without any host-side sort.
+const uint16_t* order_on_device(int dev, const uint32_t* keys, int KW, int used_words, const uint16_t* vals, int nv,
+                                uint64_t count, cudaStream_t st, uint64_t* launches) {
+    size_t temp = 0;
+    CU(cub::DeviceRadixSort::SortPairs(nullptr, temp, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                       (uint32_t*)nullptr, (int)count, 0, 32, st));
+    size_t off = 0;
+    auto take = [&](size_t b) {
+        size_t at = (off + 255) & ~size_t(255);
+        off = at + std::max<size_t>(b, 16);
+        return at;
+    };
+    const size_t a_p0 = take(4 * count), a_p1 = take(4 * count), a_k0 = take(4 * count), a_k1 = take(4 * count),
+                 a_t = take(temp), a_out = take(sizeof(uint16_t) * nv * count);
+    uint8_t* b = device_arena(dev, off, 1);
+    uint32_t *p0 = (uint32_t*)(b + a_p0), *p1 = (uint32_t*)(b + a_p1), *k0 = (uint32_t*)(b + a_k0),
+             *k1 = (uint32_t*)(b + a_k1);
+    const int grid = (int)std::min<uint64_t>(4096, (count + 255) / 256);
+    iota_kernel<<<grid, 256, 0, st>>>(p0, count);
+    ++*launches;
+    for (int w = used_words - 1; w >= 0; --w) {
+        gather_key_word<<<grid, 256, 0, st>>>(keys, KW, w, p0, k0, count);
+        ++*launches;
+        CU(cub::DeviceRadixSort::SortPairs(b + a_t, temp, k0, k1, p0, p1, (int)count, 0, 32, st));
+        std::swap(p0, p1);
+    }
+    const int g2 = (int)std::min<uint64_t>(8192, (count * nv + 255) / 256);
+    uint16_t* out = (uint16_t*)(b + a_out);
+    permute_rows<<<std::max(g2, 1), 256, 0, st>>>(vals, p0, nv, count, out);
+    ++*launches;
+    CU(cudaGetLastError());
+    return out;
+}
+
 struct Records { // solutions copied back from the device
     uint64_t count = 0;
+    bool ordered = false; // vals already in the reference's DFS order
     std::vector<uint16_t> vals;
     std::vector<uint32_t> keys;
     std::vector<uint64_t> stats;
@@ -308,15 +367,31 @@ struct RunOut {
     bool has_first = false;
 };
 
+// Multi-GPU sharding plumbing.
+struct ShardIO {
+    int split_depth = -1;        // > 0: frontier expansion; open nodes at this depth become tasks
+    uint64_t task_cap = 0;
+    uint32_t* task_dev = nullptr; // [task_cap][OS] device buffer (arena slot 1)
+    uint64_t n_tasks = 0;         // out: tasks emitted
+    const std::vector<int32_t>* seeds = nullptr; // seeded run: task indices of this shard
+};
+
+__global__ void gather_tasks(const uint32_t* src, const int32_t* idx, int n, size_t os, uint32_t* dst) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < (size_t)n * os; i += (size_t)gridDim.x * blockDim.x)
+        dst[i] = src[(size_t)idx[i / os] * os + i % os];
+}
+
 // One device search: upload, launch, download.
 void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine, bool record, uint64_t sol_cap,
-                RunOut& out) {
+                RunOut& out, bool want_keys = false, ShardIO* shard = nullptr) {
     const int dev = current_device(cfg.device);
     Prepared P;
     prepare(hm, hm.words.data(), P);
     const int n = P.n;
     const bool parallel = engine == CUBICS_ENGINE_PARALLEL;
-    const int KW = parallel ? static_cast<int>((P.depth_bound + 1 + 31) / 32) : 0;
+    const bool keyed = parallel || (shard && shard->split_depth > 0);
+    const int KW = keyed ? static_cast<int>((P.depth_bound + 1 + 31) / 32) : 0;
+    const int n_seed = (shard && shard->seeds) ? static_cast<int>(shard->seeds->size()) : 0;
     if (parallel && KW > 4096) throw StatusError{CUBICS_E_UNSUPPORTED, "search tree too deep for ordered parallel keys"};
     out.KW = KW;
     // launch geometry
@@ -363,15 +438,16 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
     };
     const size_t a_blob = take(P.blob.bytes.size());
     const size_t a_ws = take(sizeof(WorkState));
-    const uint32_t ring_cap = 2u * (uint32_t)n_ctx;
+    const uint32_t ring_cap = 2u * (uint32_t)n_ctx + (uint32_t)n_seed;
     const size_t a_queue = take(sizeof(unsigned long long) * ring_cap);
-    const size_t a_busy = take(sizeof(int32_t) * n_ctx);
+    const size_t a_busy = take(sizeof(int32_t) * (n_ctx + n_seed));
     const size_t a_hf = take(sizeof(int32_t) * n_ctx);
     const size_t zero_end = off;
     const size_t a_frames = take(sizeof(uint32_t) * NWP * frame_cap * n_ctx);
     const size_t a_meta = take(sizeof(int32_t) * 4 * frame_cap * n_ctx);
     const size_t a_gdom = take(in_smem ? 0 : sizeof(uint32_t) * 2 * NWP * n_ctx);
-    const size_t a_outbox = take(parallel ? sizeof(uint32_t) * OS * n_ctx : 0);
+    const size_t a_outbox = take(parallel ? sizeof(uint32_t) * OS * (n_ctx + n_seed) : 0);
+    const size_t a_seedidx = take(sizeof(int32_t) * n_seed);
     const size_t a_svals = take(sizeof(uint16_t) * n * sol_cap);
     const size_t a_skeys = take(sizeof(uint32_t) * KW * sol_cap);
     const size_t a_sstats = take(parallel ? 0 : sizeof(uint64_t) * 3 * sol_cap);
@@ -388,7 +464,8 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
     try {
         // staging: blob + initial WorkState in pinned memory, one H2D copy
         WorkState w0{};
-        w0.outstanding = n_ctx;
+        w0.outstanding = n_ctx + n_seed;
+        w0.hot.push_ticket = (uint32_t)n_seed;
         const size_t stage_bytes = a_ws + sizeof(WorkState);
         uint8_t* stage = pinned_arena(dev, stage_bytes);
         std::memset(stage, 0, stage_bytes);
@@ -397,6 +474,19 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
         CU(cudaMemcpyAsync(base, stage, stage_bytes, cudaMemcpyHostToDevice, st));
         out.h2d += stage_bytes;
         CU(cudaMemsetAsync(base + a_queue, 0, zero_end - a_queue, st));
+        if (n_seed) { // pre-published tasks: ring tickets 0..n_seed-1 point at outbox slots n_ctx+i
+            std::vector<unsigned long long> ring0(n_seed);
+            for (int i = 0; i < n_seed; ++i) ring0[i] = ((unsigned long long)(i + 1) << 32) | (unsigned)(n_ctx + i);
+            CU(cudaMemcpyAsync(base + a_queue, ring0.data(), sizeof(unsigned long long) * n_seed, cudaMemcpyHostToDevice, st));
+            CU(cudaMemcpyAsync(base + a_seedidx, shard->seeds->data(), sizeof(int32_t) * n_seed, cudaMemcpyHostToDevice, st));
+            out.h2d += (sizeof(unsigned long long) + sizeof(int32_t)) * n_seed;
+            const size_t total = (size_t)n_seed * OS;
+            gather_tasks<<<(int)std::min<size_t>(4096, (total + 255) / 256), 256, 0, st>>>(
+                shard->task_dev, reinterpret_cast<const int32_t*>(base + a_seedidx), n_seed, OS,
+                reinterpret_cast<uint32_t*>(base + a_outbox) + (size_t)n_ctx * OS);
+            CU(cudaGetLastError());
+            out.launches += 1;
+        }
 
         SearchParams S{};
         S.M = P.bind(base + a_blob);
@@ -429,6 +519,10 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
         S.ctx_first_vals = reinterpret_cast<uint16_t*>(base + a_fval);
         S.ctx_has_first = reinterpret_cast<int32_t*>(base + a_hf);
         S.inc_vals = reinterpret_cast<uint16_t*>(base + a_inc);
+        S.split_depth = shard ? shard->split_depth : -1;
+        S.task_cap = shard ? (int64_t)shard->task_cap : 0;
+        S.tasks = shard ? shard->task_dev : nullptr;
+        S.n_seed = n_seed;
 
         CU(cudaEventRecord(e0, st));
 #define LS(w) launch_search<w>(S, n_ctx, block, L.total, st)
@@ -447,10 +541,17 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
         out.rec.count = recorded;
         if (recorded) {
             out.rec.vals.resize(recorded * n);
-            CU(cudaMemcpyAsync(out.rec.vals.data(), base + a_svals, sizeof(uint16_t) * n * recorded,
-                               cudaMemcpyDeviceToHost, st));
+            const uint16_t* src = reinterpret_cast<const uint16_t*>(base + a_svals);
+            if (parallel && KW && n && recorded > 1 && !want_keys) {
+                const int used = std::max(1, std::min(KW, (out.ws.max_depth + 31) / 32));
+                src = order_on_device(dev, reinterpret_cast<const uint32_t*>(base + a_skeys), KW, used, src, n, recorded,
+                                      st, &out.launches);
+                out.rec.ordered = true;
+            }
+            CU(cudaMemcpyAsync(out.rec.vals.data(), src, sizeof(uint16_t) * n * recorded, cudaMemcpyDeviceToHost, st));
             out.d2h += sizeof(uint16_t) * n * recorded;
-            if (KW) {
+            if (!parallel) out.rec.ordered = true;
+            if (KW && want_keys) {
                 out.rec.keys.resize(recorded * KW);
                 CU(cudaMemcpyAsync(out.rec.keys.data(), base + a_skeys, sizeof(uint32_t) * KW * recorded,
                                    cudaMemcpyDeviceToHost, st));
@@ -487,6 +588,7 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
                 out.d2h += sizeof(uint16_t) * n;
             }
         }
+        if (shard) shard->n_tasks = (uint64_t)out.ws.n_tasks;
         if (parallel && hm.goal != CUBICS_SATISFY && n) {
             out.inc_vals.resize(n);
             CU(cudaMemcpyAsync(out.inc_vals.data(), base + a_inc, sizeof(uint16_t) * n, cudaMemcpyDeviceToHost, st));
@@ -586,63 +688,106 @@ extern "C" void cubics_search_config_init(cubics_search_config* c) {
     c->count_only = 0;
 }
 
+namespace {
+// Search for every solution with records materialised (rerun once with an exact buffer when the
+// first guess overflowed), then hand each solution, in the reference's DFS order, to visit(i, row).
+template <class Visit>
+int satisfy_records(const HostModel& m, const cubics_search_config& cfg, bool record, cubics_result* out,
+                    Visit&& visit) {
+    const double t0 = now_ms();
+    std::memset(out, 0, sizeof *out);
+    const int engine = pick_engine(cfg, false);
+    uint64_t cap = default_sol_cap(m, cfg);
+    RunOut r;
+    run_search(m, cfg, engine, record, cap, r);
+    if (record && r.ws.stats[3] > r.rec.count && r.rec.count == cap) { // buffer overflow: rerun exact
+        RunOut r2;
+        run_search(m, cfg, engine, record, r.ws.stats[3], r2);
+        r2.h2d += r.h2d;
+        r2.d2h += r.d2h;
+        r2.launches += r.launches;
+        r = std::move(r2);
+    }
+    fill_result(r, out);
+    const int n = m.n_vars();
+    out->complete = !r.ws.limit_hit && !r.ws.user_stop;
+    out->has_solution = r.ws.stats[3] > 0;
+    if (m.goal != CUBICS_SATISFY && r.rec.count) {
+        const size_t last = r.rec.count - 1;
+        out->objective = m.offset[m.goal_var] + r.rec.vals[last * n + m.goal_var];
+    }
+    if (record && r.rec.count) {
+        std::vector<uint64_t> order(r.rec.count);
+        std::iota(order.begin(), order.end(), 0);
+        if (!r.rec.ordered && r.KW) {
+            const int KW = r.KW;
+            const uint32_t* K = r.rec.keys.data();
+            std::sort(order.begin(), order.end(), [&](uint64_t a, uint64_t b) {
+                return std::lexicographical_compare(K + a * KW, K + (a + 1) * KW, K + b * KW, K + (b + 1) * KW);
+            });
+        }
+        for (uint64_t i = 0; i < order.size(); ++i) {
+            const uint64_t s = order[i];
+            if (!visit(i, r.rec.vals.data() + s * n)) {
+                if (!r.KW && !r.rec.stats.empty()) { // parity: the reference stops right here
+                    out->stats.nodes = r.rec.stats[s * 3 + 0];
+                    out->stats.failures = r.rec.stats[s * 3 + 1];
+                    out->stats.rounds = r.rec.stats[s * 3 + 2];
+                    out->stats.solutions = i + 1;
+                }
+                out->complete = 0;
+                break;
+            }
+        }
+    }
+    out->total_ms = now_ms() - t0;
+    return CUBICS_OK;
+}
+} // namespace
+
 extern "C" int cubics_solve_satisfy(const cubics_model* h, const cubics_search_config* cfg, cubics_solution_cb cb,
                                     void* user, cubics_result* out) {
     if (!h || !cfg || !out) return CUBICS_E_INVALID;
     return guarded([&] {
-        const double t0 = now_ms();
-        std::memset(out, 0, sizeof *out);
         const HostModel& m = h->m;
-        const int engine = pick_engine(*cfg, false);
-        const bool record = cb && !cfg->count_only;
-        uint64_t cap = default_sol_cap(m, *cfg);
-        RunOut r;
-        run_search(m, *cfg, engine, record, cap, r);
-        if (record && r.ws.stats[3] > r.rec.count && r.rec.count == cap) { // buffer overflow: rerun exact
-            RunOut r2;
-            run_search(m, *cfg, engine, record, r.ws.stats[3], r2);
-            r2.h2d += r.h2d;
-            r2.d2h += r.d2h;
-            r2.launches += r.launches;
-            r = std::move(r2);
-        }
-        fill_result(r, out);
         const int n = m.n_vars();
-        out->complete = !r.ws.limit_hit && !r.ws.user_stop;
-        out->has_solution = r.ws.stats[3] > 0;
-        if (m.goal != CUBICS_SATISFY && r.rec.count) {
-            const size_t last = r.rec.count - 1;
-            out->objective = m.offset[m.goal_var] + r.rec.vals[last * n + m.goal_var];
-        }
-        if (record && r.rec.count) {
-            std::vector<uint64_t> order(r.rec.count);
-            std::iota(order.begin(), order.end(), 0);
-            if (r.KW) {
-                const int KW = r.KW;
-                const uint32_t* K = r.rec.keys.data();
-                std::sort(order.begin(), order.end(), [&](uint64_t a, uint64_t b) {
-                    return std::lexicographical_compare(K + a * KW, K + (a + 1) * KW, K + b * KW, K + (b + 1) * KW);
-                });
-            }
-            std::vector<int64_t> vals(n);
-            for (uint64_t i = 0; i < order.size(); ++i) {
-                const uint64_t s = order[i];
-                for (int v = 0; v < n; ++v) vals[v] = m.offset[v] + r.rec.vals[s * n + v];
-                if (!cb(user, vals.data(), n)) {
-                    if (!r.KW && !r.rec.stats.empty()) { // parity: the reference stops right here
-                        out->stats.nodes = r.rec.stats[s * 3 + 0];
-                        out->stats.failures = r.rec.stats[s * 3 + 1];
-                        out->stats.rounds = r.rec.stats[s * 3 + 2];
-                        out->stats.solutions = i + 1;
-                    }
-                    out->complete = 0;
-                    break;
-                }
-            }
-        }
-        out->total_ms = now_ms() - t0;
-        return CUBICS_OK;
+        std::vector<int64_t> vals(n);
+        return satisfy_records(m, *cfg, cb && !cfg->count_only, out, [&](uint64_t, const uint16_t* row) {
+            for (int v = 0; v < n; ++v) vals[v] = m.offset[v] + row[v];
+            return cb(user, vals.data(), n) != 0;
+        });
     });
+}
+
+extern "C" int cubics_enumerate(const cubics_model* h, const cubics_search_config* cfg, cubics_solutions** sols,
+                                cubics_result* out) {
+    if (!h || !cfg || !out || !sols) return CUBICS_E_INVALID;
+    *sols = nullptr;
+    return guarded([&] {
+        const HostModel& m = h->m;
+        const int n = m.n_vars();
+        auto* S = new cubics_solutions{};
+        S->n_vars = n;
+        std::vector<int64_t> buf;
+        int rc = satisfy_records(m, *cfg, !cfg->count_only, out, [&](uint64_t i, const uint16_t* row) {
+            if (buf.empty()) buf.resize(out->stats.solutions * (uint64_t)n);
+            int64_t* dst = buf.data() + i * n;
+            for (int v = 0; v < n; ++v) dst[v] = m.offset[v] + row[v];
+            return true;
+        });
+        S->count = buf.empty() ? 0 : out->stats.solutions;
+        S->values = new int64_t[std::max<size_t>(buf.size(), 1)];
+        std::memcpy(S->values, buf.data(), sizeof(int64_t) * buf.size());
+        *sols = S;
+        out->total_ms += 0;
+        return rc;
+    });
+}
+
+extern "C" void cubics_solutions_free(cubics_solutions* s) {
+    if (!s) return;
+    delete[] s->values;
+    delete s;
 }
 
 extern "C" int cubics_solve_optimize(const cubics_model* h, const cubics_search_config* cfg, int64_t* best_values,
@@ -686,22 +831,95 @@ extern "C" int cubics_solve_shard(const cubics_model* h, const cubics_search_con
     return guarded([&]() -> int {
         const double t0 = now_ms();
         std::memset(out, 0, sizeof *out);
-        if (shard_count != 1) throw StatusError{CUBICS_E_UNSUPPORTED, "multi-shard search not built yet"};
         const HostModel& m = h->m;
+        if (m.goal != CUBICS_SATISFY) throw StatusError{CUBICS_E_UNSUPPORTED, "sharded search enumerates (satisfy goal)"};
         cubics_search_config c = *cfg;
         c.engine = CUBICS_ENGINE_PARALLEL;
-        pick_engine(c, m.goal != CUBICS_SATISFY);
+        pick_engine(c, false);
         const bool record = cb && !c.count_only;
-        RunOut r;
-        run_search(m, c, CUBICS_ENGINE_PARALLEL, record, record ? default_sol_cap(m, c) : 0, r);
-        fill_result(r, out);
-        out->complete = 1;
-        out->has_solution = r.ws.stats[3] > 0;
         const int n = m.n_vars();
         std::vector<int64_t> vals(n);
-        for (uint64_t s = 0; s < r.rec.count; ++s) {
-            for (int v = 0; v < n; ++v) vals[v] = m.offset[v] + r.rec.vals[s * n + v];
-            if (!cb(user, r.rec.keys.data() + s * r.KW, r.KW, vals.data(), n)) break;
+        auto deliver = [&](const RunOut& r) {
+            for (uint64_t s = 0; s < r.rec.count; ++s) {
+                for (int v = 0; v < n; ++v) vals[v] = m.offset[v] + r.rec.vals[s * n + v];
+                if (!cb(user, r.rec.keys.data() + s * r.KW, r.KW, vals.data(), n)) return false;
+            }
+            return true;
+        };
+        if (shard_count == 1) {
+            RunOut r;
+            run_search(m, c, CUBICS_ENGINE_PARALLEL, record, record ? default_sol_cap(m, c) : 0, r, true);
+            fill_result(r, out);
+            out->complete = 1;
+            out->has_solution = r.ws.stats[3] > 0;
+            if (record) deliver(r);
+            out->total_ms = now_ms() - t0;
+            return CUBICS_OK;
+        }
+        // 1. deterministic frontier: expand the tree (in parallel; exact node semantics) until
+        //    the open nodes at the split depth are plentiful; they are numbered in DFS order
+        Prepared P;
+        prepare(m, m.words.data(), P);
+        const int KW = static_cast<int>((P.depth_bound + 1 + 31) / 32);
+        const size_t OS = P.NWP + dev::round4((size_t)KW + 2);
+        const int dev = current_device(c.device);
+        const uint64_t want = 256ull * (uint64_t)shard_count;
+        RunOut ex;
+        ShardIO io;
+        for (int depth = 8;; depth += 4) {
+            io = ShardIO{};
+            io.split_depth = depth;
+            io.task_cap = std::max<uint64_t>(4096, 8 * want);
+            for (;;) {
+                io.task_dev = reinterpret_cast<uint32_t*>(device_arena(dev, sizeof(uint32_t) * OS * io.task_cap, 1));
+                ex = RunOut{};
+                run_search(m, c, CUBICS_ENGINE_PARALLEL, record, record ? default_sol_cap(m, c) : 0, ex, true, &io);
+                if (io.n_tasks <= io.task_cap) break;
+                io.task_cap = io.n_tasks;
+            }
+            if (io.n_tasks >= want || io.n_tasks == 0 || depth >= 64 || (uint64_t)depth >= P.depth_bound) break;
+        }
+        // 2. DFS rank of each task = order of its path key
+        const uint64_t nt = io.n_tasks;
+        std::vector<uint32_t> keys(nt * KW);
+        if (nt)
+            CU(cudaMemcpy2D(keys.data(), sizeof(uint32_t) * KW, io.task_dev + P.NWP, sizeof(uint32_t) * OS,
+                            sizeof(uint32_t) * KW, nt, cudaMemcpyDeviceToHost));
+        std::vector<int32_t> order(nt);
+        std::iota(order.begin(), order.end(), 0);
+        std::sort(order.begin(), order.end(), [&](int32_t x, int32_t y) {
+            return std::lexicographical_compare(keys.begin() + (size_t)x * KW, keys.begin() + (size_t)(x + 1) * KW,
+                                                keys.begin() + (size_t)y * KW, keys.begin() + (size_t)(y + 1) * KW);
+        });
+        std::vector<int32_t> mine;
+        for (uint64_t r = shard_index; r < nt; r += shard_count) mine.push_back(order[r]);
+        // 3. this shard's subtrees, seeded into the parallel engine
+        RunOut run;
+        if (!mine.empty()) {
+            ShardIO seeded;
+            seeded.task_dev = io.task_dev;
+            seeded.seeds = &mine;
+            run_search(m, c, CUBICS_ENGINE_PARALLEL, record, record ? default_sol_cap(m, c) : 0, run, true, &seeded);
+        }
+        fill_result(run, out);
+        if (shard_index == 0) { // nodes above the frontier belong to shard 0
+            out->stats.nodes += ex.ws.stats[0];
+            out->stats.failures += ex.ws.stats[1];
+            out->stats.rounds += ex.ws.stats[2];
+            out->stats.solutions += ex.ws.stats[3];
+        }
+        out->device_ms = run.device_ms + ex.device_ms;
+        out->h2d_bytes += ex.h2d;
+        out->d2h_bytes += ex.d2h + sizeof(uint32_t) * KW * nt;
+        out->kernel_launches += ex.launches;
+        out->complete = 1;
+        out->has_solution = out->stats.solutions > 0;
+        if (record) {
+            if (shard_index == 0 && !deliver(ex)) {
+                out->total_ms = now_ms() - t0;
+                return CUBICS_OK;
+            }
+            if (!mine.empty()) deliver(run);
         }
         out->total_ms = now_ms() - t0;
         return CUBICS_OK;

@@ -135,6 +135,7 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
     RoundCtx R{dom, rm, mates, post, post_ok, chg0, chg1, smem + L.scratch, L.stride, nullptr, P.alldiff,
                P.exact_wipe};
     bool first_all = true; // the root's first round evaluates every propagator
+    int trig_var = -1;     // var changed by the branch that created the current node
     uint32_t* frames = P.frames + (size_t)ctx * P.frame_cap * NWP;
     int32_t* meta = P.frame_meta + (size_t)ctx * P.frame_cap * 4;
     WorkState* ws = P.ws;
@@ -210,11 +211,12 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
         }
         sp = base = 0;
         first_all = false;
+        trig_var = tvar;
         return true;
     };
 
     bool have_work;
-    if (!parallel || ctx == 0) {
+    if (!parallel || (ctx == 0 && !P.n_seed)) {
         copy4(dom, M.init_dom, NWP);
         have_work = true;
     } else {
@@ -223,6 +225,23 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
     __syncthreads();
 
     while (have_work) {
+        bool backtrack = false;
+        if (P.split_depth >= 0 && depth >= P.split_depth) {
+            // ============ frontier expansion: this open node becomes a task (counted by its shard)
+            if (tid == 0) s_ll = (long long)atomicAdd((unsigned long long*)&ws->n_tasks, 1ull);
+            __syncthreads();
+            const long long t = s_ll;
+            if (t < P.task_cap) {
+                uint32_t* tb = P.tasks + (size_t)t * OS;
+                copy4(tb, dom, NWP);
+                for (int i = tid; i < KW; i += T) tb[NWP + i] = path[i];
+                if (tid == 0) {
+                    tb[NWP + KW] = (uint32_t)depth;
+                    tb[NWP + KW + 1] = (uint32_t)trig_var;
+                }
+            }
+            backtrack = true;
+        } else {
         // ================= node entry (descend, search.cpp:80-111)
         ++nodes;
         if (P.node_limit && nodes > P.node_limit) {
@@ -237,7 +256,6 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
             if (optimizing) g_bound = ld_volatile_s64(&ws->bound);
             my_busy = ld_volatile(&P.outbox_busy[ctx]);
         }
-        bool backtrack = false;
         if (optimizing) { // branch-and-bound shrink (:87-101), done by thread 0
             if (tid == 0) {
                 int empty = 0;
@@ -290,7 +308,10 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
             const int sel = select_var<W>(M, dom, P.var_heuristic, s_red);
             if (sel < 0) {
                 // ============ solution leaf (emit_solution, search.cpp:134-156)
-                if (tid == 0) s_ll = parallel ? (long long)atomicAdd((unsigned long long*)&ws->sol_count, 1ull) : (long long)sols;
+                if (tid == 0) {
+                    s_ll = parallel ? (long long)atomicAdd((unsigned long long*)&ws->sol_count, 1ull) : (long long)sols;
+                    if (parallel) atomicMax(&ws->max_depth, depth);
+                }
                 __syncthreads();
                 const unsigned long long idx = (unsigned long long)s_ll;
                 ++sols;
@@ -378,6 +399,7 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
                 __syncthreads();
                 if (tid < W) dom[(size_t)sel * W + tid] = (tid == (bit >> 5)) ? (1u << (bit & 31)) : 0u;
                 if (tid == 0 && chg0) chg0[sel >> 5] |= 1u << (sel & 31);
+                trig_var = sel;
                 ++sp;
                 ++depth;
                 const int want = s_flag;
@@ -412,6 +434,7 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
                 continue;
             }
         }
+        } // node processing
         // ================= backtrack: right branch of the deepest pending frame (:122-131)
         if (parallel) {
             if (tid == 0) s_flag = hot.z;
@@ -439,6 +462,7 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
             }
         }
         depth = d + 1;
+        trig_var = var;
         __syncthreads();
     }
     __syncthreads();

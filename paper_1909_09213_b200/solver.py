@@ -373,13 +373,33 @@ def solve_satisfy(model: Model, cfg: SearchConfig | None = None, cb=None) -> Sat
                          res.h2d_bytes, res.d2h_bytes, res.kernel_launches)
 
 
+def enumerate_array(model: Model, cfg: SearchConfig | None = None):
+    """cubics_enumerate: (numpy int64 array [count, n_vars] in DFS order, SatisfyResult)."""
+    import numpy as np
+
+    cfg = cfg or SearchConfig()
+    res = A.Result()
+    sols = C.POINTER(A.Solutions)()
+    c = cfg.to_c()
+    _check(lib().cubics_enumerate(model.handle, C.byref(c), C.byref(sols), C.byref(res)), "enumerate")
+    try:
+        cnt, nv = sols.contents.count, sols.contents.n_vars
+        if cnt and nv:
+            arr = np.ctypeslib.as_array(sols.contents.values, shape=(cnt, nv)).copy()
+        else:
+            arr = np.zeros((cnt, nv), dtype=np.int64)
+    finally:
+        lib().cubics_solutions_free(sols)
+    return arr, SatisfyResult(_stats(res), bool(res.complete), res.engine, res.contexts, res.device_ms,
+                              res.total_ms, res.h2d_bytes, res.d2h_bytes, res.kernel_launches)
+
+
 def enumerate_solutions(model: Model, cfg: SearchConfig | None = None, stats: SearchStats | None = None):
-    """fd::enumerate_solutions: every solution (values lists) in DFS order."""
-    out = []
-    r = solve_satisfy(model, cfg, lambda s: out.append(s) or True)
+    """fd::enumerate_solutions: every solution (Solution objects) in DFS order."""
+    arr, r = enumerate_array(model, cfg)
     if stats is not None:
         stats.nodes, stats.failures, stats.rounds, stats.solutions = r.stats.as_tuple()
-    return out
+    return [Solution(row) for row in arr.tolist()]
 
 
 def solve_optimize(model: Model, cfg: SearchConfig | None = None) -> OptimizeResult:

@@ -213,3 +213,26 @@ def test_callback_stop_truncates_stats_like_reference():
         ro = O.solve_satisfy(m, S.SearchConfig(), (lambda acc: (lambda s: acc.append(s) or len(acc) < k))([]))
         assert r.stats.as_tuple() == ro.stats.as_tuple()
         assert r.complete is False and len(seen) == k
+
+
+@pytest.mark.parametrize("key", ["nq8|--all", "nq10|--all", "nq12|--all", "magic3|--all", "nq8|--all --fc"])
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_sharded_search_sums_exactly(key, world):
+    # every rank's cubics_solve_shard, run one after another on this GPU; the sum of the shards'
+    # stats is the reference's, and their key-merged solutions are the reference's stream
+    from paper_1909_09213_b200 import distributed as D
+
+    inst, flags = G.split_key(key)
+    m = S.parse_model(G.model_text(inst))
+    cfg = G.cfg_from_flags(flags)
+    tot = [0, 0, 0, 0]
+    streams = []
+    for r in range(world):
+        keyed = []
+        res = S.solve_shard(m, cfg, r, world, lambda k, v, keyed=keyed: keyed.append((tuple(k), v)) or True)
+        tot = [a + b for a, b in zip(tot, res.stats.as_tuple())]
+        streams.append(keyed)
+    g = G.goldens()[key]
+    assert tuple(tot) == G.expected_tuple(g)
+    merged = D.merge_keyed(streams)
+    assert merged == [s.values for s in O.enumerate_solutions(m, cfg)]
