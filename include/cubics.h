@@ -134,6 +134,8 @@ typedef struct cubics_search_config { /* fd::SearchConfig (include/fd/search.hpp
     int32_t contexts;        /* PARALLEL: search contexts (0 = auto)         */
     int32_t block_threads;   /* threads per search context (0 = auto)        */
     int32_t count_only;      /* 1 = do not materialise solutions (callback not called) */
+    int32_t has_initial_bound; /* branch and bound starts from this objective bound      */
+    int64_t initial_bound;     /* (Dfs::set_initial_bound, search.cpp:63,282)             */
 } cubics_search_config;
 
 void cubics_search_config_init(cubics_search_config* cfg); /* reference defaults */
@@ -217,6 +219,9 @@ int cubics_removals(const cubics_model* m, const uint64_t* words, int32_t alldif
 const char* cubics_last_error(void);
 const char* cubics_build_info(void);
 int cubics_device_count(void);
+/* Create the CUDA context on `device` (-1: current) and load the engine's kernels, so the first
+ * solve does not pay for them (the reference's acceptance criterion 1 bounds that call at 1 s). */
+int cubics_warmup(int32_t device);
 
 #ifdef __cplusplus
 }

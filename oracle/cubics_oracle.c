@@ -702,6 +702,8 @@ static int run_dfs(const cubics_model_desc* d, const cubics_search_config* cfg, 
     s.obj = d->goal_var;
     s.cb = cb;
     s.user = user;
+    s.has_bound = cfg->has_initial_bound != 0; /* Dfs::set_initial_bound (search.cpp:63) */
+    s.bound = cfg->initial_bound;
     size_t bytes = sizeof(uint64_t) * (size_t)(m.total + 1);
     s.st.m = &m;
     s.st.W = (uint64_t*)malloc(bytes);

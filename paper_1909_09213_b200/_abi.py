@@ -66,6 +66,8 @@ class SearchConfig(C.Structure):
         ("contexts", C.c_int32),
         ("block_threads", C.c_int32),
         ("count_only", C.c_int32),
+        ("has_initial_bound", C.c_int32),
+        ("initial_bound", C.c_int64),
     ]
 
 
@@ -107,7 +109,7 @@ EXPORTED = [
     "cubics_model_var_name", "cubics_model_validate", "cubics_search_config_init",
     "cubics_solve_satisfy", "cubics_enumerate", "cubics_solutions_free", "cubics_solve_optimize",
     "cubics_solve_shard", "cubics_propagate",
-    "cubics_removals", "cubics_last_error", "cubics_build_info", "cubics_device_count",
+    "cubics_removals", "cubics_last_error", "cubics_build_info", "cubics_device_count", "cubics_warmup",
 ]
 
 
@@ -149,4 +151,6 @@ def declare(lib):
     lib.cubics_build_info.restype = C.c_char_p
     lib.cubics_device_count.argtypes = []
     lib.cubics_device_count.restype = C.c_int
+    lib.cubics_warmup.argtypes = [C.c_int32]
+    lib.cubics_warmup.restype = C.c_int
     return lib

@@ -465,6 +465,8 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
         // staging: blob + initial WorkState in pinned memory, one H2D copy
         WorkState w0{};
         w0.outstanding = n_ctx + n_seed;
+        w0.hot.has_bound = cfg.has_initial_bound ? 1 : 0;
+        w0.bound = cfg.initial_bound;
         w0.hot.push_ticket = (uint32_t)n_seed;
         const size_t stage_bytes = a_ws + sizeof(WorkState);
         uint8_t* stage = pinned_arena(dev, stage_bytes);
@@ -519,6 +521,8 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
         S.ctx_first_vals = reinterpret_cast<uint16_t*>(base + a_fval);
         S.ctx_has_first = reinterpret_cast<int32_t*>(base + a_hf);
         S.inc_vals = reinterpret_cast<uint16_t*>(base + a_inc);
+        S.has_init_bound = cfg.has_initial_bound ? 1 : 0;
+        S.init_bound = cfg.initial_bound;
         S.split_depth = shard ? shard->split_depth : -1;
         S.task_cap = shard ? (int64_t)shard->task_cap : 0;
         S.tasks = shard ? shard->task_dev : nullptr;
@@ -696,7 +700,9 @@ int satisfy_records(const HostModel& m, const cubics_search_config& cfg, bool re
                     Visit&& visit) {
     const double t0 = now_ms();
     std::memset(out, 0, sizeof *out);
-    const int engine = pick_engine(cfg, false);
+    // an objective makes the stream a sequence of incumbents, whose order only the reference
+    // node order reproduces: AUTO picks the parity engine then
+    const int engine = pick_engine(cfg, m.goal != CUBICS_SATISFY);
     uint64_t cap = default_sol_cap(m, cfg);
     RunOut r;
     run_search(m, cfg, engine, record, cap, r);
@@ -1045,6 +1051,39 @@ extern "C" int cubics_removals(const cubics_model* h, const uint64_t* words, int
 #define CUBICS_STR(x) CUBICS_STR2(x)
 extern "C" const char* cubics_build_info(void) {
     return "cubics-b200 abi=1 arch=sm_100a engine=persistent-dfs(parity|parallel) nvcc=" CUBICS_STR(__CUDACC_VER_MAJOR__) "." CUBICS_STR(__CUDACC_VER_MINOR__);
+}
+
+extern "C" int cubics_warmup(int32_t device) {
+    return guarded([&] {
+        current_device(device);
+        CU(cudaFree(nullptr));
+        // one tiny search and one tiny fixpoint per common word count load the kernels
+        HostModel m;
+        m.names = {"a", "b"};
+        m.offset = {1, 1};
+        m.width = {2, 2};
+        m.finish_vars();
+        m.words.assign(m.word_start.back(), 3);
+        m.con_kind = {CUBICS_ALLDIFF};
+        m.con_op = {0};
+        m.con_value = {0};
+        m.con_start = {0, 2};
+        m.term_var = {0, 1};
+        m.term_coeff = {1, 1};
+        cubics_search_config c;
+        cubics_search_config_init(&c);
+        c.device = device;
+        c.count_only = 1;
+        for (int engine : {CUBICS_ENGINE_PARITY, CUBICS_ENGINE_PARALLEL}) {
+            c.engine = engine;
+            RunOut r;
+            run_search(m, c, engine, false, 0, r);
+        }
+        cubics_model h{m};
+        std::vector<uint64_t> w(m.words);
+        cubics_fixpoint_result fr{};
+        return cubics_propagate(&h, w.data(), CUBICS_ARC_CONSISTENT, 0, &fr);
+    });
 }
 
 extern "C" int cubics_device_count(void) {

@@ -92,6 +92,7 @@ class SearchConfig:
     contexts: int = 0
     block_threads: int = 0
     count_only: bool = False
+    initial_bound: int | None = None
 
     def to_c(self) -> A.SearchConfig:
         c = A.SearchConfig()
@@ -99,6 +100,9 @@ class SearchConfig:
                   "node_limit", "engine", "device", "contexts", "block_threads"):
             setattr(c, f, getattr(self, f))
         c.count_only = 1 if self.count_only else 0
+        if self.initial_bound is not None:
+            c.has_initial_bound = 1
+            c.initial_bound = self.initial_bound
         return c
 
 
