@@ -29,7 +29,10 @@ struct DevModel {
     const int64_t* off;  // [n]
     const uint32_t* init_dom; // [n*W]
     int32_t nr;
-    const RelBinRec* rb;
+    const RelBinRec* rb;         // generic records first, then the var-form != records
+    int32_t nr_gen;              // records [0, nr_gen) are not var-form !=
+    const int32_t* ne_start;     // [n+1] var-form != incidence: when v becomes a singleton at bit b,
+    const int2* ne_edge;         //   each edge (p, s) removes bit b + s from var p
     int32_t nl;
     const int32_t* lin_start; // [nl+1]
     const int32_t* lin_op;    // [nl]

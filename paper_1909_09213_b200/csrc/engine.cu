@@ -107,7 +107,8 @@ struct Prepared {
     bool has_empty = false;
     uint64_t depth_bound = 0; // sum(|D| - 1): max binary-tree depth
     Blob blob;
-    size_t o_off, o_dom, o_rb, o_ls, o_lo, o_lb, o_lv, o_lc, o_as, o_av, o_ash;
+    size_t o_off, o_dom, o_rb, o_ls, o_lo, o_lb, o_lv, o_lc, o_as, o_av, o_ash, o_nes, o_nee;
+    int nr_gen = 0;
     std::vector<int> kind_index; // constraint index -> kind-local index (rb | nr+lin | nr+nl+ad)
     std::vector<int64_t> offsets;
     DevModel bind(const uint8_t* base) const {
@@ -118,6 +119,9 @@ struct Prepared {
         M.init_dom = reinterpret_cast<const uint32_t*>(base + o_dom);
         M.nr = nr;
         M.rb = reinterpret_cast<const RelBinRec*>(base + o_rb);
+        M.nr_gen = nr_gen;
+        M.ne_start = reinterpret_cast<const int32_t*>(base + o_nes);
+        M.ne_edge = reinterpret_cast<const int2*>(base + o_nee);
         M.nl = nl;
         M.lin_start = reinterpret_cast<const int32_t*>(base + o_ls);
         M.lin_op = reinterpret_cast<const int32_t*>(base + o_lo);
@@ -242,6 +246,22 @@ void prepare(const HostModel& m, const uint64_t* words, Prepared& P) {
         if (sz == 0) P.has_empty = true;
         P.depth_bound += sz > 0 ? (uint64_t)(sz - 1) : 0;
     }
+    // generic RelBin records first; var-form != records last, mirrored into a per-variable
+    // incidence list for the singleton-event path of the search kernel
+    std::stable_partition(rb.begin(), rb.end(), [](const RelBinRec& r) { return !(r.y >= 0 && r.op == CUBICS_NE); });
+    P.nr_gen = static_cast<int>(std::count_if(rb.begin(), rb.end(), [](const RelBinRec& r) { return !(r.y >= 0 && r.op == CUBICS_NE); }));
+    std::vector<int32_t> nes(n + 1, 0);
+    for (size_t i = P.nr_gen; i < rb.size(); ++i) {
+        nes[rb[i].y + 1]++; // y singleton -> removes from x
+        nes[rb[i].x + 1]++; // x singleton -> removes from y
+    }
+    for (int v = 0; v < n; ++v) nes[v + 1] += nes[v];
+    std::vector<int2> nee(nes[n]);
+    std::vector<int32_t> fill(nes.begin(), nes.end() - 1);
+    for (size_t i = P.nr_gen; i < rb.size(); ++i) {
+        nee[fill[rb[i].y]++] = make_int2(rb[i].x, rb[i].s);
+        nee[fill[rb[i].x]++] = make_int2(rb[i].y, -rb[i].s);
+    }
     P.offsets = m.offset;
     P.o_off = P.blob.add(m.offset.data(), m.offset.size());
     P.o_dom = P.blob.add(dom.data(), dom.size());
@@ -254,6 +274,8 @@ void prepare(const HostModel& m, const uint64_t* words, Prepared& P) {
     P.o_as = P.blob.add(as.data(), as.size());
     P.o_av = P.blob.add(av.data(), av.size());
     P.o_ash = P.blob.add(ash.data(), ash.size());
+    P.o_nes = P.blob.add(nes.data(), nes.size());
+    P.o_nee = P.blob.add(nee.data(), nee.size());
 }
 
 int current_device(int want) {

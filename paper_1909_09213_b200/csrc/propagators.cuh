@@ -566,6 +566,7 @@ struct RoundCtx {
     int8_t* post_ok;    // [na]
     uint32_t* chg0;     // [ceil(n/32)] vars changed since the last fixpoint (round-1 triggers)
     uint32_t* chg1;     // [ceil(n/32)] second buffer (null: triggers disabled, full sweeps)
+    bool ne_events;     // var-form != handled by the singleton-event path (search kernel)
     uint8_t* scratch;   // per-warp GAC scratch
     int scratch_stride; // bytes per warp
     const uint8_t* enabled;
@@ -598,13 +599,43 @@ __device__ __forceinline__ void run_propagators(const DevModel& M, const RoundCt
     const int ad_warps = M.na < nw ? M.na : nw;
     const int prop_threads = nw > ad_warps ? (nw - ad_warps) * 32 : T;
     if (tid < prop_threads) {
-        for (int c = tid; c < M.nr; c += prop_threads) {
+        const int nr_loop = R.ne_events ? M.nr_gen : M.nr;
+        for (int c = tid; c < nr_loop; c += prop_threads) {
             if (R.enabled && !R.enabled[c]) continue;
             if (trig) {
                 const int2 xy = *reinterpret_cast<const int2*>(M.rb + c);
                 if (!trig_bit(trig, xy.x) && (xy.y < 0 || !trig_bit(trig, xy.y))) continue;
             }
             prop_relbin<W>(M, c, R.dom, R.rm);
+        }
+        if (R.ne_events && M.nr_gen < M.nr) {
+            // x != y + k prunes only from a singleton side, and a singleton that did not change in
+            // the last apply has had its removals applied already: walk the incidence lists of the
+            // variables that just became singletons (every singleton in the root's first round).
+            const int pw = prop_threads >> 5;
+            constexpr int NB = W * 32;
+            for (int base = warp * 32; base < M.n; base += pw * 32) {
+                const int v = base + lane;
+                int b = -1;
+                if (v < M.n && (!trig || trig_bit(trig, v)) && M.ne_start[v] < M.ne_start[v + 1]) {
+                    const uint32_t* dv = R.dom + (size_t)v * W;
+                    if (dom_size<W>(dv) == 1) b = dom_first<W>(dv);
+                }
+                unsigned ev = __ballot_sync(FULL, b >= 0);
+                while (ev) {
+                    const int l = __ffs(ev) - 1;
+                    ev &= ev - 1;
+                    const int vv = base + l, bb = __shfl_sync(FULL, b, l);
+                    for (int e = M.ne_start[vv] + lane; e < M.ne_start[vv + 1]; e += 32) {
+                        const int2 ps = M.ne_edge[e];
+                        const int bit = bb + ps.y;
+                        if (bit >= 0 && bit < NB) {
+                            const uint32_t m = (1u << (bit & 31)) & R.dom[(size_t)ps.x * W + (bit >> 5)];
+                            if (m) atomicOr(R.rm + (size_t)ps.x * W + (bit >> 5), m);
+                        }
+                    }
+                }
+            }
         }
         for (int c = tid; c < M.nl; c += prop_threads) {
             if (R.enabled && !R.enabled[M.nr + c]) continue;

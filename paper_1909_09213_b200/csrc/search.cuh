@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
     uint32_t* chg0 = L.has_chg ? reinterpret_cast<uint32_t*>(smem + L.chg) : nullptr;
     uint32_t* chg1 = L.has_chg ? chg0 + ((n + 31) >> 5) : nullptr;
     const int nbw = (n + 31) >> 5;
-    RoundCtx R{dom, rm, mates, post, post_ok, chg0, chg1, smem + L.scratch, L.stride, nullptr, P.alldiff,
+    RoundCtx R{dom, rm, mates, post, post_ok, chg0, chg1, L.has_chg, smem + L.scratch, L.stride, nullptr, P.alldiff,
                P.exact_wipe};
     bool first_all = true; // the root's first round evaluates every propagator
     int trig_var = -1;     // var changed by the branch that created the current node
@@ -496,7 +496,7 @@ __global__ void __launch_bounds__(1024) propagate_kernel(const PropParams P, uin
     uint32_t* rm = dom_in_smem ? reinterpret_cast<uint32_t*>(smem + L.rm) : gscratch + NWP;
     int16_t* mates = reinterpret_cast<int16_t*>(smem + L.mates);
     uint32_t* chg0 = L.has_chg ? reinterpret_cast<uint32_t*>(smem + L.chg) : nullptr;
-    RoundCtx R{dom, rm, mates, nullptr, nullptr, chg0, L.has_chg ? chg0 + ((M.n + 31) >> 5) : nullptr,
+    RoundCtx R{dom, rm, mates, nullptr, nullptr, chg0, L.has_chg ? chg0 + ((M.n + 31) >> 5) : nullptr, false,
                smem + L.scratch, L.stride, P.enabled, P.alldiff, 1};
     for (size_t i = tid; i < NWP; i += T) {
         dom[i] = P.dom[i];
