@@ -57,7 +57,8 @@ struct Arena {
     void* ptr = nullptr;
     size_t cap = 0;
 };
-std::mutex g_arena_mu;
+// one search at a time per device: the arenas below are reused by every call
+std::recursive_mutex g_dev_mu[64];
 Arena g_arena[2][64];
 Arena g_pinned[64];
 
@@ -407,6 +408,7 @@ __global__ void gather_tasks(const uint32_t* src, const int32_t* idx, int n, siz
 void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine, bool record, uint64_t sol_cap,
                 RunOut& out, bool want_keys = false, ShardIO* shard = nullptr) {
     const int dev = current_device(cfg.device);
+    std::lock_guard<std::recursive_mutex> lock(g_dev_mu[dev]);
     Prepared P;
     prepare(hm, hm.words.data(), P);
     const int n = P.n;
@@ -891,6 +893,7 @@ extern "C" int cubics_solve_shard(const cubics_model* h, const cubics_search_con
         const int KW = static_cast<int>((P.depth_bound + 1 + 31) / 32);
         const size_t OS = P.NWP + dev::round4((size_t)KW + 2);
         const int dev = current_device(c.device);
+        std::lock_guard<std::recursive_mutex> lock(g_dev_mu[dev]); // the task buffer lives across two runs
         const uint64_t want = 256ull * (uint64_t)shard_count;
         RunOut ex;
         ShardIO io;
@@ -959,6 +962,7 @@ int run_prop(const cubics_model* h, const uint64_t* words_in, uint64_t* words_ou
              const int32_t* cons, int32_t n_cons, bool removals_only, cubics_fixpoint_result* fr) {
     const HostModel& m = h->m;
     const int dev = current_device(-1);
+    std::lock_guard<std::recursive_mutex> lock(g_dev_mu[dev]);
     Prepared P;
     // the removal subset decides which constraints are evaluated (INT64_MIN pre-check included)
     HostModel sub;

@@ -13,6 +13,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 
 #include "device_model.hpp"
 #include "layout.hpp"
@@ -282,40 +283,59 @@ __device__ __forceinline__ unsigned long long ballot64(bool a, bool b) {
     return (unsigned long long)__ballot_sync(FULL, a) | ((unsigned long long)__ballot_sync(FULL, b) << 32);
 }
 
+template <bool TWO>
+using MemberSet = typename std::conditional<TWO, unsigned long long, unsigned>::type;
+
+template <bool TWO>
+__device__ __forceinline__ MemberSet<TWO> ballot_m(bool a, bool b) {
+    if constexpr (TWO) return ballot64(a, b);
+    else return __ballot_sync(FULL, a);
+}
+
+template <bool TWO>
+__device__ __forceinline__ int ffs_m(MemberSet<TWO> x) {
+    if constexpr (TWO) return __ffsll((long long)x) - 1;
+    else return __ffs(x) - 1;
+}
+
 // Bit-parallel BFS augmenting path from member r (uniform). Updates mate[], MV. true on success.
-template <int W>
-__device__ bool gac_augment(int r, const uint32_t (&D0)[W], const uint32_t (&D1)[W], bool h0, bool h1,
-                            int& m0, int& m1, uint32_t (&MV)[W], const WarpScratch& ws, int lane) {
+// Each member remembers the BFS layer it entered (lay0/lay1, registers), so the walk back needs
+// no shared memory: at layer l the predecessor of value j is a member of layer l containing j.
+template <int W, bool TWO>
+__device__ bool gac_augment(int r, const uint32_t (&D0)[W], const uint32_t (&D1)[W], bool h0, bool h1, int& m0,
+                            int& m1, uint32_t (&MV)[W], int lane) {
+    using MS = MemberSet<TWO>;
     uint32_t vis[W];
 #pragma unroll
     for (int w = 0; w < W; ++w) vis[w] = 0;
-    unsigned long long front = 1ull << r;
-    if (lane == 0) ws.layers[0] = front;
+    MS front = (MS)1 << r;
+    int lay0 = lane == r ? 0 : -1, lay1 = (TWO && lane + 32 == r) ? 0 : -1;
     int L = 0;
     for (;;) {
-        const bool f0 = h0 && ((front >> lane) & 1ull), f1 = h1 && ((front >> (lane + 32)) & 1ull);
+        const bool f0 = h0 && ((front >> lane) & 1u);
+        bool f1 = false;
+        if constexpr (TWO) f1 = h1 && ((front >> (lane + 32)) & 1ull);
         uint32_t nv[W];
         uint32_t any = 0;
         int found = -1;
 #pragma unroll
         for (int w = 0; w < W; ++w) {
-            uint32_t c = (f0 ? D0[w] : 0u) | (f1 ? D1[w] : 0u);
+            uint32_t c = f0 ? D0[w] : 0u;
+            if constexpr (TWO) c |= f1 ? D1[w] : 0u;
             nv[w] = __reduce_or_sync(FULL, c) & ~vis[w];
             vis[w] |= nv[w];
             any |= nv[w];
-            uint32_t fr = nv[w] & ~MV[w];
+            const uint32_t fr = nv[w] & ~MV[w];
             if (fr && found < 0) found = w * 32 + __ffs(fr) - 1;
         }
         if (!any) return false;
         if (found >= 0) { // walk back through the layers, re-matching along the path
             int j = found;
             for (int l = L;; --l) {
-                __syncwarp();
-                const unsigned long long lay = ws.layers[l];
-                const bool c0 = h0 && ((lay >> lane) & 1ull) && testbit_r<W>(D0, j);
-                const bool c1 = h1 && ((lay >> (lane + 32)) & 1ull) && testbit_r<W>(D1, j);
-                const unsigned long long bal = ballot64(c0, c1);
-                const int k = __ffsll((long long)bal) - 1;
+                const bool c0 = h0 && lay0 == l && testbit_r<W>(D0, j);
+                bool c1 = false;
+                if constexpr (TWO) c1 = h1 && lay1 == l && testbit_r<W>(D1, j);
+                const int k = ffs_m<TWO>(ballot_m<TWO>(c0, c1));
                 const int kl = k & 31, ks = k >> 5;
                 const int old = __shfl_sync(FULL, ks ? m1 : m0, kl);
                 if (lane == kl) {
@@ -327,15 +347,15 @@ __device__ bool gac_augment(int r, const uint32_t (&D0)[W], const uint32_t (&D1)
             }
 #pragma unroll
             for (int w = 0; w < W; ++w) MV[w] |= bitword(found, w);
-            __syncwarp();
             return true;
         }
-        const bool t0 = h0 && m0 >= 0 && testbit_r<W>(nv, m0);
-        const bool t1 = h1 && m1 >= 0 && testbit_r<W>(nv, m1);
-        front = ballot64(t0, t1);
         ++L;
-        __syncwarp();
-        if (lane == 0) ws.layers[L] = front;
+        const bool t0 = h0 && m0 >= 0 && lay0 < 0 && testbit_r<W>(nv, m0);
+        bool t1 = false;
+        if constexpr (TWO) t1 = h1 && m1 >= 0 && lay1 < 0 && testbit_r<W>(nv, m1);
+        if (t0) lay0 = L;
+        if (t1) lay1 = L;
+        front = ballot_m<TWO>(t0, t1);
     }
 }
 
@@ -345,11 +365,13 @@ __device__ bool gac_augment(int r, const uint32_t (&D0)[W], const uint32_t (&D1)
 // On infeasibility the reference wipes the first member Kuhn leaves unmatched (:379-386); with
 // exact_wipe we recompute the matching greedily in member order, which leaves the same first
 // member unmatched (transversal-matroid greedy basis), and wipe it.
-template <int W>
+// TWO = false: <= 32 members, one per lane, 32-bit member sets; TWO = true: <= 64 members.
+template <int W, bool TWO>
 __device__ void prop_alldiff_gac(const DevModel& M, int a, const uint32_t* dom, uint32_t* rm, int16_t* mates,
                                  const WarpScratch& ws, int lane, int exact_wipe, uint32_t* post, int8_t* post_ok) {
+    using MS = MemberSet<TWO>;
     const int b = M.ad_start[a], n = M.ad_start[a + 1] - b;
-    const bool h0 = lane < n, h1 = lane + 32 < n;
+    const bool h0 = lane < n, h1 = TWO && lane + 32 < n;
     uint32_t D0[W], D1[W];
     int v0 = -1, v1 = -1, s0 = 0, s1 = 0;
     if (h0) {
@@ -381,12 +403,12 @@ __device__ void prop_alldiff_gac(const DevModel& M, int a, const uint32_t* dom, 
 #pragma unroll
     for (int w = 0; w < W; ++w) MV[w] = __reduce_or_sync(FULL, bitword(m0, w) | bitword(m1, w));
 
-    unsigned long long unm = ballot64(h0 && m0 < 0, h1 && m1 < 0);
+    MS unm = ballot_m<TWO>(h0 && m0 < 0, h1 && m1 < 0);
     int fail = -1;
     while (unm) {
-        const int r = __ffsll((long long)unm) - 1;
+        const int r = ffs_m<TWO>(unm);
         unm &= unm - 1;
-        if (!gac_augment<W>(r, D0, D1, h0, h1, m0, m1, MV, ws, lane)) {
+        if (!gac_augment<W, TWO>(r, D0, D1, h0, h1, m0, m1, MV, lane)) {
             fail = r;
             break;
         }
@@ -397,7 +419,7 @@ __device__ void prop_alldiff_gac(const DevModel& M, int a, const uint32_t* dom, 
 #pragma unroll
             for (int w = 0; w < W; ++w) MV[w] = 0;
             for (int r = 0; r < n; ++r)
-                if (!gac_augment<W>(r, D0, D1, h0, h1, m0, m1, MV, ws, lane)) {
+                if (!gac_augment<W, TWO>(r, D0, D1, h0, h1, m0, m1, MV, lane)) {
                     fail = r;
                     break;
                 }
@@ -427,48 +449,52 @@ __device__ void prop_alldiff_gac(const DevModel& M, int a, const uint32_t* dom, 
     __syncwarp();
     // free values F = U & ~MV ; pred(k) = { m : mate(m) in D(k) }
     uint32_t F[W];
-    unsigned long long p0 = 0, p1 = 0;
+    MS p0 = 0, p1 = 0;
     bool sd0 = false, sd1 = false;
 #pragma unroll
     for (int w = 0; w < W; ++w) {
         F[w] = __reduce_or_sync(FULL, D0[w] | D1[w]) & ~MV[w];
         sd0 |= (D0[w] & F[w]) != 0;
         sd1 |= (D1[w] & F[w]) != 0;
-        uint32_t x0 = D0[w] & MV[w], x1 = D1[w] & MV[w];
+        uint32_t x0 = D0[w] & MV[w];
         while (x0) {
-            p0 |= 1ull << ws.owner[w * 32 + __ffs(x0) - 1];
+            p0 |= (MS)1 << ws.owner[w * 32 + __ffs(x0) - 1];
             x0 &= x0 - 1;
         }
-        while (x1) {
-            p1 |= 1ull << ws.owner[w * 32 + __ffs(x1) - 1];
-            x1 &= x1 - 1;
+        if constexpr (TWO) {
+            uint32_t x1 = D1[w] & MV[w];
+            while (x1) {
+                p1 |= (MS)1 << ws.owner[w * 32 + __ffs(x1) - 1];
+                x1 &= x1 - 1;
+            }
         }
     }
     // Warshall: anc(k) = members that reach k. A singleton member has no in-edge (its only value
     // is its own mate), so it is never interior to a path: only non-singletons serve as pivots.
-    const unsigned long long pivots = ballot64(h0 && dom_size<W>(D0) > 1, h1 && dom_size<W>(D1) > 1);
-    for (unsigned long long q = pivots; q; q &= q - 1) {
-        const int p = __ffsll((long long)q) - 1;
-        const unsigned long long ap = __shfl_sync(FULL, (p >> 5) ? p1 : p0, p & 31);
-        if ((p0 >> p) & 1ull) p0 |= ap;
-        if ((p1 >> p) & 1ull) p1 |= ap;
+    const MS pivots = ballot_m<TWO>(h0 && dom_size<W>(D0) > 1, h1 && dom_size<W>(D1) > 1);
+    for (MS q = pivots; q; q &= q - 1) {
+        const int p = ffs_m<TWO>(q);
+        const MS ap = __shfl_sync(FULL, (p >> 5) ? p1 : p0, p & 31);
+        if ((p0 >> p) & 1u) p0 |= ap;
+        if constexpr (TWO)
+            if ((p1 >> p) & 1u) p1 |= ap;
     }
     // members reached from free values (seeds: D(k) meets F)
-    const unsigned long long S = ballot64(h0 && sd0, h1 && sd1);
+    const MS S = ballot_m<TWO>(h0 && sd0, h1 && sd1);
     const bool r0 = h0 && (p0 & S), r1 = h1 && (p1 & S);
     uint32_t KEEP[W];
 #pragma unroll
     for (int w = 0; w < W; ++w) KEEP[w] = F[w] | __reduce_or_sync(FULL, (r0 ? bitword(m0, w) : 0u) | (r1 ? bitword(m1, w) : 0u));
     ws.anc[lane] = p0;
-    ws.anc[lane + 32] = p1;
+    if constexpr (TWO) ws.anc[lane + 32] = p1;
     __syncwarp();
     // an unmatched edge (k, j) survives iff j is kept above or owner(j) is in k's SCC
 #pragma unroll
-    for (int sl = 0; sl < 2; ++sl) {
+    for (int sl = 0; sl < (TWO ? 2 : 1); ++sl) {
         const bool h = sl ? h1 : h0;
         if (!h) continue;
         const int k = lane + 32 * sl, mk = sl ? m1 : m0, v = sl ? v1 : v0, sh = sl ? s1 : s0;
-        const unsigned long long ak = sl ? p1 : p0;
+        const MS ak = sl ? p1 : p0;
         uint32_t rem[W];
         bool anyr = false;
 #pragma unroll
@@ -479,7 +505,7 @@ __device__ void prop_alldiff_gac(const DevModel& M, int a, const uint32_t* dom, 
                 const int bit = __ffs(x) - 1;
                 x &= x - 1;
                 const int m = ws.owner[w * 32 + bit];
-                if (((ak >> m) & 1ull) && ((ws.anc[m] >> k) & 1ull)) cand &= ~(1u << bit);
+                if (((ak >> m) & 1u) && ((((MS)ws.anc[m]) >> k) & 1u)) cand &= ~(1u << bit);
             }
             rem[w] = cand;
             anyr |= cand != 0;
@@ -657,9 +683,15 @@ __device__ __forceinline__ void run_propagators(const DevModel& M, const RoundCt
                 for (int t = b + lane; t < e; t += 32) hit |= trig_bit(trig, M.ad_var[t]);
                 if (!__any_sync(FULL, hit)) continue;
             }
-            if (R.alldiff)
-                prop_alldiff_gac<W>(M, a, R.dom, R.rm, R.mates + M.ad_start[a], ws, lane, R.exact_wipe,
-                                    R.post ? R.post + (size_t)M.ad_start[a] * W : nullptr, R.post_ok + a);
+            if (R.alldiff) {
+                uint32_t* post = R.post ? R.post + (size_t)M.ad_start[a] * W : nullptr;
+                if (M.ad_start[a + 1] - M.ad_start[a] <= 32)
+                    prop_alldiff_gac<W, false>(M, a, R.dom, R.rm, R.mates + M.ad_start[a], ws, lane, R.exact_wipe, post,
+                                               R.post_ok + a);
+                else
+                    prop_alldiff_gac<W, true>(M, a, R.dom, R.rm, R.mates + M.ad_start[a], ws, lane, R.exact_wipe, post,
+                                              R.post_ok + a);
+            }
             else prop_alldiff_fc<W>(M, a, R.dom, R.rm, lane);
         }
     }
