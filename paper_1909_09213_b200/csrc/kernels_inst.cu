@@ -10,7 +10,9 @@ namespace cubics {
 
 template <>
 cudaError_t launch_search<CUBICS_W>(const SearchParams& P, int grid, int block, size_t smem, cudaStream_t st) {
-    auto k = dev::search_kernel<CUBICS_W>;
+    // the generic block kernel also runs one-warp contexts: a __syncwarp-specialised variant
+    // (search_kernel<W, true>) measured slower on B200 (19.3 vs 14.0 ms on nq14; register spills)
+    auto k = dev::search_kernel<CUBICS_W, false>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k<<<grid, block, smem, st>>>(P);
@@ -19,7 +21,7 @@ cudaError_t launch_search<CUBICS_W>(const SearchParams& P, int grid, int block, 
 
 template <>
 cudaError_t occupancy_search<CUBICS_W>(int block, size_t smem, int* out) {
-    auto k = dev::search_kernel<CUBICS_W>;
+    auto k = dev::search_kernel<CUBICS_W, false>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, k, block, smem);

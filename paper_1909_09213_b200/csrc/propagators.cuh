@@ -26,6 +26,21 @@ typedef __int128 i128;
 
 enum RoundStatus : int { R_CHANGED = 0, R_STABLE = 1, R_FAILED = 2, R_ERROR = 3 };
 
+// Block-level primitives specialised for one-warp search contexts (ONE: blockDim.x == 32, the
+// throughput configuration): barriers become __syncwarp and block votes become warp votes.
+template <bool ONE>
+__device__ __forceinline__ int nthreads() { return ONE ? 32 : (int)blockDim.x; }
+template <bool ONE>
+__device__ __forceinline__ void bar() {
+    if constexpr (ONE) __syncwarp();
+    else __syncthreads();
+}
+template <bool ONE>
+__device__ __forceinline__ int bar_or(int x) {
+    if constexpr (ONE) return __any_sync(FULL, x);
+    else return __syncthreads_or(x);
+}
+
 // ------------------------------------------------------------------ bitset helpers
 template <int W>
 __device__ __forceinline__ bool dom_empty(const uint32_t* d) {
@@ -618,10 +633,10 @@ __device__ __forceinline__ bool trig_bit(const uint32_t* t, int v) { return (t[v
 // untriggered propagator sees exactly the domains of its last evaluation, whose removals are
 // already applied, so skipping it changes no domain, no "changed" flag and no round count.
 // *s_err receives DERR_OVERFLOW.
-template <int W>
+template <int W, bool ONE = false>
 __device__ __forceinline__ void run_propagators(const DevModel& M, const RoundCtx& R, int* s_err,
                                                 const uint32_t* trig) {
-    const int tid = threadIdx.x, T = blockDim.x, nw = T >> 5, warp = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x, T = nthreads<ONE>(), nw = T >> 5, warp = ONE ? 0 : tid >> 5, lane = tid & 31;
     const int ad_warps = M.na < nw ? M.na : nw;
     const int prop_threads = nw > ad_warps ? (nw - ad_warps) * 32 : T;
     if (tid < prop_threads) {
@@ -699,10 +714,10 @@ __device__ __forceinline__ void run_propagators(const DevModel& M, const RoundCt
 
 // Phase B: dom &= ~rm. Returns R_CHANGED / R_STABLE / R_FAILED / R_ERROR.
 // failed_var (when non-null) receives the lowest empty var id on failure.
-template <int W>
+template <int W, bool ONE = false>
 __device__ __forceinline__ int apply_removals(const DevModel& M, const RoundCtx& R, int* s_err, int* s_min,
                                               int* failed_var, uint32_t* chg_out) {
-    const int tid = threadIdx.x, T = blockDim.x;
+    const int tid = threadIdx.x, T = nthreads<ONE>();
     int changed = 0, empty_min = 0x7fffffff;
     for (int v = tid; v < M.n; v += T) {
         uint32_t* d = R.dom + (size_t)v * W;
@@ -728,19 +743,19 @@ __device__ __forceinline__ int apply_removals(const DevModel& M, const RoundCtx&
         }
         if (!any && v < empty_min) empty_min = v;
     }
-    const int ch = __syncthreads_or(changed);
+    const int ch = bar_or<ONE>(changed);
     const int err = *s_err;
     if (err) return R_ERROR;
     if (!ch) return R_STABLE;
-    const int em = __syncthreads_or(empty_min != 0x7fffffff);
+    const int em = bar_or<ONE>(empty_min != 0x7fffffff);
     if (!em) return R_CHANGED;
     if (failed_var) {
         if (tid == 0) *s_min = 0x7fffffff;
-        __syncthreads();
+        bar<ONE>();
         if (empty_min != 0x7fffffff) atomicMin(s_min, empty_min);
-        __syncthreads();
+        bar<ONE>();
         *failed_var = *s_min;
-        __syncthreads();
+        bar<ONE>();
     }
     return R_FAILED;
 }
@@ -748,10 +763,10 @@ __device__ __forceinline__ int apply_removals(const DevModel& M, const RoundCtx&
 // propagate_fixpoint (propagation.cpp:516-532); *rounds counts every round including the last.
 // first_all: evaluate every propagator in round 1; otherwise round 1 is triggered by the vars
 // set in R.chg0 (the caller's branch decision). Both trigger buffers are left dirty.
-template <int W>
+template <int W, bool ONE = false>
 __device__ int block_fixpoint(const DevModel& M, const RoundCtx& R, int* s_err, int* s_min, int max_rounds,
                               int* rounds, int* failed_var, bool first_all) {
-    const int tid = threadIdx.x, T = blockDim.x;
+    const int tid = threadIdx.x, T = nthreads<ONE>();
     const int nb = (M.n + 31) >> 5;
     uint32_t* cur = R.chg0;
     uint32_t* nxt = R.chg1;
@@ -760,9 +775,9 @@ __device__ int block_fixpoint(const DevModel& M, const RoundCtx& R, int* s_err, 
     for (;;) {
         if (nxt)
             for (int i = tid; i < nb; i += T) nxt[i] = 0;
-        run_propagators<W>(M, R, s_err, all ? nullptr : cur);
-        __syncthreads();
-        const int st = apply_removals<W>(M, R, s_err, s_min, failed_var, nxt);
+        run_propagators<W, ONE>(M, R, s_err, all ? nullptr : cur);
+        bar<ONE>();
+        const int st = apply_removals<W, ONE>(M, R, s_err, s_min, failed_var, nxt);
         ++r;
         if (st != R_CHANGED || (max_rounds > 0 && r >= max_rounds)) {
             *rounds = r;

@@ -60,17 +60,19 @@ __device__ __forceinline__ void spin_unlock(int32_t* l) {
     atomicExch(l, 0);
 }
 
-// block-wide copy of nw4 uint4 words
+// block-wide copy of nwords/4 uint4 words
+template <bool ONE = false>
 __device__ __forceinline__ void copy4(uint32_t* dst, const uint32_t* src, size_t nwords) {
     uint4* d = reinterpret_cast<uint4*>(dst);
     const uint4* s = reinterpret_cast<const uint4*>(src);
-    for (size_t i = threadIdx.x; i < nwords / 4; i += blockDim.x) d[i] = s[i];
+    for (size_t i = threadIdx.x; i < nwords / 4; i += nthreads<ONE>()) d[i] = s[i];
 }
 
+template <bool ONE = false>
 __device__ __forceinline__ void copy4_cg(uint32_t* dst, const uint32_t* src, size_t nwords) {
     uint4* d = reinterpret_cast<uint4*>(dst);
     const uint4* s = reinterpret_cast<const uint4*>(src);
-    for (size_t i = threadIdx.x; i < nwords / 4; i += blockDim.x) d[i] = __ldcg(s + i);
+    for (size_t i = threadIdx.x; i < nwords / 4; i += nthreads<ONE>()) d[i] = __ldcg(s + i);
 }
 
 // DFS path key: decision at depth d is bit (31 - d%32) of word d/32, so comparing the words as
@@ -86,9 +88,9 @@ __device__ __forceinline__ uint32_t path_right_word(uint32_t word, int i, int d)
 }
 
 // block argmin of (size, id) over unbound vars; -1 when every domain is a singleton
-template <int W>
+template <int W, bool ONE = false>
 __device__ __forceinline__ int select_var(const DevModel& M, const uint32_t* dom, int first_fail, unsigned* s_red) {
-    const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = T >> 5;
+    const int tid = threadIdx.x, T = nthreads<ONE>(), lane = tid & 31, warp = tid >> 5, nw = T >> 5;
     unsigned best = 0xffffffffu;
     for (int v = tid; v < M.n; v += T) {
         const int sz = dom_size<W>(dom + (size_t)v * W);
@@ -98,7 +100,7 @@ __device__ __forceinline__ int select_var(const DevModel& M, const uint32_t* dom
         }
     }
     best = __reduce_min_sync(FULL, best);
-    if (nw > 1) {
+    if (!ONE && nw > 1) {
         if (lane == 0) s_red[warp] = best;
         __syncthreads();
         unsigned x = lane < nw ? s_red[lane] : 0xffffffffu;
@@ -108,15 +110,15 @@ __device__ __forceinline__ int select_var(const DevModel& M, const uint32_t* dom
     return best == 0xffffffffu ? -1 : (int)(best & 0x1fffffu);
 }
 
-template <int W>
-__global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
+template <int W, bool ONE>
+__global__ void __launch_bounds__(ONE ? 32 : 1024, ONE ? 32 : 1) search_kernel(const SearchParams P) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ int s_err, s_min, s_flag, s_src;
     __shared__ unsigned s_red[32];
     __shared__ long long s_ll;
 
     const DevModel& M = P.M;
-    const int ctx = blockIdx.x, tid = threadIdx.x, T = blockDim.x, nw = T >> 5;
+    const int ctx = blockIdx.x, tid = threadIdx.x, T = nthreads<ONE>(), nw = T >> 5;
     const bool parallel = P.mode == MODE_PARALLEL;
     const int n = M.n;
     const size_t NW = (size_t)n * W, NWP = round4(NW);
@@ -193,17 +195,17 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
             idle_cyc += clock64() - t0;
             s_src = got;
         }
-        __syncthreads();
+        bar<ONE>();
         const int got = s_src;
         if (got < 0) return false;
         const uint32_t* ob = P.outbox + (size_t)got * OS;
-        copy4_cg(dom, ob, NWP);
+        copy4_cg<ONE>(dom, ob, NWP);
         for (int i = tid; i < KW; i += T) path[i] = __ldcg(ob + NWP + i);
         depth = (int)__ldcg(ob + NWP + KW);
         const int tvar = (int)__ldcg(ob + NWP + KW + 1);
         if (chg0)
             for (int i = tid; i < 2 * nbw; i += T) chg0[i] = 0;
-        __syncthreads();
+        bar<ONE>();
         if (tid == 0) {
             if (chg0) chg0[tvar >> 5] |= 1u << (tvar & 31);
             __threadfence();
@@ -217,23 +219,23 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
 
     bool have_work;
     if (!parallel || (ctx == 0 && !P.n_seed)) {
-        copy4(dom, M.init_dom, NWP);
+        copy4<ONE>(dom, M.init_dom, NWP);
         have_work = true;
     } else {
         have_work = get_work();
     }
-    __syncthreads();
+    bar<ONE>();
 
     while (have_work) {
         bool backtrack = false;
         if (P.split_depth >= 0 && depth >= P.split_depth) {
             // ============ frontier expansion: this open node becomes a task (counted by its shard)
             if (tid == 0) s_ll = (long long)atomicAdd((unsigned long long*)&ws->n_tasks, 1ull);
-            __syncthreads();
+            bar<ONE>();
             const long long t = s_ll;
             if (t < P.task_cap) {
                 uint32_t* tb = P.tasks + (size_t)t * OS;
-                copy4(tb, dom, NWP);
+                copy4<ONE>(tb, dom, NWP);
                 for (int i = tid; i < KW; i += T) tb[NWP + i] = path[i];
                 if (tid == 0) {
                     tb[NWP + KW] = (uint32_t)depth;
@@ -282,13 +284,13 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
                 }
                 s_flag = empty;
             }
-            __syncthreads();
+            bar<ONE>();
             backtrack = s_flag != 0;
             if (backtrack) ++failures;
         }
         if (!backtrack) {
             int r = 0;
-            const int st = block_fixpoint<W>(M, R, &s_err, &s_min, 0, &r, nullptr, first_all);
+            const int st = block_fixpoint<W, ONE>(M, R, &s_err, &s_min, 0, &r, nullptr, first_all);
             first_all = false;
             rounds += (unsigned long long)r;
             if (st == R_ERROR) {
@@ -305,14 +307,14 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
         }
         if (parallel && tid == 0) g_has_bound = (int)hot.w; // the prefetched bound pairs with this flag
         if (!backtrack) {
-            const int sel = select_var<W>(M, dom, P.var_heuristic, s_red);
+            const int sel = select_var<W, ONE>(M, dom, P.var_heuristic, s_red);
             if (sel < 0) {
                 // ============ solution leaf (emit_solution, search.cpp:134-156)
                 if (tid == 0) {
                     s_ll = parallel ? (long long)atomicAdd((unsigned long long*)&ws->sol_count, 1ull) : (long long)sols;
                     if (parallel) atomicMax(&ws->max_depth, depth);
                 }
-                __syncthreads();
+                bar<ONE>();
                 const unsigned long long idx = (unsigned long long)s_ll;
                 ++sols;
                 if (P.record && idx < P.sol_cap) {
@@ -334,7 +336,7 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
                             }
                         s_flag = less || !has_first;
                     }
-                    __syncthreads();
+                    bar<ONE>();
                     if (s_flag) {
                         has_first = true;
                         for (int i = tid; i < KW; i += T) {
@@ -365,7 +367,7 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
                         g_has_bound = 1;
                     }
                 }
-                __syncthreads();
+                bar<ONE>();
                 if (!parallel && sols >= P.max_solutions) {
                     if (tid == 0) {
                         ws->user_stop = 1;
@@ -384,7 +386,7 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
                     break;
                 }
                 const int bit = dom_first<W>(dom + (size_t)sel * W);
-                copy4(frames + (size_t)sp * NWP, dom, NWP);
+                copy4<ONE>(frames + (size_t)sp * NWP, dom, NWP);
                 if (chg0)
                     for (int i = tid; i < 2 * nbw; i += T) chg0[i] = 0;
                 if (tid == 0) {
@@ -396,7 +398,7 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
                     if (parallel && !want && sp + 1 > base && !my_busy && hot.y > hot.x) want = 1;
                     s_flag = want;
                 }
-                __syncthreads();
+                bar<ONE>();
                 if (tid < W) dom[(size_t)sel * W + tid] = (tid == (bit >> 5)) ? (1u << (bit & 31)) : 0u;
                 if (tid == 0 && chg0) chg0[sel >> 5] |= 1u << (sel & 31);
                 trig_var = sel;
@@ -420,7 +422,7 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
                         ob[NWP + KW] = (uint32_t)(fdepth + 1);
                         ob[NWP + KW + 1] = (uint32_t)fvar;
                     }
-                    __syncthreads();
+                    bar<ONE>();
                     if (tid == 0) {
                         P.outbox_busy[ctx] = 1;
                         atomicAdd(&ws->outstanding, 1);
@@ -430,7 +432,7 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
                         ++donations;
                     }
                 }
-                __syncthreads();
+                bar<ONE>();
                 continue;
             }
         }
@@ -438,21 +440,21 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
         // ================= backtrack: right branch of the deepest pending frame (:122-131)
         if (parallel) {
             if (tid == 0) s_flag = hot.z;
-            __syncthreads();
+            bar<ONE>();
             if (s_flag) break;
         }
         if (sp == base) {
             if (!parallel) break;
             have_work = get_work();
-            __syncthreads();
+            bar<ONE>();
             continue;
         }
         --sp;
-        copy4(dom, frames + (size_t)sp * NWP, NWP);
+        copy4<ONE>(dom, frames + (size_t)sp * NWP, NWP);
         if (chg0)
             for (int i = tid; i < 2 * nbw; i += T) chg0[i] = 0;
         const int var = meta[sp * 4 + 0], bit = meta[sp * 4 + 1], d = meta[sp * 4 + 2];
-        __syncthreads();
+        bar<ONE>();
         if (tid == 0) {
             dom[(size_t)var * W + (bit >> 5)] &= ~(1u << (bit & 31));
             if (chg0) chg0[var >> 5] |= 1u << (var & 31);
@@ -463,9 +465,9 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
         }
         depth = d + 1;
         trig_var = var;
-        __syncthreads();
+        bar<ONE>();
     }
-    __syncthreads();
+    bar<ONE>();
     if (parallel && tid == 0 && have_work) {
         // unwound by stop: this context no longer counts as outstanding
         atomicSub(&ws->outstanding, 1);
