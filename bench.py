@@ -152,6 +152,49 @@ def impl_reference(args):
     return 0
 
 
+GOLDEN = os.path.join(ROOT, "tests", "golden", "goldens.json")
+
+
+def run_extras(S, A, device):
+    """The other BASELINE.json configs, one run each (device time; stats vs the reference goldens).
+    Reference CPU times are the survey-box / golden-run figures recorded in goldens.json."""
+    gold = json.load(open(GOLDEN))
+    out = {}
+    cases = [
+        ("golomb10", "golomb10", A.ENGINE_PARALLEL, {}, "B&B to optimum, parallel engine (node count schedule-dependent)"),
+        ("golomb10_parity", "golomb10", A.ENGINE_PARITY, {}, "B&B, parity engine (reference node order)"),
+        ("magic5_first", "magic5|--max 1", A.ENGINE_PARITY, {"max_solutions": 1}, "first solution, parity engine"),
+        ("magic4_all", "magic4|--all", A.ENGINE_PARALLEL, {}, "all solutions, parallel engine"),
+        ("rcsp_1000_first", "rcsp_1000|--max 1", A.ENGINE_PARITY, {"max_solutions": 1}, "first solution, parity engine"),
+        ("rcsp_100000_limit200", "rcsp_100000|--max 1 --node-limit 200", A.ENGINE_PARITY,
+         {"max_solutions": 1, "node_limit": 200}, "node-limited parity"),
+    ]
+    for name, key, engine, kw, what in cases:
+        inst = key.split("|")[0]
+        g = gold.get(key)
+        m = S.parse_model(open(os.path.join(MODELS, inst + ".fd")).read())
+        cfg = S.SearchConfig(engine=engine, device=device, count_only=True, **kw)
+        try:
+            if m.goal != 0:
+                r = S.solve_optimize(m, cfg)
+                extra = {"objective": r.best.objective if r.best else None}
+            else:
+                r = S.solve_satisfy(m, cfg)
+                extra = {}
+            st = r.stats.as_tuple()
+            exp = (g["nodes"], g["failures"], g["rounds"], g["solutions"]) if g else None
+            rec = {"what": what, "device_ms": round(r.device_ms, 3), "nodes": st[0],
+                   "nodes_per_s": st[0] / (r.device_ms / 1e3) if r.device_ms else None,
+                   "stats_equal_reference": (st == exp) if exp else None,
+                   "reference_cpu_ms": g.get("time_ms") if g else None, **extra}
+            if m.goal != 0 and g:
+                rec["objective_equal_reference"] = extra["objective"] == g.get("objective")
+            out[name] = rec
+        except Exception as e:  # noqa: BLE001 - reported, never hidden
+            out[name] = {"what": what, "error": repr(e)}
+    return out
+
+
 def impl_ours(args):
     from paper_1909_09213_b200 import _abi as A
     from paper_1909_09213_b200 import solver as S
@@ -205,6 +248,7 @@ def impl_ours(args):
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
         h2d, d2h, e2e_launches = r2.h2d_bytes, r2.d2h_bytes, r2.kernel_launches
         assert arr.shape[0] == r2.stats.solutions
+    extras = run_extras(S, A, device) if (rank == 0 and not args.no_extras) else None
     ms = max(dev_ms) if dev_ms else 0.0
     nodes = stats0.nodes
     if world > 1:
@@ -248,6 +292,7 @@ def impl_ours(args):
                      "note": "latency/barrier-bound search; A from SURVEY 8(d)"},
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
+        "other_configs": extras,
     }
     print(json.dumps(line))
     if world > 1:
@@ -267,6 +312,7 @@ def main():
     ap.add_argument("--cpu-node-limit", type=int, default=400000)
     ap.add_argument("--ref-node-limit", type=int, default=200000)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extras", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return impl_reference(args)
