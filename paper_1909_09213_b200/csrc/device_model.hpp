@@ -43,6 +43,9 @@ struct DevModel {
     const int32_t* ad_start;  // [na+1]
     const int32_t* ad_var;
     const int32_t* ad_shift;
+    const int32_t* ad_uw;        // [na] 0: fast warp path (<= 64 members, universe in W words);
+                                 //      > 0: generic path over a uw-word universe (big_words scratch)
+    int32_t big_words;           // u32 words of per-warp scratch the generic path needs (0: none)
     int32_t total_members;
     int32_t goal;
     int32_t goal_var;
@@ -102,6 +105,7 @@ struct SearchParams {
     int32_t record;        // 1: materialise solutions
     int32_t dom_in_smem;
     // per-context global scratch
+    uint32_t* big_scratch; // [n_ctx * warps][M.big_words] generic alldifferent working sets
     uint32_t* frames;      // [n_ctx][frame_cap][NW]
     int32_t* frame_meta;   // [n_ctx][frame_cap][4] : var, bit, depth, pad
     uint32_t* gdom;        // [n_ctx][2*NW] when domains do not fit in shared memory
@@ -140,6 +144,7 @@ struct PropParams {
     const uint8_t* enabled; // per constraint kind-local enable flags [nr + nl + na] or null
     uint32_t* dom;         // [NW] in/out
     uint32_t* out;         // removals output (removals_only)
+    uint32_t* big_scratch; // [warps][M.big_words]
     int32_t* result;       // failed, failed_var, rounds, last_status, error
 };
 

@@ -30,7 +30,9 @@ using namespace cubics;
 
 namespace {
 
-constexpr int kMaxAllDiffMembers = 64;
+constexpr int kFastAllDiffMembers = 64;  // warp fast path; larger ones take the generic path
+constexpr int kMaxAllDiffMembers = 4096;  // generic path limit (n x n member bit rows per warp)
+constexpr long kMaxUniverseWords = 1024;  // generic path value universe (32768 values)
 constexpr size_t kSmemBudget = 200 * 1024;
 
 struct CudaError {
@@ -108,7 +110,8 @@ struct Prepared {
     bool has_empty = false;
     uint64_t depth_bound = 0; // sum(|D| - 1): max binary-tree depth
     Blob blob;
-    size_t o_off, o_dom, o_rb, o_ls, o_lo, o_lb, o_lv, o_lc, o_as, o_av, o_ash, o_nes, o_nee;
+    size_t o_off, o_dom, o_rb, o_ls, o_lo, o_lb, o_lv, o_lc, o_as, o_av, o_ash, o_nes, o_nee, o_auw;
+    size_t big_words = 0;
     int nr_gen = 0;
     std::vector<int> kind_index; // constraint index -> kind-local index (rb | nr+lin | nr+nl+ad)
     std::vector<int64_t> offsets;
@@ -133,6 +136,8 @@ struct Prepared {
         M.ad_start = reinterpret_cast<const int32_t*>(base + o_as);
         M.ad_var = reinterpret_cast<const int32_t*>(base + o_av);
         M.ad_shift = reinterpret_cast<const int32_t*>(base + o_ash);
+        M.ad_uw = reinterpret_cast<const int32_t*>(base + o_auw);
+        M.big_words = static_cast<int32_t>(big_words);
         M.total_members = total_members;
         return M;
     }
@@ -207,10 +212,12 @@ void prepare(const HostModel& m, const uint64_t* words, Prepared& P) {
             break;
         }
     }
+    std::vector<int32_t> auw;
+    size_t big_words = 0;
     for (int c : ad_cons) {
         const int b = m.con_start[c], e = m.con_start[c + 1];
         if (e - b > kMaxAllDiffMembers)
-            throw StatusError{CUBICS_E_UNSUPPORTED, "alldifferent with more than 64 members"};
+            throw StatusError{CUBICS_E_UNSUPPORTED, "alldifferent with more than 4096 members"};
         __int128 uoff = 0, uend = 0;
         for (int t = b; t < e; ++t) {
             const int v = m.term_var[t];
@@ -219,8 +226,16 @@ void prepare(const HostModel& m, const uint64_t* words, Prepared& P) {
             if (t == b || en > uend) uend = en;
         }
         const __int128 span = uend - uoff;
-        if (span > 32 * 32) throw StatusError{CUBICS_E_UNSUPPORTED, "alldifferent value universe wider than 1024"};
-        need = std::max(need, static_cast<int>((span + 31) / 32));
+        const long uwords = static_cast<long>((span + 31) / 32);
+        if (uwords > kMaxUniverseWords)
+            throw StatusError{CUBICS_E_UNSUPPORTED, "alldifferent value universe wider than 32768 values"};
+        if (e - b <= kFastAllDiffMembers && span <= 32 * 32) {
+            need = std::max(need, static_cast<int>(uwords));
+            auw.push_back(0);
+        } else {
+            auw.push_back(static_cast<int32_t>(uwords));
+            big_words = std::max(big_words, dev::big_scratch_words(e - b, static_cast<int>(uwords)));
+        }
         P.kind_index[c] = static_cast<int>(as.size()) - 1;
         for (int t = b; t < e; ++t) {
             av.push_back(m.term_var[t]);
@@ -228,6 +243,7 @@ void prepare(const HostModel& m, const uint64_t* words, Prepared& P) {
         }
         as.push_back(static_cast<int32_t>(av.size()));
     }
+    P.big_words = (big_words + 3) & ~size_t(3);
     int W = 1;
     while (W < need) W *= 2;
     if (W > 32) throw StatusError{CUBICS_E_UNSUPPORTED, "domain wider than 1024 values"};
@@ -275,21 +291,45 @@ void prepare(const HostModel& m, const uint64_t* words, Prepared& P) {
     P.o_as = P.blob.add(as.data(), as.size());
     P.o_av = P.blob.add(av.data(), av.size());
     P.o_ash = P.blob.add(ash.data(), ash.size());
+    P.o_auw = P.blob.add(auw.data(), auw.size());
     P.o_nes = P.blob.add(nes.data(), nes.size());
     P.o_nee = P.blob.add(nee.data(), nee.size());
 }
 
+// per-device state created once: capability check, one non-blocking stream, timing events
+struct DevState {
+    bool checked = false;
+    bool ok = false;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+};
+DevState g_dev[64];
+int g_count = -1;
+
 int current_device(int want) {
-    int count = 0;
-    CU(cudaGetDeviceCount(&count));
-    if (count == 0) throw CudaError{"no CUDA device"};
+    if (g_count < 0) {
+        int count = 0;
+        CU(cudaGetDeviceCount(&count));
+        g_count = count;
+    }
+    if (g_count == 0) throw CudaError{"no CUDA device"};
     int dev = want;
     if (dev < 0) CU(cudaGetDevice(&dev));
-    if (dev >= count) throw CudaError{"device ordinal out of range"};
+    if (dev >= g_count || dev >= 64) throw CudaError{"device ordinal out of range"};
     CU(cudaSetDevice(dev));
-    cudaDeviceProp prop;
-    CU(cudaGetDeviceProperties(&prop, dev));
-    if (prop.major < 10) throw CudaError{"device is not sm_100 class (Blackwell)"};
+    DevState& s = g_dev[dev];
+    if (!s.checked) {
+        int major = 0;
+        CU(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+        s.ok = major >= 10;
+        s.checked = true;
+        if (s.ok) {
+            CU(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+            CU(cudaEventCreate(&s.e0));
+            CU(cudaEventCreate(&s.e1));
+        }
+    }
+    if (!s.ok) throw CudaError{"device is not sm_100 class (Blackwell)"};
     return dev;
 }
 
@@ -467,6 +507,7 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
     const size_t a_busy = take(sizeof(int32_t) * (n_ctx + n_seed));
     const size_t a_hf = take(sizeof(int32_t) * n_ctx);
     const size_t zero_end = off;
+    const size_t a_big = take(sizeof(uint32_t) * P.big_words * (size_t)nw * n_ctx);
     const size_t a_frames = take(sizeof(uint32_t) * NWP * frame_cap * n_ctx);
     const size_t a_meta = take(sizeof(int32_t) * 4 * frame_cap * n_ctx);
     const size_t a_gdom = take(in_smem ? 0 : sizeof(uint32_t) * 2 * NWP * n_ctx);
@@ -480,12 +521,9 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
     const size_t a_inc = take(sizeof(uint16_t) * std::max(n, 1));
     uint8_t* base = device_arena(dev, off);
 
-    cudaStream_t st = nullptr;
-    CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    cudaEvent_t e0, e1;
-    CU(cudaEventCreate(&e0));
-    CU(cudaEventCreate(&e1));
-    try {
+    cudaStream_t st = g_dev[dev].stream;
+    cudaEvent_t e0 = g_dev[dev].e0, e1 = g_dev[dev].e1;
+    {
         // staging: blob + initial WorkState in pinned memory, one H2D copy
         WorkState w0{};
         w0.outstanding = n_ctx + n_seed;
@@ -529,6 +567,7 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
         S.KW = KW;
         S.record = record ? 1 : 0;
         S.dom_in_smem = in_smem ? 1 : 0;
+        S.big_scratch = P.big_words ? reinterpret_cast<uint32_t*>(base + a_big) : nullptr;
         S.frames = reinterpret_cast<uint32_t*>(base + a_frames);
         S.frame_meta = reinterpret_cast<int32_t*>(base + a_meta);
         S.gdom = reinterpret_cast<uint32_t*>(base + a_gdom);
@@ -623,15 +662,7 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
             out.d2h += sizeof(uint16_t) * n;
         }
         CU(cudaStreamSynchronize(st));
-    } catch (...) {
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
-        cudaStreamDestroy(st);
-        throw;
     }
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    cudaStreamDestroy(st);
     if (std::getenv("CUBICS_DEBUG")) {
         const WorkState& w = out.ws;
         const double tot = (double)w.busy_cycles + (double)w.idle_cycles;
@@ -1014,13 +1045,14 @@ int run_prop(const cubics_model* h, const uint64_t* words_in, uint64_t* words_ou
     const size_t a_out = take(sizeof(uint32_t) * NWP);
     const size_t a_res = take(sizeof(int32_t) * 8);
     const size_t a_scr = take(in_smem ? 0 : sizeof(uint32_t) * 2 * NWP);
+    const size_t a_big = take(sizeof(uint32_t) * P.big_words * (size_t)(block / 32));
     uint8_t* base = device_arena(dev, off);
-    std::vector<uint8_t> stage(a_dom + sizeof(uint32_t) * NWP, 0);
-    std::memcpy(stage.data() + a_blob, P.blob.bytes.data(), P.blob.bytes.size());
-    std::memcpy(stage.data() + a_dom, P.blob.bytes.data() + P.o_dom, sizeof(uint32_t) * NWP);
-    cudaStream_t st = nullptr;
-    CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    CU(cudaMemcpyAsync(base, stage.data(), stage.size(), cudaMemcpyHostToDevice, st));
+    const size_t stage_bytes = a_dom + sizeof(uint32_t) * NWP;
+    uint8_t* stage = pinned_arena(dev, stage_bytes);
+    std::memcpy(stage + a_blob, P.blob.bytes.data(), P.blob.bytes.size());
+    std::memcpy(stage + a_dom, P.blob.bytes.data() + P.o_dom, sizeof(uint32_t) * NWP);
+    cudaStream_t st = g_dev[dev].stream;
+    CU(cudaMemcpyAsync(base, stage, stage_bytes, cudaMemcpyHostToDevice, st));
     PropParams PP{};
     PP.M = P.bind(base + a_blob);
     PP.alldiff = alldiff == CUBICS_FORWARD_CHECKING ? 0 : 1;
@@ -1030,6 +1062,7 @@ int run_prop(const cubics_model* h, const uint64_t* words_in, uint64_t* words_ou
     PP.dom = reinterpret_cast<uint32_t*>(base + a_dom);
     PP.out = reinterpret_cast<uint32_t*>(base + a_out);
     PP.result = reinterpret_cast<int32_t*>(base + a_res);
+    PP.big_scratch = P.big_words ? reinterpret_cast<uint32_t*>(base + a_big) : nullptr;
     uint32_t* scr = reinterpret_cast<uint32_t*>(base + a_scr);
 #define LP(w) launch_propagate<w>(PP, block, L.total, st, scr, in_smem ? 1 : 0)
     CUBICS_DISPATCH_W(P.W, LP)
@@ -1040,7 +1073,6 @@ int run_prop(const cubics_model* h, const uint64_t* words_in, uint64_t* words_ou
                        cudaMemcpyDeviceToHost, st));
     CU(cudaMemcpyAsync(res, PP.result, sizeof res, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
-    cudaStreamDestroy(st);
     if (res[4] == DERR_OVERFLOW) throw StatusError{CUBICS_E_OVERFLOW, "overflow in linear propagation"};
     // back to the u64 reference layout
     for (int v = 0; v < m.n_vars(); ++v) {

@@ -8,12 +8,24 @@
 
 namespace cubics {
 
+namespace {
+// cudaFuncSetAttribute only when a launch needs more dynamic shared memory than already granted
+template <class K>
+cudaError_t grant_smem(K k, size_t smem, size_t& granted) {
+    if (smem <= granted) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) granted = smem;
+    return e;
+}
+size_t g_search_smem = 48 * 1024, g_prop_smem = 48 * 1024;
+} // namespace
+
 template <>
 cudaError_t launch_search<CUBICS_W>(const SearchParams& P, int grid, int block, size_t smem, cudaStream_t st) {
     // the generic block kernel also runs one-warp contexts: a __syncwarp-specialised variant
     // (search_kernel<W, true>) measured slower on B200 (19.3 vs 14.0 ms on nq14; register spills)
     auto k = dev::search_kernel<CUBICS_W, false>;
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = grant_smem(k, smem, g_search_smem);
     if (e != cudaSuccess) return e;
     k<<<grid, block, smem, st>>>(P);
     return cudaGetLastError();
@@ -22,7 +34,7 @@ cudaError_t launch_search<CUBICS_W>(const SearchParams& P, int grid, int block, 
 template <>
 cudaError_t occupancy_search<CUBICS_W>(int block, size_t smem, int* out) {
     auto k = dev::search_kernel<CUBICS_W, false>;
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = grant_smem(k, smem, g_search_smem);
     if (e != cudaSuccess) return e;
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, k, block, smem);
 }
@@ -31,7 +43,7 @@ template <>
 cudaError_t launch_propagate<CUBICS_W>(const PropParams& P, int block, size_t smem, cudaStream_t st,
                                        uint32_t* scratch, int in_smem) {
     auto k = dev::propagate_kernel<CUBICS_W>;
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = grant_smem(k, smem, g_prop_smem);
     if (e != cudaSuccess) return e;
     k<<<1, block, smem, st>>>(P, scratch, in_smem);
     return cudaGetLastError();

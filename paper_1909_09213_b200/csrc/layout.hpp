@@ -18,6 +18,13 @@ CUBICS_HD constexpr size_t round4(size_t x) { return (x + 3) & ~size_t(3); }
 // per-warp alldifferent scratch: BFS layers [66] + ancestor sets [64] (u64) + value owners [W*32] (u8)
 CUBICS_HD constexpr int warp_scratch_bytes(int W) { return (66 + 64) * 8 + W * 32; }
 
+// u32 words of per-warp scratch of the generic alldifferent path (propagators.cuh BigScratch)
+CUBICS_HD inline size_t big_scratch_words(int n, int uw) {
+    const size_t nwm = ((size_t)n + 31) / 32;
+    return (size_t)n * uw + (size_t)n * nwm + (size_t)uw * 32 + (size_t)n + 2 * (size_t)n + 6 * (size_t)uw +
+           2 * nwm + 4 + 8;
+}
+
 struct SmemLayout {
     size_t dom, rm, mates, scratch, path, bestkey, post, post_ok, chg, total;
     int stride;

@@ -598,6 +598,293 @@ __device__ void prop_alldiff_fc(const DevModel& M, int a, const uint32_t* dom, u
     }
 }
 
+// ------------------------------------------------------------------ AllDifferent, generic path
+// Any member count / value-universe width (the fast path above covers <= 64 members and a
+// universe of <= 1024 values). Same algorithm, working sets in a per-warp global scratch:
+// BFS augmentation over explicit frontier lists, Warshall over n x n member bit rows.
+struct BigScratch {
+    uint32_t* D;     // [n][uw] member domains in the value universe
+    uint32_t* anc;   // [n][nwm] ancestor sets
+    int32_t* owner;  // [uw*32] matched value -> member
+    int32_t* layer;  // [n]
+    int32_t* fl;     // [2][n] BFS frontier lists
+    uint32_t* vec;   // [6][uw] vis, nv, MV, F, KEEP, spare
+    uint32_t* mset;  // [2][nwm] seed set, pivot set
+    int32_t* cnt;    // [4]
+};
+
+__device__ inline BigScratch big_layout(uint32_t* base, int n, int uw) {
+    const int nwm = (n + 31) / 32;
+    BigScratch S;
+    uint32_t* p = base;
+    S.D = p;
+    p += (size_t)n * uw;
+    S.anc = p;
+    p += (size_t)n * nwm;
+    S.owner = reinterpret_cast<int32_t*>(p);
+    p += (size_t)uw * 32;
+    S.layer = reinterpret_cast<int32_t*>(p);
+    p += n;
+    S.fl = reinterpret_cast<int32_t*>(p);
+    p += 2 * (size_t)n;
+    S.vec = p;
+    p += 6 * (size_t)uw;
+    S.mset = p;
+    p += 2 * (size_t)nwm;
+    S.cnt = reinterpret_cast<int32_t*>(p);
+    return S;
+}
+
+__device__ __forceinline__ bool bit_of(const uint32_t* v, int j) { return (v[j >> 5] >> (j & 31)) & 1u; }
+
+// BFS augmenting path from member r over the generic layout; true on success
+__device__ inline bool big_augment(int r, int n, int uw, const BigScratch& S, int16_t* mates, int lane) {
+    uint32_t *vis = S.vec, *nv = S.vec + uw, *MV = S.vec + 2 * uw;
+    for (int w = lane; w < uw; w += 32) vis[w] = 0;
+    for (int k = lane; k < n; k += 32) S.layer[k] = -1;
+    __syncwarp();
+    if (lane == 0) {
+        S.fl[0] = r;
+        S.cnt[0] = 1;
+        S.layer[r] = 0;
+    }
+    __syncwarp();
+    int cur = 0, L = 0;
+    for (;;) {
+        const int c = S.cnt[cur];
+        const int32_t* fr = S.fl + (size_t)cur * n;
+        bool any = false;
+        int found = 0x7fffffff;
+        for (int w = lane; w < uw; w += 32) {
+            uint32_t acc = 0;
+            for (int i = 0; i < c; ++i) acc |= S.D[(size_t)fr[i] * uw + w];
+            const uint32_t x = acc & ~vis[w];
+            nv[w] = x;
+            vis[w] |= x;
+            any |= x != 0;
+            const uint32_t f = x & ~MV[w];
+            if (f && found == 0x7fffffff) found = w * 32 + __ffs(f) - 1;
+        }
+        any = __any_sync(FULL, any);
+        found = __reduce_min_sync(FULL, (unsigned)found);
+        if (!any) return false;
+        if (found != 0x7fffffff) {
+            int j = found;
+            for (int l = L;; --l) {
+                int best = 0x7fffffff;
+                for (int k = lane; k < n; k += 32)
+                    if (S.layer[k] == l && bit_of(S.D + (size_t)k * uw, j) && k < best) best = k;
+                const int k = (int)__reduce_min_sync(FULL, (unsigned)best);
+                const int old = mates[k];
+                __syncwarp();
+                if (lane == 0) {
+                    mates[k] = (int16_t)j;
+                    S.owner[j] = k;
+                }
+                __syncwarp();
+                if (l == 0) break;
+                j = old;
+            }
+            if (lane == 0) MV[found >> 5] |= 1u << (found & 31);
+            __syncwarp();
+            return true;
+        }
+        __syncwarp();
+        if (lane == 0) S.cnt[cur ^ 1] = 0;
+        __syncwarp();
+        int32_t* nx = S.fl + (size_t)(cur ^ 1) * n;
+        for (int w = lane; w < uw; w += 32) {
+            uint32_t x = nv[w];
+            while (x) {
+                const int j = w * 32 + __ffs(x) - 1;
+                x &= x - 1;
+                const int k = S.owner[j];
+                S.layer[k] = L + 1;
+                nx[atomicAdd(&S.cnt[cur ^ 1], 1)] = k;
+            }
+        }
+        __syncwarp();
+        cur ^= 1;
+        ++L;
+    }
+}
+
+template <int W>
+__device__ void big_load(const DevModel& M, int a, const uint32_t* dom, const BigScratch& S, int n, int uw, int lane) {
+    const int b = M.ad_start[a];
+    for (int k = lane; k < n; k += 32) {
+        const uint32_t* dv = dom + (size_t)M.ad_var[b + k] * W;
+        const int sh = M.ad_shift[b + k];
+        for (int w = 0; w < uw; ++w) S.D[(size_t)k * uw + w] = shifted_word<W>(dv, w, sh);
+    }
+    __syncwarp();
+}
+
+// universe-space removals of member k back to its own bits
+template <int W>
+__device__ __forceinline__ void big_remove(uint32_t* rm, int v, int sh, int w, uint32_t cand) {
+    while (cand) {
+        const int vb = w * 32 + __ffs(cand) - 1 - sh;
+        cand &= cand - 1;
+        if (vb >= 0 && vb < W * 32) atomicOr(rm + (size_t)v * W + (vb >> 5), 1u << (vb & 31));
+    }
+}
+
+template <int W>
+__device__ void prop_alldiff_gac_big(const DevModel& M, int a, const uint32_t* dom, uint32_t* rm, int16_t* mates,
+                                     uint32_t* scratch, int lane, int exact_wipe) {
+    const int b = M.ad_start[a], n = M.ad_start[a + 1] - b, uw = M.ad_uw[a], nwm = (n + 31) / 32;
+    const BigScratch S = big_layout(scratch, n, uw);
+    uint32_t *MV = S.vec + 2 * uw, *F = S.vec + 3 * uw, *KEEP = S.vec + 4 * uw;
+    uint32_t *SEED = S.mset, *PIV = S.mset + nwm;
+    big_load<W>(M, a, dom, S, n, uw, lane);
+    for (int w = lane; w < uw; w += 32) MV[w] = 0;
+    __syncwarp();
+    for (int k = lane; k < n; k += 32) { // warm start: keep still-valid matched edges
+        int m = mates[k];
+        if (m >= 0 && !bit_of(S.D + (size_t)k * uw, m)) m = mates[k] = -1;
+        if (m >= 0) {
+            atomicOr(MV + (m >> 5), 1u << (m & 31));
+            S.owner[m] = k;
+        }
+    }
+    __syncwarp();
+    int fail = -1;
+    for (int base = 0; base < n && fail < 0; base += 32) {
+        unsigned unm = __ballot_sync(FULL, base + lane < n && mates[base + lane] < 0);
+        while (unm) {
+            const int r = base + __ffs(unm) - 1;
+            unm &= unm - 1;
+            if (!big_augment(r, n, uw, S, mates, lane)) {
+                fail = r;
+                break;
+            }
+        }
+    }
+    if (fail >= 0) {
+        if (exact_wipe) { // greedy matching in member order: its first failure is Kuhn's
+            for (int k = lane; k < n; k += 32) mates[k] = -1;
+            for (int w = lane; w < uw; w += 32) MV[w] = 0;
+            __syncwarp();
+            for (int r = 0; r < n; ++r)
+                if (!big_augment(r, n, uw, S, mates, lane)) {
+                    fail = r;
+                    break;
+                }
+        }
+        if (lane == 0) {
+            const int v = M.ad_var[b + fail];
+            for (int w = 0; w < W; ++w) {
+                const uint32_t d = dom[(size_t)v * W + w];
+                if (d) atomicOr(rm + (size_t)v * W + w, d);
+            }
+        }
+        __syncwarp();
+        return;
+    }
+    // free values, predecessor rows, seeds, pivots
+    for (int w = lane; w < uw; w += 32) {
+        uint32_t u = 0;
+        for (int k = 0; k < n; ++k) u |= S.D[(size_t)k * uw + w];
+        F[w] = u & ~MV[w];
+        KEEP[w] = F[w];
+    }
+    for (int i = lane; i < 2 * nwm; i += 32) S.mset[i] = 0;
+    __syncwarp();
+    for (int k = lane; k < n; k += 32) {
+        uint32_t* row = S.anc + (size_t)k * nwm;
+        for (int i = 0; i < nwm; ++i) row[i] = 0;
+        bool seed = false;
+        int size = 0;
+        for (int w = 0; w < uw; ++w) {
+            const uint32_t d = S.D[(size_t)k * uw + w];
+            size += __popc(d);
+            seed |= (d & F[w]) != 0;
+            uint32_t x = d & MV[w];
+            while (x) {
+                const int m = S.owner[w * 32 + __ffs(x) - 1];
+                x &= x - 1;
+                row[m >> 5] |= 1u << (m & 31);
+            }
+        }
+        if (seed) atomicOr(SEED + (k >> 5), 1u << (k & 31));
+        if (size > 1) atomicOr(PIV + (k >> 5), 1u << (k & 31));
+    }
+    __syncwarp();
+    for (int pw = 0; pw < nwm; ++pw) { // Warshall over the non-singleton pivots
+        uint32_t pm = PIV[pw];
+        while (pm) {
+            const int p = pw * 32 + __ffs(pm) - 1;
+            pm &= pm - 1;
+            const uint32_t* rp = S.anc + (size_t)p * nwm;
+            for (int k = lane; k < n; k += 32) {
+                uint32_t* rk = S.anc + (size_t)k * nwm;
+                if (k != p && bit_of(rk, p))
+                    for (int i = 0; i < nwm; ++i) rk[i] |= rp[i];
+            }
+            __syncwarp();
+        }
+    }
+    for (int k = lane; k < n; k += 32) { // members reached from a free value keep their mate
+        const uint32_t* rk = S.anc + (size_t)k * nwm;
+        bool reached = bit_of(SEED, k);
+        for (int i = 0; i < nwm && !reached; ++i) reached = (rk[i] & SEED[i]) != 0;
+        const int m = mates[k];
+        if (reached && m >= 0) atomicOr(KEEP + (m >> 5), 1u << (m & 31));
+    }
+    __syncwarp();
+    for (int k = lane; k < n; k += 32) {
+        const int v = M.ad_var[b + k], sh = M.ad_shift[b + k], mk = mates[k];
+        const uint32_t* rk = S.anc + (size_t)k * nwm;
+        for (int w = 0; w < uw; ++w) {
+            uint32_t cand = S.D[(size_t)k * uw + w] & ~KEEP[w] & ~bitword(mk, w);
+            uint32_t x = cand;
+            while (x) {
+                const int bit = __ffs(x) - 1;
+                x &= x - 1;
+                const int m = S.owner[w * 32 + bit];
+                if (bit_of(rk, m) && bit_of(S.anc + (size_t)m * nwm, k)) cand &= ~(1u << bit);
+            }
+            if (cand) big_remove<W>(rm, v, sh, w, cand);
+        }
+    }
+    __syncwarp();
+}
+
+template <int W>
+__device__ void prop_alldiff_fc_big(const DevModel& M, int a, const uint32_t* dom, uint32_t* rm, uint32_t* scratch,
+                                    int lane) {
+    const int b = M.ad_start[a], n = M.ad_start[a + 1] - b, uw = M.ad_uw[a];
+    const BigScratch S = big_layout(scratch, n, uw);
+    uint32_t *once = S.vec, *twice = S.vec + uw;
+    big_load<W>(M, a, dom, S, n, uw, lane);
+    for (int w = lane; w < uw; w += 32) once[w] = twice[w] = 0;
+    __syncwarp();
+    for (int k = lane; k < n; k += 32) {
+        int size = 0, j = -1;
+        for (int w = 0; w < uw; ++w) {
+            const uint32_t d = S.D[(size_t)k * uw + w];
+            if (d && j < 0) j = w * 32 + __ffs(d) - 1;
+            size += __popc(d);
+        }
+        if (size == 1) {
+            const uint32_t old = atomicOr(once + (j >> 5), 1u << (j & 31));
+            if (old & (1u << (j & 31))) atomicOr(twice + (j >> 5), 1u << (j & 31));
+        }
+        S.layer[k] = size == 1 ? j : -1;
+    }
+    __syncwarp();
+    for (int k = lane; k < n; k += 32) {
+        const int v = M.ad_var[b + k], sh = M.ad_shift[b + k], j = S.layer[k];
+        for (int w = 0; w < uw; ++w) {
+            const uint32_t own = bitword(j, w);
+            uint32_t rem = (j >= 0 ? ((once[w] & ~own) | (twice[w] & own)) : once[w]) & S.D[(size_t)k * uw + w];
+            if (rem) big_remove<W>(rm, v, sh, w, rem);
+        }
+    }
+    __syncwarp();
+}
+
 // ------------------------------------------------------------------ one bulk-synchronous round
 struct RoundCtx {
     uint32_t* dom;
@@ -608,6 +895,7 @@ struct RoundCtx {
     uint32_t* chg0;     // [ceil(n/32)] vars changed since the last fixpoint (round-1 triggers)
     uint32_t* chg1;     // [ceil(n/32)] second buffer (null: triggers disabled, full sweeps)
     bool ne_events;     // var-form != handled by the singleton-event path (search kernel)
+    uint32_t* big;      // this block's generic-alldifferent scratch ([warps][M.big_words]) or null
     uint8_t* scratch;   // per-warp GAC scratch
     int scratch_stride; // bytes per warp
     const uint8_t* enabled;
@@ -698,7 +986,11 @@ __device__ __forceinline__ void run_propagators(const DevModel& M, const RoundCt
                 for (int t = b + lane; t < e; t += 32) hit |= trig_bit(trig, M.ad_var[t]);
                 if (!__any_sync(FULL, hit)) continue;
             }
-            if (R.alldiff) {
+            if (M.ad_uw[a] > 0) { // generic path: many members or a wide value universe
+                uint32_t* scratch = R.big + (size_t)warp * M.big_words;
+                if (R.alldiff) prop_alldiff_gac_big<W>(M, a, R.dom, R.rm, R.mates + M.ad_start[a], scratch, lane, R.exact_wipe);
+                else prop_alldiff_fc_big<W>(M, a, R.dom, R.rm, scratch, lane);
+            } else if (R.alldiff) {
                 uint32_t* post = R.post ? R.post + (size_t)M.ad_start[a] * W : nullptr;
                 if (M.ad_start[a + 1] - M.ad_start[a] <= 32)
                     prop_alldiff_gac<W, false>(M, a, R.dom, R.rm, R.mates + M.ad_start[a], ws, lane, R.exact_wipe, post,

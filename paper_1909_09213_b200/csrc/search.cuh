@@ -134,8 +134,10 @@ __global__ void __launch_bounds__(ONE ? 32 : 1024, ONE ? 32 : 1) search_kernel(c
     uint32_t* chg0 = L.has_chg ? reinterpret_cast<uint32_t*>(smem + L.chg) : nullptr;
     uint32_t* chg1 = L.has_chg ? chg0 + ((n + 31) >> 5) : nullptr;
     const int nbw = (n + 31) >> 5;
-    RoundCtx R{dom, rm, mates, post, post_ok, chg0, chg1, L.has_chg, smem + L.scratch, L.stride, nullptr, P.alldiff,
-               P.exact_wipe};
+    RoundCtx R{dom,     rm,      mates,     post,
+               post_ok, chg0,    chg1,      L.has_chg,
+               P.big_scratch ? P.big_scratch + (size_t)ctx * nw * M.big_words : nullptr,
+               smem + L.scratch, L.stride, nullptr, P.alldiff, P.exact_wipe};
     bool first_all = true; // the root's first round evaluates every propagator
     int trig_var = -1;     // var changed by the branch that created the current node
     uint32_t* frames = P.frames + (size_t)ctx * P.frame_cap * NWP;
@@ -499,7 +501,7 @@ __global__ void __launch_bounds__(1024) propagate_kernel(const PropParams P, uin
     int16_t* mates = reinterpret_cast<int16_t*>(smem + L.mates);
     uint32_t* chg0 = L.has_chg ? reinterpret_cast<uint32_t*>(smem + L.chg) : nullptr;
     RoundCtx R{dom, rm, mates, nullptr, nullptr, chg0, L.has_chg ? chg0 + ((M.n + 31) >> 5) : nullptr, false,
-               smem + L.scratch, L.stride, P.enabled, P.alldiff, 1};
+               P.big_scratch, smem + L.scratch, L.stride, P.enabled, P.alldiff, 1};
     for (size_t i = tid; i < NWP; i += T) {
         dom[i] = P.dom[i];
         rm[i] = 0;

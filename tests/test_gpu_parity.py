@@ -236,3 +236,57 @@ def test_sharded_search_sums_exactly(key, world):
     assert tuple(tot) == G.expected_tuple(g)
     merged = D.merge_keyed(streams)
     assert merged == [s.values for s in O.enumerate_solutions(m, cfg)]
+
+
+# ---- generic alldifferent path (> 64 members or a value universe wider than 1024)
+def _random_alldiff_model(rng, n, width, offsets=None):
+    offs = offsets or [1] * n
+    lines = [f"var v{i} in {offs[i]}..{offs[i] + width - 1};" for i in range(n)]
+    lines.append("constraint alldifferent(" + ", ".join(f"v{i}" for i in range(n)) + ");")
+    lines.append("solve satisfy;")
+    return S.parse_model("\n".join(lines))
+
+
+def test_big_alldiff_removals_and_fixpoints():
+    rng = models.Rng(4242)
+    for trial in range(40):
+        n = 65 + rng.below(60)
+        width = n + rng.below(8)
+        m = _random_alldiff_model(rng, n, width)
+        doms = []
+        for v in range(n):
+            d = S.Domain(1, width)
+            for x in range(1, width + 1):
+                if d.size() > 2 and rng.below(3) == 0:
+                    d.remove(x)
+            doms.append(d)
+        for level in (0, 1):
+            assert S.removals(m, doms, alldiff=level) == O.removals(m, doms, alldiff=level), (trial, level)
+            gd, gf = S.propagate_fixpoint(m, doms, alldiff=level)
+            od, of = O.propagate_fixpoint(m, doms, alldiff=level)
+            assert gf == of and gd == od, (trial, level)
+
+
+def test_wide_universe_alldiff():
+    rng = models.Rng(99)
+    for trial in range(40):
+        n = 3 + rng.below(6)
+        offs = [rng.range(-3000, 3000) for _ in range(n)]
+        # two members share a range so pruning happens; the rest sit far apart
+        offs[1] = offs[0]
+        m = _random_alldiff_model(rng, n, 3, offs)
+        doms = [S.Domain(o, o + 2) for o in offs]
+        doms[0].remove(offs[0] + 2)
+        doms[1].remove(offs[1] + 2)
+        for level in (0, 1):
+            assert S.removals(m, doms, alldiff=level) == O.removals(m, doms, alldiff=level), (trial, level)
+
+
+def test_big_alldiff_search_matches_oracle():
+    for n in (66, 70):
+        m = S.parse_model(models.gen_nqueens(n))
+        cfg = S.SearchConfig(max_solutions=1)
+        got, exp = [], []
+        r = S.solve_satisfy(m, cfg, lambda s: got.append(s.values) or True)
+        ro = O.solve_satisfy(m, cfg, lambda s: exp.append(s.values) or True)
+        assert r.stats.as_tuple() == ro.stats.as_tuple() and got == exp, n
