@@ -88,6 +88,7 @@ struct WorkState {
     uint64_t idle_cycles;  // sum over contexts of clock64 cycles waiting for work
     uint64_t lock_fails;   // unused (kept for the debug line)
     int32_t max_depth;     // deepest solution leaf (parallel): key words that can differ
+    int32_t best_lock;     // first mode: guards hot.has_bound, which then holds the best record
     int64_t n_tasks;       // frontier expansion: open nodes emitted at split_depth
 };
 
@@ -134,6 +135,15 @@ struct SearchParams {
     uint32_t* tasks;          // [task_cap][OS] same layout as an outbox slot
     // seeded parallel run: outbox slots [n_ctx, n_ctx + n_seed) hold pre-published tasks
     int32_t n_seed;
+    // exact parallel first solution (max_solutions == 1): every subtree handed out ("segment",
+    // id = ring ticket + 1; the root is segment 0) records its root path key and its own stats;
+    // solutions record their segment and segment-local stats; subtrees right of the best
+    // solution key found so far are abandoned. The host then sums exactly the reference's prefix.
+    int32_t first_mode;
+    int64_t seg_cap;
+    uint32_t* seg_key;     // [seg_cap][KW]
+    uint64_t* seg_stats;   // [seg_cap][3]
+    int32_t* sol_seg;      // [sol_cap]
 };
 
 struct PropParams {

@@ -454,6 +454,13 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
     const int n = P.n;
     const bool parallel = engine == CUBICS_ENGINE_PARALLEL;
     const bool keyed = parallel || (shard && shard->split_depth > 0);
+    // exact parallel first solution: complete otherwise-equal search, max_solutions == 1
+    const bool first_mode = parallel && !shard && hm.goal == CUBICS_SATISFY && cfg.max_solutions == 1 &&
+                            cfg.node_limit == 0;
+    if (first_mode) {
+        record = true;
+        sol_cap = 65536;
+    }
     const int KW = keyed ? static_cast<int>((P.depth_bound + 1 + 31) / 32) : 0;
     const int n_seed = (shard && shard->seeds) ? static_cast<int>(shard->seeds->size()) : 0;
     if (parallel && KW > 4096) throw StatusError{CUBICS_E_UNSUPPORTED, "search tree too deep for ordered parallel keys"};
@@ -515,19 +522,25 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
     const size_t a_seedidx = take(sizeof(int32_t) * n_seed);
     const size_t a_svals = take(sizeof(uint16_t) * n * sol_cap);
     const size_t a_skeys = take(sizeof(uint32_t) * KW * sol_cap);
-    const size_t a_sstats = take(parallel ? 0 : sizeof(uint64_t) * 3 * sol_cap);
+    const size_t a_sstats = take(parallel && !first_mode ? 0 : sizeof(uint64_t) * 3 * sol_cap);
     const size_t a_fkey = take(sizeof(uint32_t) * KW * n_ctx);
     const size_t a_fval = take(parallel ? sizeof(uint16_t) * n * n_ctx : 0);
     const size_t a_inc = take(sizeof(uint16_t) * std::max(n, 1));
+    // one segment per handed-out subtree; sized by memory (<= 1 GiB), parity fallback beyond
+    const int64_t seg_cap = first_mode ? std::min<int64_t>((int64_t)1 << 21, ((int64_t)1 << 30) / (4 * KW + 24)) : 0;
+    const size_t a_segk = take(sizeof(uint32_t) * KW * seg_cap);
+    const size_t a_segs = take(sizeof(uint64_t) * 3 * seg_cap);
+    const size_t a_sseg = take(first_mode ? sizeof(int32_t) * sol_cap : 0);
     uint8_t* base = device_arena(dev, off);
 
     cudaStream_t st = g_dev[dev].stream;
     cudaEvent_t e0 = g_dev[dev].e0, e1 = g_dev[dev].e1;
+    bool recorded_first_done = false;
     {
         // staging: blob + initial WorkState in pinned memory, one H2D copy
         WorkState w0{};
         w0.outstanding = n_ctx + n_seed;
-        w0.hot.has_bound = cfg.has_initial_bound ? 1 : 0;
+        w0.hot.has_bound = first_mode ? -1 : (cfg.has_initial_bound ? 1 : 0);
         w0.bound = cfg.initial_bound;
         w0.hot.push_ticket = (uint32_t)n_seed;
         const size_t stage_bytes = a_ws + sizeof(WorkState);
@@ -538,6 +551,10 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
         CU(cudaMemcpyAsync(base, stage, stage_bytes, cudaMemcpyHostToDevice, st));
         out.h2d += stage_bytes;
         CU(cudaMemsetAsync(base + a_queue, 0, zero_end - a_queue, st));
+        if (first_mode) {
+            CU(cudaMemsetAsync(base + a_segk, 0, sizeof(uint32_t) * KW * seg_cap, st));
+            CU(cudaMemsetAsync(base + a_segs, 0, sizeof(uint64_t) * 3 * seg_cap, st));
+        }
         if (n_seed) { // pre-published tasks: ring tickets 0..n_seed-1 point at outbox slots n_ctx+i
             std::vector<unsigned long long> ring0(n_seed);
             for (int i = 0; i < n_seed; ++i) ring0[i] = ((unsigned long long)(i + 1) << 32) | (unsigned)(n_ctx + i);
@@ -590,6 +607,11 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
         S.task_cap = shard ? (int64_t)shard->task_cap : 0;
         S.tasks = shard ? shard->task_dev : nullptr;
         S.n_seed = n_seed;
+        S.first_mode = first_mode ? 1 : 0;
+        S.seg_cap = seg_cap;
+        S.seg_key = reinterpret_cast<uint32_t*>(base + a_segk);
+        S.seg_stats = reinterpret_cast<uint64_t*>(base + a_segs);
+        S.sol_seg = reinterpret_cast<int32_t*>(base + a_sseg);
 
         CU(cudaEventRecord(e0, st));
 #define LS(w) launch_search<w>(S, n_ctx, block, L.total, st)
@@ -603,10 +625,52 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
         float ms = 0;
         CU(cudaEventElapsedTime(&ms, e0, e1));
         out.device_ms = ms;
+        if (first_mode) { // the reference's prefix up to the DFS-first solution, summed exactly
+            const uint64_t nseg = (uint64_t)out.ws.hot.push_ticket + 1, nsol = out.ws.sol_count;
+            if (nseg > (uint64_t)seg_cap || nsol > sol_cap)
+                throw StatusError{CUBICS_E_CAPACITY, "first-solution bookkeeping capacity"};
+            std::vector<uint32_t> sk(nseg * KW), solk(nsol * KW);
+            std::vector<uint64_t> ss(nseg * 3), sst(nsol * 3);
+            std::vector<int32_t> sseg(nsol);
+            CU(cudaMemcpyAsync(sk.data(), base + a_segk, sizeof(uint32_t) * KW * nseg, cudaMemcpyDeviceToHost, st));
+            CU(cudaMemcpyAsync(ss.data(), base + a_segs, sizeof(uint64_t) * 3 * nseg, cudaMemcpyDeviceToHost, st));
+            if (nsol) {
+                CU(cudaMemcpyAsync(solk.data(), base + a_skeys, sizeof(uint32_t) * KW * nsol, cudaMemcpyDeviceToHost, st));
+                CU(cudaMemcpyAsync(sst.data(), base + a_sstats, sizeof(uint64_t) * 3 * nsol, cudaMemcpyDeviceToHost, st));
+                CU(cudaMemcpyAsync(sseg.data(), base + a_sseg, sizeof(int32_t) * nsol, cudaMemcpyDeviceToHost, st));
+            }
+            CU(cudaStreamSynchronize(st));
+            out.d2h += sizeof(uint32_t) * KW * (nseg + nsol) + sizeof(uint64_t) * 3 * (nseg + nsol) + 4 * nsol;
+            auto less = [&](const uint32_t* a, const uint32_t* b) { return std::lexicographical_compare(a, a + KW, b, b + KW); };
+            int64_t best = -1;
+            for (uint64_t i = 0; i < nsol; ++i)
+                if (best < 0 || less(&solk[i * KW], &solk[best * KW])) best = (int64_t)i;
+            uint64_t tot[3] = {0, 0, 0};
+            for (uint64_t s = 0; s < nseg; ++s) {
+                if (best >= 0 && (int64_t)sseg[best] == (int64_t)s) continue;
+                if (best >= 0 && less(&solk[best * KW], &sk[s * KW])) continue; // right of the answer
+                for (int i = 0; i < 3; ++i) tot[i] += ss[s * 3 + i];
+            }
+            if (best >= 0) {
+                for (int i = 0; i < 3; ++i) tot[i] += sst[best * 3 + i];
+                out.rec.count = 1;
+                out.rec.ordered = true;
+                out.rec.vals.resize(n);
+                CU(cudaMemcpy(out.rec.vals.data(), base + a_svals + sizeof(uint16_t) * n * best, sizeof(uint16_t) * n,
+                              cudaMemcpyDeviceToHost));
+                out.d2h += sizeof(uint16_t) * n;
+                out.ws.user_stop = 1; // max_solutions reached, as the reference reports it
+            }
+            out.ws.stats[0] = tot[0];
+            out.ws.stats[1] = tot[1];
+            out.ws.stats[2] = tot[2];
+            out.ws.stats[3] = best >= 0 ? 1 : 0;
+            recorded_first_done = true;
+        }
         const uint64_t got = std::min<uint64_t>(out.ws.sol_count ? out.ws.sol_count : 0, sol_cap);
         uint64_t recorded = parallel ? got : std::min<uint64_t>(out.ws.stats[3], sol_cap);
-        out.rec.count = recorded;
-        if (recorded) {
+        if (!recorded_first_done) out.rec.count = recorded;
+        if (recorded && !recorded_first_done) {
             out.rec.vals.resize(recorded * n);
             const uint16_t* src = reinterpret_cast<const uint16_t*>(base + a_svals);
             if (parallel && KW && n && recorded > 1 && !want_keys) {
@@ -631,7 +695,7 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
                 out.d2h += sizeof(uint64_t) * 3 * recorded;
             }
         }
-        if (parallel && KW && n) { // DFS-first solution over the contexts' firsts
+        if (parallel && KW && n && !first_mode) { // DFS-first solution over the contexts' firsts
             std::vector<int32_t> hf(n_ctx);
             std::vector<uint32_t> fk((size_t)KW * n_ctx);
             CU(cudaMemcpyAsync(hf.data(), base + a_hf, sizeof(int32_t) * n_ctx, cudaMemcpyDeviceToHost, st));
@@ -693,13 +757,15 @@ void fill_result(const RunOut& r, cubics_result* out) {
 int pick_engine(const cubics_search_config& cfg, bool optimize_goal) {
     if (cfg.engine == CUBICS_ENGINE_PARITY || cfg.engine == CUBICS_ENGINE_PARALLEL) {
         if (cfg.engine == CUBICS_ENGINE_PARALLEL &&
-            (cfg.node_limit != 0 || (!optimize_goal && cfg.max_solutions != std::numeric_limits<uint64_t>::max())))
+            (cfg.node_limit != 0 ||
+             (!optimize_goal && cfg.max_solutions != std::numeric_limits<uint64_t>::max() && cfg.max_solutions != 1)))
             throw StatusError{CUBICS_E_UNSUPPORTED,
                               "parallel engine needs a complete search (no node_limit, unbounded max_solutions)"};
         return cfg.engine;
     }
-    if (!optimize_goal && cfg.node_limit == 0 && cfg.max_solutions == std::numeric_limits<uint64_t>::max())
-        return CUBICS_ENGINE_PARALLEL;
+    if (!optimize_goal && cfg.node_limit == 0 &&
+        (cfg.max_solutions == std::numeric_limits<uint64_t>::max() || cfg.max_solutions == 1))
+        return CUBICS_ENGINE_PARALLEL; // complete enumeration, or the exact parallel first solution
     return CUBICS_ENGINE_PARITY;
 }
 
@@ -757,10 +823,19 @@ int satisfy_records(const HostModel& m, const cubics_search_config& cfg, bool re
     std::memset(out, 0, sizeof *out);
     // an objective makes the stream a sequence of incumbents, whose order only the reference
     // node order reproduces: AUTO picks the parity engine then
-    const int engine = pick_engine(cfg, m.goal != CUBICS_SATISFY);
+    int engine = pick_engine(cfg, m.goal != CUBICS_SATISFY);
     uint64_t cap = default_sol_cap(m, cfg);
     RunOut r;
-    run_search(m, cfg, engine, record, cap, r);
+    try {
+        run_search(m, cfg, engine, record, cap, r);
+    } catch (const StatusError& e) {
+        // the exact parallel first solution ran out of bookkeeping space: the parity engine
+        // gives the same answer and stats
+        if (e.code != CUBICS_E_CAPACITY || engine != CUBICS_ENGINE_PARALLEL || cfg.max_solutions != 1) throw;
+        engine = CUBICS_ENGINE_PARITY;
+        r = RunOut{};
+        run_search(m, cfg, engine, record, cap, r);
+    }
     if (record && r.ws.stats[3] > r.rec.count && r.rec.count == cap) { // buffer overflow: rerun exact
         RunOut r2;
         run_search(m, cfg, engine, record, r.ws.stats[3], r2);

@@ -139,6 +139,7 @@ __global__ void __launch_bounds__(ONE ? 32 : 1024, ONE ? 32 : 1) search_kernel(c
                P.big_scratch ? P.big_scratch + (size_t)ctx * nw * M.big_words : nullptr,
                smem + L.scratch, L.stride, nullptr, P.alldiff, P.exact_wipe};
     bool first_all = true; // the root's first round evaluates every propagator
+    bool skip_node = false; // first mode: the task just taken lies right of the best solution
     int trig_var = -1;     // var changed by the branch that created the current node
     uint32_t* frames = P.frames + (size_t)ctx * P.frame_cap * NWP;
     int32_t* meta = P.frame_meta + (size_t)ctx * P.frame_cap * 4;
@@ -170,6 +171,44 @@ __global__ void __launch_bounds__(ONE ? 32 : 1024, ONE ? 32 : 1) search_kernel(c
 
     long long idle_cyc = 0, steals = 0, donations = 0;
     const long long t_start = clock64();
+    // first mode: current segment and the counters at its start; thread 0 caches the best key
+    const bool first_mode = P.first_mode != 0;
+    long long seg = (!parallel || ctx == 0) && !P.n_seed ? 0 : -1;
+    unsigned long long seg_n0 = 0, seg_f0 = 0, seg_r0 = 0;
+    int gbest_idx = -1;
+    auto flush_seg = [&]() {
+        if (first_mode && tid == 0 && seg >= 0 && seg < P.seg_cap) {
+            P.seg_stats[seg * 3 + 0] = nodes - seg_n0;
+            P.seg_stats[seg * 3 + 1] = failures - seg_f0;
+            P.seg_stats[seg * 3 + 2] = rounds - seg_r0;
+        }
+    };
+    // first mode: is the current path key right of the best solution key (thread 0 only)?
+    auto right_of_best = [&]() -> bool {
+        const int bi = (int)hot.w;
+        if (bi < 0) return false;
+        if (bi != gbest_idx) {
+            gbest_idx = bi;
+            for (int i = 0; i < KW; ++i) bestkey[i] = __ldcg(P.sol_keys + (size_t)bi * KW + i);
+        }
+        for (int i = 0; i < KW; ++i)
+            if (path[i] != bestkey[i]) return path[i] > bestkey[i];
+        return false;
+    };
+    // first mode: is the right branch taken at depth d (key: path prefix, bit d) right of the best?
+    auto frame_right_of_best = [&](int d) -> bool {
+        const int bi = (int)hot.w;
+        if (bi < 0) return false;
+        if (bi != gbest_idx) {
+            gbest_idx = bi;
+            for (int i = 0; i < KW; ++i) bestkey[i] = __ldcg(P.sol_keys + (size_t)bi * KW + i);
+        }
+        for (int i = 0; i < KW; ++i) {
+            const uint32_t k = path_right_word(path[i], i, d);
+            if (k != bestkey[i]) return k > bestkey[i];
+        }
+        return false;
+    };
 
     // Idle: take a ticket and wait for the task published under it (lock-free ticket queue:
     // each waiter spins on its own ring slot, so there is no shared hot spot to contend on).
@@ -196,10 +235,15 @@ __global__ void __launch_bounds__(ONE ? 32 : 1024, ONE ? 32 : 1) search_kernel(c
             }
             idle_cyc += clock64() - t0;
             s_src = got;
+            s_ll = (long long)t + 1; // segment id of the subtree published under ticket t
         }
         bar<ONE>();
         const int got = s_src;
         if (got < 0) return false;
+        seg = s_ll;
+        seg_n0 = nodes;
+        seg_f0 = failures;
+        seg_r0 = rounds;
         const uint32_t* ob = P.outbox + (size_t)got * OS;
         copy4_cg<ONE>(dom, ob, NWP);
         for (int i = tid; i < KW; i += T) path[i] = __ldcg(ob + NWP + i);
@@ -216,6 +260,19 @@ __global__ void __launch_bounds__(ONE ? 32 : 1024, ONE ? 32 : 1) search_kernel(c
         sp = base = 0;
         first_all = false;
         trig_var = tvar;
+        if (first_mode) {
+            if (seg < P.seg_cap)
+                for (int i = tid; i < KW; i += T) P.seg_key[(size_t)seg * KW + i] = path[i];
+            if (tid == 0) {
+                hot = ld_volatile_v4(reinterpret_cast<const uint4*>(&ws->hot));
+                s_flag = right_of_best(); // the whole subtree lies right of a known solution
+            }
+            bar<ONE>();
+            if (s_flag) {
+                flush_seg();
+                skip_node = true; // zero nodes: the main loop's backtrack takes the next task
+            }
+        }
         return true;
     };
 
@@ -230,7 +287,10 @@ __global__ void __launch_bounds__(ONE ? 32 : 1024, ONE ? 32 : 1) search_kernel(c
 
     while (have_work) {
         bool backtrack = false;
-        if (P.split_depth >= 0 && depth >= P.split_depth) {
+        if (skip_node) {
+            skip_node = false;
+            backtrack = true;
+        } else if (P.split_depth >= 0 && depth >= P.split_depth) {
             // ============ frontier expansion: this open node becomes a task (counted by its shard)
             if (tid == 0) s_ll = (long long)atomicAdd((unsigned long long*)&ws->n_tasks, 1ull);
             bar<ONE>();
@@ -313,22 +373,48 @@ __global__ void __launch_bounds__(ONE ? 32 : 1024, ONE ? 32 : 1) search_kernel(c
             if (sel < 0) {
                 // ============ solution leaf (emit_solution, search.cpp:134-156)
                 if (tid == 0) {
-                    s_ll = parallel ? (long long)atomicAdd((unsigned long long*)&ws->sol_count, 1ull) : (long long)sols;
+                    if (first_mode) // only a solution left of the best known one can matter
+                        s_ll = right_of_best() ? -1 : (long long)atomicAdd((unsigned long long*)&ws->sol_count, 1ull);
+                    else
+                        s_ll = parallel ? (long long)atomicAdd((unsigned long long*)&ws->sol_count, 1ull) : (long long)sols;
                     if (parallel) atomicMax(&ws->max_depth, depth);
                 }
                 bar<ONE>();
-                const unsigned long long idx = (unsigned long long)s_ll;
+                const long long sidx = s_ll;
+                const unsigned long long idx = (unsigned long long)sidx;
                 ++sols;
-                if (P.record && idx < P.sol_cap) {
+                if (P.record && sidx >= 0 && idx < P.sol_cap) {
                     for (int v = tid; v < n; v += T) P.sol_vals[idx * n + v] = (uint16_t)dom_first<W>(dom + (size_t)v * W);
                     for (int i = tid; i < KW; i += T) P.sol_keys[idx * KW + i] = path[i];
-                    if (tid == 0 && !parallel) {
-                        P.sol_stats[idx * 3 + 0] = nodes;
-                        P.sol_stats[idx * 3 + 1] = failures;
-                        P.sol_stats[idx * 3 + 2] = rounds;
+                    if (tid == 0 && (!parallel || first_mode)) { // parity: global; first mode: segment-local
+                        P.sol_stats[idx * 3 + 0] = nodes - seg_n0;
+                        P.sol_stats[idx * 3 + 1] = failures - seg_f0;
+                        P.sol_stats[idx * 3 + 2] = rounds - seg_r0;
+                        if (first_mode) P.sol_seg[idx] = (int32_t)seg;
                     }
                 }
-                if (parallel && KW > 0) { // per-context DFS-first solution
+                if (first_mode) {
+                    bar<ONE>();
+                    if (tid == 0 && sidx >= 0 && idx < P.sol_cap) { // publish as the best if still the best
+                        __threadfence();
+                        spin_lock(&ws->best_lock);
+                        volatile int32_t* gb = &ws->hot.has_bound;
+                        const int cur = *gb;
+                        bool better = cur < 0;
+                        for (int i = 0; i < KW && !better; ++i) {
+                            const uint32_t a = path[i], b = __ldcg(P.sol_keys + (size_t)cur * KW + i);
+                            if (a != b) {
+                                better = a < b;
+                                break;
+                            }
+                        }
+                        if (better) *gb = (int32_t)idx;
+                        spin_unlock(&ws->best_lock);
+                    }
+                    // everything this context would visit next lies right of this solution
+                    sp = base;
+                }
+                if (parallel && KW > 0 && !first_mode) { // per-context DFS-first solution
                     if (tid == 0) {
                         int less = 0;
                         for (int i = 0; i < KW; ++i)
@@ -398,6 +484,9 @@ __global__ void __launch_bounds__(ONE ? 32 : 1024, ONE ? 32 : 1) search_kernel(c
                     // donate the shallowest pending right branch when someone waits for work
                     int want = hot.z ? 2 : 0;
                     if (parallel && !want && sp + 1 > base && !my_busy && hot.y > hot.x) want = 1;
+                    // first mode: pending branches right of the best solution are dropped, never
+                    // handed out (the shallowest pending branch is the rightmost one)
+                    if (first_mode && want == 1 && frame_right_of_best(meta[base * 4 + 2])) want = 3;
                     s_flag = want;
                 }
                 bar<ONE>();
@@ -408,6 +497,7 @@ __global__ void __launch_bounds__(ONE ? 32 : 1024, ONE ? 32 : 1) search_kernel(c
                 ++depth;
                 const int want = s_flag;
                 if (want == 2) break;
+                if (want == 3) ++base;
                 if (want == 1) {
                     const int f = base++;
                     const int fvar = meta[f * 4 + 0], fbit = meta[f * 4 + 1], fdepth = meta[f * 4 + 2];
@@ -447,6 +537,7 @@ __global__ void __launch_bounds__(ONE ? 32 : 1024, ONE ? 32 : 1) search_kernel(c
         }
         if (sp == base) {
             if (!parallel) break;
+            flush_seg();
             have_work = get_work();
             bar<ONE>();
             continue;
@@ -464,11 +555,17 @@ __global__ void __launch_bounds__(ONE ? 32 : 1024, ONE ? 32 : 1) search_kernel(c
                 const int last = depth < KW * 32 ? depth : KW * 32 - 1;
                 for (int i = d >> 5; i <= (last >> 5); ++i) path[i] = path_right_word(path[i], i, d);
             }
+            if (first_mode) s_flag = right_of_best(); // this branch and all pending ones lie right of it
         }
         depth = d + 1;
         trig_var = var;
         bar<ONE>();
+        if (first_mode && s_flag) {
+            sp = base;
+            skip_node = true;
+        }
     }
+    flush_seg();
     bar<ONE>();
     if (parallel && tid == 0 && have_work) {
         // unwound by stop: this context no longer counts as outstanding

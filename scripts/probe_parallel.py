@@ -23,7 +23,8 @@ configs = [(A.ENGINE_PARITY, 0, 0)] if "--parity" in args else []
 if "--no-parallel" not in args:
     configs += [(A.ENGINE_PARALLEL, c, b) for c in grid for b in blocks]
 for eng, ctx, blk in configs:
-    cfg = S.SearchConfig(engine=eng, contexts=ctx, block_threads=blk, count_only=True)
+    cfg = S.SearchConfig(engine=eng, contexts=ctx, block_threads=blk, count_only=True,
+                         max_solutions=1 if "--first" in args else A.UINT64_MAX)
     if m.goal != 0:
         r = S.solve_optimize(m, cfg)
         extra = f" obj={r.best.objective if r.best else None}"

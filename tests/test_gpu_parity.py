@@ -290,3 +290,14 @@ def test_big_alldiff_search_matches_oracle():
         r = S.solve_satisfy(m, cfg, lambda s: got.append(s.values) or True)
         ro = O.solve_satisfy(m, cfg, lambda s: exp.append(s.values) or True)
         assert r.stats.as_tuple() == ro.stats.as_tuple() and got == exp, n
+
+
+@pytest.mark.parametrize("key", ["nq8|--max 1", "nq14|--max 1", "nq24|--max 1", "nq40|--max 1", "magic4|--max 1",
+                                 "magic5|--max 1", "rcsp_1000|--max 1"])
+def test_parallel_first_solution_exact(key):
+    # many contexts, subtrees right of the best known solution abandoned, and still the
+    # reference's exact nodes/failures/rounds up to its DFS-first solution
+    g = G.goldens()[key]
+    stats, sol = gpu_case(key, PARALLEL)
+    assert stats == G.expected_tuple(g)
+    assert sol == g["first"]
