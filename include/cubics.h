@@ -49,7 +49,8 @@ enum cubics_status {
 };
 
 /* ---- model vocabulary, numerically identical to the reference enums --------------------- */
-enum cubics_kind { CUBICS_RELBIN = 0, CUBICS_LINEAR = 1, CUBICS_ALLDIFF = 2 }; /* fd::ConstraintKind */
+enum cubics_kind { CUBICS_RELBIN = 0, CUBICS_LINEAR = 1, CUBICS_ALLDIFF = 2, /* fd::ConstraintKind */
+                   CUBICS_TABLE = 3 /* extension: positive extensional constraint (allowed tuples) */ };
 enum cubics_relop { CUBICS_LT = 0, CUBICS_LE, CUBICS_GT, CUBICS_GE, CUBICS_EQ, CUBICS_NE }; /* fd::RelOp */
 enum cubics_linop { CUBICS_LIN_LE = 0, CUBICS_LIN_EQ = 1 };                    /* fd::LinOp */
 enum cubics_goal { CUBICS_SATISFY = 0, CUBICS_MINIMIZE = 1, CUBICS_MAXIMIZE = 2 }; /* fd::Goal */
@@ -68,7 +69,12 @@ enum cubics_alldiff { CUBICS_FORWARD_CHECKING = 0, CUBICS_ARC_CONSISTENT = 1 }; 
  *            con_value = rhs_value (the literal, or k).               (model.hpp:26-32)
  *   LINEAR : terms = (term_coeff, term_var) pairs; con_op = linop; con_value = bound. (:42-46)
  *   ALLDIFF: terms = member vars; con_op and con_value ignored.        (:48-50)
- * term_coeff may be NULL when there is no LINEAR constraint.
+ *   TABLE  : terms = scope vars (k); con_value = number of allowed tuples t; the tuples are
+ *            t*k int64 values at table_data[con_value_offset...]: tuple i of constraint c is
+ *            table_data[table_start[c] + i*k .. + k). Extension beyond the reference (whose
+ *            Constraint variant has no table kind, model.hpp:52): BASELINE config 5.
+ * term_coeff may be NULL when there is no LINEAR constraint; table_start / table_data may be
+ * NULL when there is no TABLE constraint.
  */
 typedef struct cubics_model_desc {
     int32_t n_vars;
@@ -84,6 +90,8 @@ typedef struct cubics_model_desc {
     const int64_t* term_coeff;
     int32_t goal;     /* enum cubics_goal */
     int32_t goal_var; /* objective variable when goal != SATISFY */
+    const int64_t* table_start; /* n_cons entries (used for TABLE constraints only) */
+    const int64_t* table_data;
 } cubics_model_desc;
 
 typedef struct cubics_model cubics_model; /* opaque, host-side */

@@ -444,11 +444,39 @@ out:
     free(queue);
 }
 
+/* Extension (no reference counterpart, BASELINE config 5): positive table constraint. A value is
+ * supported when some allowed tuple has it in its position and every other component in the
+ * respective domain (positions are independent, as Linear treats repeated variables). */
+static void prop_table(const Model* m, int c, const uint64_t* S, uint64_t* R) {
+    const cubics_model_desc* d = m->d;
+    const int t0 = d->con_start[c], k = d->con_start[c + 1] - t0;
+    const int64_t nt = d->con_value[c];
+    const int64_t* data = d->table_data + d->table_start[c];
+    for (int j = 0; j < k; ++j)
+        if (d_size(m, S, d->term_var[t0 + j]) == 0) return;
+    uint64_t* sup = (uint64_t*)calloc((size_t)k * 16u, sizeof(uint64_t));
+    for (int64_t i = 0; i < nt; ++i) {
+        int valid = 1;
+        for (int j = 0; j < k && valid; ++j) valid = d_contains(m, S, d->term_var[t0 + j], data[i * k + j]);
+        if (!valid) continue;
+        for (int j = 0; j < k; ++j) {
+            int pos = (int)(data[i * k + j] - m->off[d->term_var[t0 + j]]);
+            sup[j * 16 + pos / 64] |= (uint64_t)1 << (pos % 64);
+        }
+    }
+    for (int j = 0; j < k; ++j) {
+        int v = d->term_var[t0 + j];
+        for (int w = 0; w < d_nw(m, v); ++w) R[m->ws[v] + w] |= S[m->ws[v] + w] & ~sup[j * 16 + w];
+    }
+    free(sup);
+}
+
 /* propagate_one (propagation.cpp:435-442). Returns nonzero on overflow. */
 static int propagate_one(const Model* m, int c, const uint64_t* S, uint64_t* R, int alldiff) {
     switch (m->d->con_kind[c]) {
     case CUBICS_RELBIN: prop_rel_bin(m, c, S, R); return 0;
     case CUBICS_LINEAR: return prop_linear(m, c, S, R);
+    case CUBICS_TABLE: prop_table(m, c, S, R); return 0;
     default:
         if (alldiff == CUBICS_ARC_CONSISTENT) prop_alldiff_gac(m, c, S, R);
         else prop_alldiff_fc(m, c, S, R);

@@ -16,7 +16,7 @@ OK, E_INVALID, E_PARSE, E_OVERFLOW, E_NO_OBJECTIVE, E_CUDA, E_CAPACITY, E_UNSUPP
 STATUS_NAMES = {0: "OK", 1: "INVALID", 2: "PARSE", 3: "OVERFLOW", 4: "NO_OBJECTIVE", 5: "CUDA",
                 6: "CAPACITY", 7: "UNSUPPORTED"}
 
-RELBIN, LINEAR, ALLDIFF = 0, 1, 2
+RELBIN, LINEAR, ALLDIFF, TABLE = 0, 1, 2, 3
 LT, LE, GT, GE, EQ, NE = range(6)
 LIN_LE, LIN_EQ = 0, 1
 SATISFY, MINIMIZE, MAXIMIZE = 0, 1, 2
@@ -41,6 +41,8 @@ class ModelDesc(C.Structure):
         ("term_coeff", C.POINTER(C.c_int64)),
         ("goal", C.c_int32),
         ("goal_var", C.c_int32),
+        ("table_start", C.POINTER(C.c_int64)),
+        ("table_data", C.POINTER(C.c_int64)),
     ]
 
 

@@ -46,6 +46,17 @@ struct DevModel {
     const int32_t* ad_uw;        // [na] 0: fast warp path (<= 64 members, universe in W words);
                                  //      > 0: generic path over a uw-word universe (big_words scratch)
     int32_t big_words;           // u32 words of per-warp scratch the generic path needs (0: none)
+    // positive table constraints (extension, BASELINE config 5)
+    int32_t ntb;                 // binary tables: bitwise arc consistency over support bitsets
+    const int32_t* tb_xy;        // [2*ntb] scope (x, y)
+    const int64_t* tb_off;       // [2*ntb] u32-word offsets of x's and y's support blocks in tb_sup
+    const uint32_t* tb_sup;      // block of x: width_x rows of W words, row a = y bits allowed with x=a
+    int32_t ntn;                 // n-ary tables (arity <= 8): tuple scan
+    const int32_t* tn_start;     // [ntn+1] scope CSR
+    const int32_t* tn_var;
+    const int64_t* tn_nt;        // [ntn] tuples
+    const int64_t* tn_off;       // [ntn] offset into tn_data
+    const int16_t* tn_data;      // tuples as bit indices (-1: value outside the domain range)
     int32_t total_members;
     int32_t goal;
     int32_t goal_var;

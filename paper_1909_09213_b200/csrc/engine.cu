@@ -111,6 +111,8 @@ struct Prepared {
     uint64_t depth_bound = 0; // sum(|D| - 1): max binary-tree depth
     Blob blob;
     size_t o_off, o_dom, o_rb, o_ls, o_lo, o_lb, o_lv, o_lc, o_as, o_av, o_ash, o_nes, o_nee, o_auw;
+    size_t o_tbxy, o_tboff, o_tbsup, o_tns, o_tnv, o_tnn, o_tno, o_tnd;
+    int ntb = 0, ntn = 0;
     size_t big_words = 0;
     int nr_gen = 0;
     std::vector<int> kind_index; // constraint index -> kind-local index (rb | nr+lin | nr+nl+ad)
@@ -138,6 +140,16 @@ struct Prepared {
         M.ad_shift = reinterpret_cast<const int32_t*>(base + o_ash);
         M.ad_uw = reinterpret_cast<const int32_t*>(base + o_auw);
         M.big_words = static_cast<int32_t>(big_words);
+        M.ntb = ntb;
+        M.tb_xy = reinterpret_cast<const int32_t*>(base + o_tbxy);
+        M.tb_off = reinterpret_cast<const int64_t*>(base + o_tboff);
+        M.tb_sup = reinterpret_cast<const uint32_t*>(base + o_tbsup);
+        M.ntn = ntn;
+        M.tn_start = reinterpret_cast<const int32_t*>(base + o_tns);
+        M.tn_var = reinterpret_cast<const int32_t*>(base + o_tnv);
+        M.tn_nt = reinterpret_cast<const int64_t*>(base + o_tnn);
+        M.tn_off = reinterpret_cast<const int64_t*>(base + o_tno);
+        M.tn_data = reinterpret_cast<const int16_t*>(base + o_tnd);
         M.total_members = total_members;
         return M;
     }
@@ -162,7 +174,10 @@ void prepare(const HostModel& m, const uint64_t* words, Prepared& P) {
     std::vector<int32_t> ls{0}, lo, lv, as{0}, av, ash;
     std::vector<int64_t> lb, lc;
     P.kind_index.assign(m.n_cons(), 0);
-    std::vector<int> ad_cons;
+    std::vector<int> ad_cons, tables2;
+    std::vector<int32_t> tn_start{0}, tn_var;
+    std::vector<int64_t> tn_nt, tn_off;
+    std::vector<int16_t> tn_data;
     for (int c = 0; c < m.n_cons(); ++c) {
         const int b = m.con_start[c], e = m.con_start[c + 1];
         switch (m.con_kind[c]) {
@@ -207,6 +222,27 @@ void prepare(const HostModel& m, const uint64_t* words, Prepared& P) {
             ls.push_back(static_cast<int32_t>(lv.size()));
             break;
         }
+        case CUBICS_TABLE: {
+            const int k = e - b;
+            const int64_t nt = m.con_value[c];
+            const int64_t* data = m.table_data.data() + m.table_start[c];
+            if (k == 2) { // support bitsets: row a of x's block = the y bits allowed with x = a
+                tables2.push_back(c);
+            } else {
+                if (k > 8) throw StatusError{CUBICS_E_UNSUPPORTED, "table constraint of arity > 8"};
+                tn_off.push_back(static_cast<int64_t>(tn_data.size()));
+                tn_nt.push_back(nt);
+                for (int64_t i = 0; i < nt; ++i)
+                    for (int j = 0; j < k; ++j) {
+                        const int v = m.term_var[b + j];
+                        const __int128 pos = (__int128)data[i * k + j] - m.offset[v];
+                        tn_data.push_back(pos >= 0 && pos < m.width[v] ? static_cast<int16_t>(pos) : int16_t(-1));
+                    }
+                for (int j = 0; j < k; ++j) tn_var.push_back(m.term_var[b + j]);
+                tn_start.push_back(static_cast<int32_t>(tn_var.size()));
+            }
+            break;
+        }
         default:
             ad_cons.push_back(c);
             break;
@@ -249,6 +285,28 @@ void prepare(const HostModel& m, const uint64_t* words, Prepared& P) {
     if (W > 32) throw StatusError{CUBICS_E_UNSUPPORTED, "domain wider than 1024 values"};
     P.W = W;
     P.NWP = dev::round4((size_t)std::max(n, 1) * W);
+    std::vector<int32_t> tb_xy;
+    std::vector<int64_t> tb_off;
+    std::vector<uint32_t> tb_sup;
+    for (int c : tables2) {
+        const int b = m.con_start[c], x = m.term_var[b], y = m.term_var[b + 1];
+        const int64_t nt = m.con_value[c];
+        const int64_t* data = m.table_data.data() + m.table_start[c];
+        const size_t ox = tb_sup.size(), oy = ox + (size_t)m.width[x] * W;
+        tb_sup.resize(oy + (size_t)m.width[y] * W, 0);
+        for (int64_t i = 0; i < nt; ++i) {
+            const __int128 a = (__int128)data[2 * i] - m.offset[x], bb = (__int128)data[2 * i + 1] - m.offset[y];
+            if (a < 0 || a >= m.width[x] || bb < 0 || bb >= m.width[y]) continue;
+            tb_sup[ox + (size_t)a * W + (size_t)(bb >> 5)] |= 1u << (int)(bb & 31);
+            tb_sup[oy + (size_t)bb * W + (size_t)(a >> 5)] |= 1u << (int)(a & 31);
+        }
+        tb_xy.push_back(x);
+        tb_xy.push_back(y);
+        tb_off.push_back(static_cast<int64_t>(ox));
+        tb_off.push_back(static_cast<int64_t>(oy));
+    }
+    P.ntb = static_cast<int>(tables2.size());
+    P.ntn = static_cast<int>(tn_nt.size());
     P.nr = static_cast<int>(rb.size());
     P.nl = static_cast<int>(lo.size());
     P.na = static_cast<int>(as.size()) - 1;
@@ -292,6 +350,14 @@ void prepare(const HostModel& m, const uint64_t* words, Prepared& P) {
     P.o_av = P.blob.add(av.data(), av.size());
     P.o_ash = P.blob.add(ash.data(), ash.size());
     P.o_auw = P.blob.add(auw.data(), auw.size());
+    P.o_tbxy = P.blob.add(tb_xy.data(), tb_xy.size());
+    P.o_tboff = P.blob.add(tb_off.data(), tb_off.size());
+    P.o_tbsup = P.blob.add(tb_sup.data(), tb_sup.size());
+    P.o_tns = P.blob.add(tn_start.data(), tn_start.size());
+    P.o_tnv = P.blob.add(tn_var.data(), tn_var.size());
+    P.o_tnn = P.blob.add(tn_nt.data(), tn_nt.size());
+    P.o_tno = P.blob.add(tn_off.data(), tn_off.size());
+    P.o_tnd = P.blob.add(tn_data.data(), tn_data.size());
     P.o_nes = P.blob.add(nes.data(), nes.size());
     P.o_nee = P.blob.add(nee.data(), nee.size());
 }
@@ -346,7 +412,7 @@ int current_device(int want) {
     }
 
 int parity_block(const Prepared& P) {
-    const int work = P.nr + P.nl;
+    const int work = P.nr + P.nl + P.ntb + P.ntn;
     int prop_warps = std::min(16, std::max(1, (work + 31) / 32));
     int ad_warps = std::min(P.na, 8);
     int apply_warps = std::min(16, std::max(1, (P.n + 63) / 64));
@@ -468,7 +534,9 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
     // launch geometry
     int block = cfg.block_threads > 0 ? ((cfg.block_threads + 31) / 32) * 32 : 0;
     if (!block) // parallel: one warp per context maximises resident contexts (32 per SM) for small models
-        block = parallel ? (P.nr + P.nl > 1024 || P.n > 1024 ? 128 : (P.W >= 8 || P.nr + P.nl > 256 ? 64 : 32))
+        block = parallel ? (P.nr + P.nl + P.ntb + P.ntn > 1024 || P.n > 1024
+                                ? 128
+                                : (P.W >= 8 || P.nr + P.nl + P.ntb + P.ntn > 256 ? 64 : 32))
                          : parity_block(P);
     block = std::min(std::max(block, 32), 1024);
     const int nw = block / 32;
@@ -1087,11 +1155,19 @@ int run_prop(const cubics_model* h, const uint64_t* words_in, uint64_t* words_ou
         sub.con_start.assign(1, 0);
         sub.term_var.clear();
         sub.term_coeff.clear();
+        sub.table_start.clear();
+        sub.table_data.clear();
         for (int c = 0; c < m.n_cons(); ++c) {
             if (!on[c]) continue;
             sub.con_kind.push_back(m.con_kind[c]);
             sub.con_op.push_back(m.con_op[c]);
             sub.con_value.push_back(m.con_value[c]);
+            sub.table_start.push_back(static_cast<int64_t>(sub.table_data.size()));
+            if (m.con_kind[c] == CUBICS_TABLE) {
+                const int64_t* src = m.table_data.data() + m.table_start[c];
+                sub.table_data.insert(sub.table_data.end(), src,
+                                      src + m.con_value[c] * (m.con_start[c + 1] - m.con_start[c]));
+            }
             for (int t = m.con_start[c]; t < m.con_start[c + 1]; ++t) {
                 sub.term_var.push_back(m.term_var[t]);
                 sub.term_coeff.push_back(m.term_coeff[t]);

@@ -44,13 +44,15 @@ cubics_model_desc HostModel::desc() const {
     d.term_coeff = term_coeff.data();
     d.goal = goal;
     d.goal_var = goal_var;
+    d.table_start = table_start.data();
+    d.table_data = table_data.data();
     return d;
 }
 
 namespace {
 
 // ---------------------------------------------------------------- lexer
-enum class T { Ident, Int, Semi, Comma, LParen, RParen, DotDot, Plus, Minus, Star, Lt, Le, Gt, Ge, Eq, Ne, End };
+enum class T { Ident, Int, Semi, Comma, LParen, RParen, DotDot, Plus, Minus, Star, Lt, Le, Gt, Ge, Eq, Ne, Colon, End };
 
 struct Tok {
     T kind = T::End;
@@ -145,6 +147,7 @@ struct Lexer {
         bool nxt_eq = pos + 1 < n && s[pos + 1] == '=';
         switch (c) {
         case ';': one(T::Semi); return;
+        case ':': one(T::Colon); return; // table constraints (extension)
         case ',': one(T::Comma); return;
         case '(': one(T::LParen); return;
         case ')': one(T::RParen); return;
@@ -246,10 +249,17 @@ struct Parser {
         return true;
     }
 
+    bool peek_lparen() const { // 'table' followed by '(' starts a table constraint
+        size_t p = lex.pos;
+        while (p < lex.n && (lex.s[p] == ' ' || lex.s[p] == '\t' || lex.s[p] == '\r' || lex.s[p] == '\n')) ++p;
+        return p < lex.n && lex.s[p] == '(';
+    }
+
     void push_con(int kind, int op, int64_t value) {
         m.con_kind.push_back(kind);
         m.con_op.push_back(op);
         m.con_value.push_back(value);
+        m.table_start.push_back(static_cast<int64_t>(m.table_data.size()));
     }
 
     void close_con() { m.con_start.push_back(static_cast<int32_t>(m.term_var.size())); }
@@ -384,10 +394,56 @@ struct Parser {
         close_con();
     }
 
+    // extension (not in the reference grammar): constraint table(x, y : 1 2, 2 3, 3 1);
+    // allowed tuples after ':', values separated by blanks, tuples by commas
+    void table() {
+        lex.take(); // table
+        if (!expect(T::LParen, "'('")) return;
+        std::vector<int> vars;
+        Tok t;
+        int v;
+        if (!expect(T::Ident, "variable name", &t) || !resolve(t, v)) return;
+        vars.push_back(v);
+        while (lex.cur.kind == T::Comma) {
+            lex.take();
+            if (!expect(T::Ident, "variable name", &t) || !resolve(t, v)) return;
+            vars.push_back(v);
+        }
+        if (!take_colon()) return;
+        const size_t k = vars.size();
+        std::vector<int64_t> data;
+        while (lex.cur.kind == T::Int) {
+            for (size_t i = 0; i < k; ++i) {
+                Tok val;
+                if (!expect(T::Int, "integer tuple value", &val)) return;
+                data.push_back(val.value);
+            }
+            if (lex.cur.kind != T::Comma) break;
+            lex.take();
+        }
+        if (!expect(T::RParen, "')'")) return;
+        push_con(CUBICS_TABLE, 0, static_cast<int64_t>(data.size() / k));
+        m.table_data.insert(m.table_data.end(), data.begin(), data.end());
+        for (int x : vars) term(x, 1);
+        close_con();
+    }
+
+    bool take_colon() {
+        if (failed()) return false;
+        if (lex.cur.kind == T::Colon) {
+            lex.take();
+            return !failed();
+        }
+        fail_syntax(lex.cur, "':'");
+        return false;
+    }
+
     void constraint() {
         lex.take(); // constraint
         const Tok first = lex.cur;
-        if (first.kind == T::Ident && first.text == "alldifferent") {
+        if (first.kind == T::Ident && first.text == "table" && peek_lparen()) {
+            table();
+        } else if (first.kind == T::Ident && first.text == "alldifferent") {
             alldiff();
         } else if (first.kind == T::Ident) {
             Tok ident = lex.take();
@@ -503,15 +559,21 @@ extern "C" int cubics_model_create(const cubics_model_desc* d, cubics_model** ou
         int cnt = d->con_start[c + 1] - d->con_start[c];
         bool ok = (k == CUBICS_RELBIN && (cnt == 1 || cnt == 2) && d->con_op[c] >= 0 && d->con_op[c] <= 5) ||
                   (k == CUBICS_LINEAR && cnt >= 0 && (d->con_op[c] == 0 || d->con_op[c] == 1)) ||
-                  (k == CUBICS_ALLDIFF && cnt >= 0);
+                  (k == CUBICS_ALLDIFF && cnt >= 0) ||
+                  (k == CUBICS_TABLE && cnt >= 1 && d->table_start && d->table_data && d->con_value[c] >= 0);
         if (!ok || d->con_start[c] > d->con_start[c + 1]) {
             delete h;
             cubics::set_error("cubics_model_create: malformed constraint " + std::to_string(c));
             return CUBICS_E_INVALID;
         }
         m.con_kind.push_back(k);
-        m.con_op.push_back(k == CUBICS_ALLDIFF ? 0 : d->con_op[c]);
+        m.con_op.push_back(k == CUBICS_ALLDIFF || k == CUBICS_TABLE ? 0 : d->con_op[c]);
         m.con_value.push_back(k == CUBICS_ALLDIFF ? 0 : d->con_value[c]);
+        m.table_start.push_back(static_cast<int64_t>(m.table_data.size()));
+        if (k == CUBICS_TABLE) {
+            const int64_t* src = d->table_data + d->table_start[c];
+            m.table_data.insert(m.table_data.end(), src, src + d->con_value[c] * cnt);
+        }
         m.con_start.push_back(d->con_start[c + 1] - d->con_start[0]);
     }
     for (int t = d->n_cons ? d->con_start[0] : 0; t < nt; ++t) {

@@ -22,6 +22,7 @@ struct HostModel {
     std::vector<uint64_t> words;
     std::vector<int32_t> con_kind, con_op, con_start{0}, term_var;
     std::vector<int64_t> con_value, term_coeff;
+    std::vector<int64_t> table_start, table_data; // TABLE: tuples of constraint c at table_start[c]
     int32_t goal = CUBICS_SATISFY;
     int32_t goal_var = 0;
 

@@ -272,6 +272,76 @@ __device__ __forceinline__ bool prop_linear(const DevModel& M, int c, const uint
     return true;
 }
 
+// ------------------------------------------------------------------ Table (extension, no reference counterpart)
+// Positive extensional constraint, generalised arc consistency. Binary tables use support bitsets
+// (bitwise AC): x keeps value a iff row a of x's support block meets D(y). N-ary tables scan
+// their tuples: a tuple is valid when every component is in its domain; valid tuples support
+// their values. Matches oracle/cubics_oracle.c prop_table.
+template <int W>
+__device__ __forceinline__ void prop_table2(const DevModel& M, int t, const uint32_t* dom, uint32_t* rm) {
+    const int x = M.tb_xy[2 * t], y = M.tb_xy[2 * t + 1];
+    const uint32_t* dx = dom + (size_t)x * W;
+    const uint32_t* dy = dom + (size_t)y * W;
+    if (dom_empty<W>(dx) || dom_empty<W>(dy)) return;
+    const uint32_t* sx = M.tb_sup + M.tb_off[2 * t];
+    const uint32_t* sy = M.tb_sup + M.tb_off[2 * t + 1];
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        uint32_t bits = dx[w], gone = 0;
+        while (bits) {
+            const int a = w * 32 + __ffs(bits) - 1;
+            bits &= bits - 1;
+            uint32_t any = 0;
+#pragma unroll
+            for (int i = 0; i < W; ++i) any |= sx[(size_t)a * W + i] & dy[i];
+            if (!any) gone |= 1u << (a & 31);
+        }
+        if (gone) atomicOr(rm + (size_t)x * W + w, gone);
+    }
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        uint32_t bits = dy[w], gone = 0;
+        while (bits) {
+            const int b = w * 32 + __ffs(bits) - 1;
+            bits &= bits - 1;
+            uint32_t any = 0;
+#pragma unroll
+            for (int i = 0; i < W; ++i) any |= sy[(size_t)b * W + i] & dx[i];
+            if (!any) gone |= 1u << (b & 31);
+        }
+        if (gone) atomicOr(rm + (size_t)y * W + w, gone);
+    }
+}
+
+template <int W>
+__device__ void prop_tablen(const DevModel& M, int t, const uint32_t* dom, uint32_t* rm) {
+    const int b = M.tn_start[t], k = M.tn_start[t + 1] - b;
+    for (int j = 0; j < k; ++j)
+        if (dom_empty<W>(dom + (size_t)M.tn_var[b + j] * W)) return;
+    uint32_t sup[8][W];
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int w = 0; w < W; ++w) sup[j][w] = 0;
+    const int16_t* tu = M.tn_data + M.tn_off[t];
+    for (int64_t i = 0; i < M.tn_nt[t]; ++i, tu += k) {
+        bool valid = true;
+        for (int j = 0; j < k && valid; ++j) {
+            const int bi = tu[j];
+            valid = bi >= 0 && ((dom[(size_t)M.tn_var[b + j] * W + (bi >> 5)] >> (bi & 31)) & 1u);
+        }
+        if (!valid) continue;
+        for (int j = 0; j < k; ++j) sup[j][tu[j] >> 5] |= 1u << (tu[j] & 31);
+    }
+    for (int j = 0; j < k; ++j) {
+        const int v = M.tn_var[b + j];
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            const uint32_t r = dom[(size_t)v * W + w] & ~sup[j][w];
+            if (r) atomicOr(rm + (size_t)v * W + w, r);
+        }
+    }
+}
+
 // ------------------------------------------------------------------ AllDifferent (warp per constraint)
 // Members are spread over the 32 lanes, two slots per lane (member l and l+32), so one warp
 // handles up to 64 members. Member domains are loaded into a common value universe (W words).
@@ -974,6 +1044,18 @@ __device__ __forceinline__ void run_propagators(const DevModel& M, const RoundCt
                 if (!hit) continue;
             }
             if (!prop_linear<W>(M, c, R.dom, R.rm)) *s_err = DERR_OVERFLOW;
+        }
+        for (int c = tid; c < M.ntb; c += prop_threads) {
+            if (trig && !trig_bit(trig, M.tb_xy[2 * c]) && !trig_bit(trig, M.tb_xy[2 * c + 1])) continue;
+            prop_table2<W>(M, c, R.dom, R.rm);
+        }
+        for (int c = tid; c < M.ntn; c += prop_threads) {
+            if (trig) {
+                bool hit = false;
+                for (int t = M.tn_start[c]; t < M.tn_start[c + 1] && !hit; ++t) hit = trig_bit(trig, M.tn_var[t]);
+                if (!hit) continue;
+            }
+            prop_tablen<W>(M, c, R.dom, R.rm);
         }
     }
     if (warp >= nw - ad_warps) {

@@ -239,6 +239,37 @@ PINNED_SHA256 = {
 }
 
 
+def random_binary_csp(n: int, d: int, m: int, tightness: float, seed: int, connect: bool = False) -> str:
+    """Random binary CSP, model B (BASELINE config 5; extension beyond the reference grammar):
+    n variables over 1..d, m distinct random pairs, each a positive table that allows
+    round((1 - tightness) * d^2) tuples drawn without replacement. The phase transition sits
+    near tightness* = 1 - d^(-n/m) (expected number of solutions = 1)."""
+    rnd = random.Random(seed)
+    lines = [f"var v{i} in 1..{d};" for i in range(n)]
+    allowed = max(1, round((1.0 - tightness) * d * d))
+    tuples = [(a, b) for a in range(1, d + 1) for b in range(1, d + 1)]
+    seen = set()
+    order = list(range(n))
+    if connect:
+        rnd.shuffle(order)
+    while len(seen) < m:
+        if connect and len(seen) < n - 1:  # a random spanning path first, so the graph is connected
+            a, b = order[len(seen)], order[len(seen) + 1]
+        else:
+            a, b = rnd.randrange(n), rnd.randrange(n)
+        if a == b or (min(a, b), max(a, b)) in seen:
+            continue
+        seen.add((min(a, b), max(a, b)))
+        tab = sorted(rnd.sample(tuples, allowed))
+        lines.append(f"constraint table(v{a}, v{b} : " + ", ".join(f"{x} {y}" for x, y in tab) + ");")
+    lines.append("solve satisfy;")
+    return "\n".join(lines) + "\n"
+
+
+def phase_transition_tightness(n: int, d: int, m: int) -> float:
+    return 1.0 - d ** (-n / m)
+
+
 def named_instance(name: str) -> str:
     """The model text of a named benchmark instance (nqN, golombM, magicN, rcsp_N)."""
     if name.startswith("nq"):
@@ -248,6 +279,11 @@ def named_instance(name: str) -> str:
         return golomb(m, m * m)
     if name.startswith("magic"):
         return magic(int(name[len("magic"):]))
+    if name.startswith("rbcsp_"):  # rbcsp_<n>: config-5 random binary CSP, d=10, m=2n, near the transition
+        n = int(name[len("rbcsp_"):])
+        m = 2 * n
+        t = phase_transition_tightness(n, 10, m) - 0.06
+        return random_binary_csp(n, 10, m, t, 5)
     if name.startswith("rcsp_"):
         n = int(name[len("rcsp_"):])
         ratio = 1.0 if n >= 100000 else 2.0

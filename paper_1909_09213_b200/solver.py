@@ -245,6 +245,14 @@ class Model:
         self.term_var = [d.term_var[i] for i in range(nt)]
         self.term_coeff = [d.term_coeff[i] for i in range(nt)] if nt else []
         self.names = [lib().cubics_model_var_name(self._h, i).decode() for i in range(self.n_vars)]
+        # positive tables (extension): tuples of constraint c, flattened
+        self.table_start = [d.table_start[i] for i in range(self.n_cons)] if self.n_cons else []
+        tot = 0
+        for c in range(self.n_cons):
+            if self.con_kind[c] == A.TABLE:
+                k = self.con_start[c + 1] - self.con_start[c]
+                tot = max(tot, self.table_start[c] + self.con_value[c] * k)
+        self.table_data = [d.table_data[i] for i in range(tot)]
 
     @property
     def handle(self):
@@ -265,7 +273,8 @@ class Model:
     def desc_arrays(self):
         """Flat arrays for building a cubics_model_desc (keeps them alive in the returned dict)."""
         return build_desc(self.offsets, self.widths, self.domains, self.con_kind, self.con_op, self.con_value,
-                          self.con_start, self.term_var, self.term_coeff, self.goal, self.goal_var)
+                          self.con_start, self.term_var, self.term_coeff, self.goal, self.goal_var,
+                          self.table_start, self.table_data)
 
     def words_of(self, domains):
         out = (C.c_uint64 * max(1, self.word_start[-1]))()
@@ -291,11 +300,13 @@ class Model:
 
     def with_domains(self, domains):
         arr = build_desc(self.offsets, self.widths, domains, self.con_kind, self.con_op, self.con_value,
-                         self.con_start, self.term_var, self.term_coeff, self.goal, self.goal_var)
+                         self.con_start, self.term_var, self.term_coeff, self.goal, self.goal_var,
+                         self.table_start, self.table_data)
         return model_from_desc(arr["desc"])
 
 
-def build_desc(offsets, widths, domains, kinds, ops, values, starts, tvars, tcoeffs, goal=A.SATISFY, goal_var=0):
+def build_desc(offsets, widths, domains, kinds, ops, values, starts, tvars, tcoeffs, goal=A.SATISFY, goal_var=0,
+               table_start=None, table_data=None):
     n, m = len(offsets), len(kinds)
     nt = starts[-1] if m else 0
     ws = [0]
@@ -311,6 +322,8 @@ def build_desc(offsets, widths, domains, kinds, ops, values, starts, tvars, tcoe
         "start": (C.c_int32 * (m + 1))(*(starts if m else [0])),
         "tvar": (C.c_int32 * max(1, nt))(*tvars),
         "tcoeff": (C.c_int64 * max(1, nt))(*(tcoeffs or [1] * nt)),
+        "tstart": (C.c_int64 * max(1, m))(*(table_start or [0] * m)),
+        "tdata": (C.c_int64 * max(1, len(table_data or [])))(*(table_data or [])),
     }
     for v, d in enumerate(domains):
         for i, x in enumerate(d.words()):
@@ -329,6 +342,8 @@ def build_desc(offsets, widths, domains, kinds, ops, values, starts, tvars, tcoe
     d.term_coeff = keep["tcoeff"]
     d.goal = goal
     d.goal_var = goal_var
+    d.table_start = keep["tstart"]
+    d.table_data = keep["tdata"]
     keep["desc"] = d
     return keep
 

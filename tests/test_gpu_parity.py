@@ -301,3 +301,67 @@ def test_parallel_first_solution_exact(key):
     stats, sol = gpu_case(key, PARALLEL)
     assert stats == G.expected_tuple(g)
     assert sol == g["first"]
+
+
+# ---- positive table constraints (extension; BASELINE config 5). Parity vs the oracle port and
+# brute force (the reference has no table constraint).
+def _brute_force(m, lo_hi):
+    tabs = []
+    for c in range(m.n_cons):
+        k = m.con_start[c + 1] - m.con_start[c]
+        vs = m.term_var[m.con_start[c]:m.con_start[c + 1]]
+        tu = {tuple(m.table_data[m.table_start[c] + i * k:m.table_start[c] + (i + 1) * k]) for i in range(m.con_value[c])}
+        tabs.append((vs, tu))
+    return [list(a) for a in itertools.product(*[range(lo, hi + 1) for lo, hi in lo_hi])
+            if all(tuple(a[v] for v in vs) in tu for vs, tu in tabs)]
+
+
+def test_table_removals_binary_and_nary():
+    rng = models.Rng(777)
+    for trial in range(60):
+        n, d = 4, 3 + rng.below(5)
+        lines = [f"var v{i} in {i}..{i + d - 1};" for i in range(n)]
+        for arity in (2, 3):
+            scope = [rng.below(n) for _ in range(arity)]
+            tuples = set()
+            for _ in range(rng.below(d * d) + 1):
+                tuples.add(tuple(scope[j] + rng.below(d + 1) - (1 if rng.below(5) == 0 else 0) for j in range(arity)))
+            body = ", ".join(" ".join(str(x) for x in t) for t in sorted(tuples))
+            lines.append(f"constraint table({', '.join(f'v{s}' for s in scope)} : {body});")
+        lines.append("solve satisfy;")
+        m = S.parse_model("\n".join(lines))
+        doms = [d_.copy() for d_ in m.domains]
+        for v in range(n):
+            for x in doms[v].values():
+                if doms[v].size() > 1 and rng.below(3) == 0:
+                    doms[v].remove(x)
+        for c in range(m.n_cons):
+            assert S.removals(m, doms, cons=[c]) == O.removals(m, doms, cons=[c]), (trial, c)
+        gd, gf = S.propagate_fixpoint(m, doms)
+        od, of = O.propagate_fixpoint(m, doms)
+        assert gd == od and gf == of, trial
+
+
+def test_table_all_solutions_vs_brute_force():
+    for seed in range(30):
+        n, d = 5 + seed % 2, 3 + seed % 2
+        text = models.random_binary_csp(n, d, 6 + seed % 4, 0.45, seed)
+        m = S.parse_model(text)
+        bf = _brute_force(m, [(1, d)] * n)
+        exp = [s.values for s in O.enumerate_solutions(m)]
+        assert sorted(exp) == sorted(bf), seed
+        for eng in (PARITY, PARALLEL):
+            st, ost = S.SearchStats(), S.SearchStats()
+            got = [s.values for s in S.enumerate_solutions(m, S.SearchConfig(engine=eng), st)]
+            O.enumerate_solutions(m, S.SearchConfig(), ost)
+            assert got == exp and st.as_tuple() == ost.as_tuple(), (seed, eng)
+
+
+def test_table_random_csp_search_matches_oracle():
+    n = 200
+    t = models.phase_transition_tightness(n, 10, 2 * n) - 0.06
+    m = S.parse_model(models.random_binary_csp(n, 10, 2 * n, t, 5))
+    for cfg in (S.SearchConfig(max_solutions=1, node_limit=1500, engine=PARITY),
+                S.SearchConfig(max_solutions=1, node_limit=1500, var_heuristic=0, engine=PARITY)):
+        r, ro = S.solve_satisfy(m, cfg), O.solve_satisfy(m, cfg)
+        assert r.stats.as_tuple() == ro.stats.as_tuple()
