@@ -225,34 +225,40 @@ class Model:
         self.n_cons = d.n_cons
         self.goal = d.goal
         self.goal_var = d.goal_var
-        self.offsets = [d.var_offset[i] for i in range(self.n_vars)]
-        self.widths = [d.var_width[i] for i in range(self.n_vars)]
+        n, mc = self.n_vars, self.n_cons
+        self.offsets = d.var_offset[:n] if n else []
+        self.widths = d.var_width[:n] if n else []
         self.word_start = [0]
         for w in self.widths:
             self.word_start.append(self.word_start[-1] + (w + 63) // 64)
-        words = [d.var_words[i] for i in range(self.word_start[-1])]
+        words = d.var_words[:self.word_start[-1]] if self.word_start[-1] else []
         self.domains = []
-        for v in range(self.n_vars):
-            bits = 0
-            for i, x in enumerate(words[self.word_start[v]:self.word_start[v + 1]]):
-                bits |= x << (64 * i)
+        for v in range(n):
+            a, b = self.word_start[v], self.word_start[v + 1]
+            bits = words[a] if b - a == 1 else sum(x << (64 * i) for i, x in enumerate(words[a:b]))
             self.domains.append(Domain(self.offsets[v], bits=bits, width=self.widths[v]))
-        self.con_kind = [d.con_kind[i] for i in range(self.n_cons)]
-        self.con_op = [d.con_op[i] for i in range(self.n_cons)]
-        self.con_value = [d.con_value[i] for i in range(self.n_cons)]
-        self.con_start = [d.con_start[i] for i in range(self.n_cons + 1)]
-        nt = self.con_start[-1] if self.n_cons else 0
-        self.term_var = [d.term_var[i] for i in range(nt)]
-        self.term_coeff = [d.term_coeff[i] for i in range(nt)] if nt else []
-        self.names = [lib().cubics_model_var_name(self._h, i).decode() for i in range(self.n_vars)]
+        self.con_kind = d.con_kind[:mc] if mc else []
+        self.con_op = d.con_op[:mc] if mc else []
+        self.con_value = d.con_value[:mc] if mc else []
+        self.con_start = d.con_start[:mc + 1] if mc else [0]
+        nt = self.con_start[-1] if mc else 0
+        self.term_var = d.term_var[:nt] if nt else []
+        self.term_coeff = d.term_coeff[:nt] if nt else []
         # positive tables (extension): tuples of constraint c, flattened
-        self.table_start = [d.table_start[i] for i in range(self.n_cons)] if self.n_cons else []
+        self.table_start = d.table_start[:mc] if mc else []
         tot = 0
-        for c in range(self.n_cons):
+        for c in range(mc):
             if self.con_kind[c] == A.TABLE:
                 k = self.con_start[c + 1] - self.con_start[c]
                 tot = max(tot, self.table_start[c] + self.con_value[c] * k)
-        self.table_data = [d.table_data[i] for i in range(tot)]
+        self.table_data = d.table_data[:tot] if tot else []
+        self._names = None
+
+    @property
+    def names(self):
+        if self._names is None:
+            self._names = [lib().cubics_model_var_name(self._h, i).decode() for i in range(self.n_vars)]
+        return self._names
 
     @property
     def handle(self):
