@@ -166,13 +166,24 @@ def run_extras(S, A, device):
         ("magic5_first", "magic5|--max 1", A.ENGINE_PARITY, {"max_solutions": 1}, "first solution, parity engine"),
         ("magic4_all", "magic4|--all", A.ENGINE_PARALLEL, {}, "all solutions, parallel engine"),
         ("rcsp_1000_first", "rcsp_1000|--max 1", A.ENGINE_PARITY, {"max_solutions": 1}, "first solution, parity engine"),
-        ("rcsp_100000_limit200", "rcsp_100000|--max 1 --node-limit 200", A.ENGINE_PARITY,
-         {"max_solutions": 1, "node_limit": 200}, "node-limited parity"),
+        ("rcsp_100000_limit200", "rcsp_100000|--max 1 --node-limit 200", A.ENGINE_AUTO,
+         {"max_solutions": 1, "node_limit": 200}, "node-limited, reference node order (grid-wide context)"),
+        # BASELINE config 5 as stated: random binary CSP with extensional tables near the phase
+        # transition (d=10, m=2n, tightness = transition - 0.06). No reference counterpart: stats
+        # are checked against the oracle port in tests/test_gpu_parity.py.
+        ("config5_rbcsp_1000_limit2000", "rbcsp_1000", A.ENGINE_AUTO, {"max_solutions": 1, "node_limit": 2000},
+         "tables, 1k vars / 2k tables, node-limited"),
+        ("config5_rbcsp_10000_limit200", "rbcsp_10000", A.ENGINE_AUTO, {"max_solutions": 1, "node_limit": 200},
+         "tables, 10k vars / 20k tables, node-limited (grid-wide context)"),
+        ("config5_rbcsp_100000_limit200", "rbcsp_100000", A.ENGINE_AUTO, {"max_solutions": 1, "node_limit": 200},
+         "tables, 100k vars / 200k tables, node-limited (grid-wide context)"),
     ]
     for name, key, engine, kw, what in cases:
         inst = key.split("|")[0]
         g = gold.get(key)
-        m = S.parse_model(open(os.path.join(MODELS, inst + ".fd")).read())
+        path = os.path.join(MODELS, inst + ".fd")
+        from paper_1909_09213_b200 import models as MD
+        m = S.parse_model(open(path).read() if os.path.exists(path) else MD.named_instance(inst))
         cfg = S.SearchConfig(engine=engine, device=device, count_only=True, **kw)
         try:
             if m.goal != 0:
@@ -183,7 +194,8 @@ def run_extras(S, A, device):
                 extra = {}
             st = r.stats.as_tuple()
             exp = (g["nodes"], g["failures"], g["rounds"], g["solutions"]) if g else None
-            rec = {"what": what, "device_ms": round(r.device_ms, 3), "nodes": st[0],
+            rec = {"what": what, "device_ms": round(r.device_ms, 3), "nodes": st[0], "stats": list(st),
+                   "engine": {1: "parity", 2: "parallel", 3: "grid"}.get(r.engine, r.engine),
                    "nodes_per_s": st[0] / (r.device_ms / 1e3) if r.device_ms else None,
                    "stats_equal_reference": (st == exp) if exp else None,
                    "reference_cpu_ms": g.get("time_ms") if g else None, **extra}

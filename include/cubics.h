@@ -123,9 +123,13 @@ enum cubics_engine {
     CUBICS_ENGINE_AUTO = 0,     /* PARALLEL for complete enumerations, else PARITY              */
     CUBICS_ENGINE_PARITY = 1,   /* one device search context, reference node order: every stat
                                    identical to the CPU reference                              */
-    CUBICS_ENGINE_PARALLEL = 2  /* many search contexts per GPU with work sharing: solutions and
-                                   all stats exact for complete enumerations; optimum exact for
-                                   branch-and-bound (node counts then schedule-dependent)       */
+    CUBICS_ENGINE_PARALLEL = 2, /* many search contexts per GPU with work sharing: solutions and
+                                   all stats exact for complete enumerations and for the first
+                                   solution; optimum exact for branch-and-bound (node counts
+                                   then schedule-dependent)                                     */
+    CUBICS_ENGINE_GRID = 3      /* PARITY semantics with one search context spanning the whole GPU
+                                   (cooperative launch): for models of 10k-100k+ variables.
+                                   AUTO picks it for large parity searches                      */
 };
 
 typedef struct cubics_search_config { /* fd::SearchConfig (include/fd/search.hpp:19-27) + engine */

@@ -22,7 +22,7 @@ LIN_LE, LIN_EQ = 0, 1
 SATISFY, MINIMIZE, MAXIMIZE = 0, 1, 2
 INPUT_ORDER, FIRST_FAIL = 0, 1
 FORWARD_CHECKING, ARC_CONSISTENT = 0, 1
-ENGINE_AUTO, ENGINE_PARITY, ENGINE_PARALLEL = 0, 1, 2
+ENGINE_AUTO, ENGINE_PARITY, ENGINE_PARALLEL, ENGINE_GRID = 0, 1, 2, 3
 UINT64_MAX = (1 << 64) - 1
 
 

@@ -16,6 +16,11 @@
 
 namespace cubics {
 
+namespace dev {
+struct Ctl;
+}
+using dev_ctl_t = dev::Ctl;
+
 struct alignas(16) RelBinRec {
     int32_t x;
     int32_t y;   // -1 for the literal form
@@ -150,6 +155,11 @@ struct SearchParams {
     // id = ring ticket + 1; the root is segment 0) records its root path key and its own stats;
     // solutions record their segment and segment-local stats; subtrees right of the best
     // solution key found so far are abandoned. The host then sums exactly the reference's prefix.
+    // grid-wide context (search_kernel_grid): control scalars, vote/min slots, trigger bitmaps
+    dev_ctl_t* grid_ctl;
+    unsigned* grid_or;     // [3]
+    unsigned* grid_min;    // [3]
+    uint32_t* grid_chg;    // [2 * ceil(n/32)]
     int32_t first_mode;
     int64_t seg_cap;
     uint32_t* seg_key;     // [seg_cap][KW]

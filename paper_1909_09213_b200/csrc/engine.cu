@@ -518,6 +518,13 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
     Prepared P;
     prepare(hm, hm.words.data(), P);
     const int n = P.n;
+    // AUTO: a large model searched with reference node order gets the grid-wide context
+    // (measured on B200: tables weigh ~4 RelBins; rbcsp_10000 / rcsp_100000 gain 1.7x / 6.8x,
+    // rcsp_10000 with 20k cheap != constraints is faster in one block)
+    if (engine == CUBICS_ENGINE_PARITY && cfg.engine == CUBICS_ENGINE_AUTO && !shard &&
+        ((long)P.nr + P.nl + 4L * (P.ntb + P.ntn) >= 40000 || P.n >= 50000))
+        engine = CUBICS_ENGINE_GRID;
+    const bool grid = engine == CUBICS_ENGINE_GRID;
     const bool parallel = engine == CUBICS_ENGINE_PARALLEL;
     const bool keyed = parallel || (shard && shard->split_depth > 0);
     // exact parallel first solution: complete otherwise-equal search, max_solutions == 1
@@ -533,6 +540,7 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
     out.KW = KW;
     // launch geometry
     int block = cfg.block_threads > 0 ? ((cfg.block_threads + 31) / 32) * 32 : 0;
+    if (!block && grid) block = 512;
     if (!block) // parallel: one warp per context maximises resident contexts (32 per SM) for small models
         block = parallel ? (P.nr + P.nl + P.ntb + P.ntn > 1024 || P.n > 1024
                                 ? 128
@@ -540,8 +548,8 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
                          : parity_block(P);
     block = std::min(std::max(block, 32), 1024);
     const int nw = block / 32;
-    bool in_smem = true;
-    dev::SmemLayout L = dev::smem_layout(P.W, n, P.total_members, nw, KW, true, P.na);
+    bool in_smem = !grid; // the grid context keeps its domains in L2/HBM
+    dev::SmemLayout L = dev::smem_layout(P.W, n, P.total_members, nw, KW, in_smem, P.na);
     if (L.total > kSmemBudget) {
         in_smem = false;
         L = dev::smem_layout(P.W, n, P.total_members, nw, KW, false, P.na);
@@ -557,6 +565,17 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
         CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         const int cap = std::max(1, per_sm) * sms;
         n_ctx = cfg.contexts > 0 ? std::min(cfg.contexts, cap) : cap;
+    }
+    int grid_blocks = 0;
+    if (grid) { // co-resident blocks for the cooperative launch
+        int per_sm = 0;
+#define OCCG(w) occupancy_search_grid<w>(block, L.total, &per_sm)
+        CUBICS_DISPATCH_W(P.W, OCCG)
+#undef OCCG
+        int sms = 0;
+        CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        if (per_sm < 1) throw StatusError{CUBICS_E_UNSUPPORTED, "grid context does not fit on an SM"};
+        grid_blocks = std::min(per_sm, 2) * sms;
     }
     out.contexts = n_ctx;
     out.engine = engine;
@@ -582,7 +601,10 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
     const size_t a_busy = take(sizeof(int32_t) * (n_ctx + n_seed));
     const size_t a_hf = take(sizeof(int32_t) * n_ctx);
     const size_t zero_end = off;
-    const size_t a_big = take(sizeof(uint32_t) * P.big_words * (size_t)nw * n_ctx);
+    const size_t a_big = take(sizeof(uint32_t) * P.big_words * (size_t)nw * (grid ? grid_blocks : n_ctx));
+    const size_t a_gctl = take(grid ? 256 : 0);
+    const size_t a_gslots = take(grid ? 6 * sizeof(unsigned) : 0);
+    const size_t a_gchg = take(grid ? sizeof(uint32_t) * 2 * (((size_t)n + 31) / 32) : 0);
     const size_t a_frames = take(sizeof(uint32_t) * NWP * frame_cap * n_ctx);
     const size_t a_meta = take(sizeof(int32_t) * 4 * frame_cap * n_ctx);
     const size_t a_gdom = take(in_smem ? 0 : sizeof(uint32_t) * 2 * NWP * n_ctx);
@@ -653,6 +675,15 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
         S.record = record ? 1 : 0;
         S.dom_in_smem = in_smem ? 1 : 0;
         S.big_scratch = P.big_words ? reinterpret_cast<uint32_t*>(base + a_big) : nullptr;
+        if (grid) {
+            const unsigned init[6] = {0, 0, 0, 0xffffffffu, 0xffffffffu, 0xffffffffu};
+            CU(cudaMemcpyAsync(base + a_gslots, init, sizeof init, cudaMemcpyHostToDevice, st));
+            CU(cudaMemsetAsync(base + a_gctl, 0, 256, st));
+            S.grid_ctl = reinterpret_cast<dev_ctl_t*>(base + a_gctl);
+            S.grid_or = reinterpret_cast<unsigned*>(base + a_gslots);
+            S.grid_min = S.grid_or + 3;
+            S.grid_chg = reinterpret_cast<uint32_t*>(base + a_gchg);
+        }
         S.frames = reinterpret_cast<uint32_t*>(base + a_frames);
         S.frame_meta = reinterpret_cast<int32_t*>(base + a_meta);
         S.gdom = reinterpret_cast<uint32_t*>(base + a_gdom);
@@ -682,9 +713,15 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
         S.sol_seg = reinterpret_cast<int32_t*>(base + a_sseg);
 
         CU(cudaEventRecord(e0, st));
+        if (grid) {
+#define LG(w) launch_search_grid<w>(S, grid_blocks, block, L.total, st)
+            CUBICS_DISPATCH_W(P.W, LG)
+#undef LG
+        } else {
 #define LS(w) launch_search<w>(S, n_ctx, block, L.total, st)
-        CUBICS_DISPATCH_W(P.W, LS)
+            CUBICS_DISPATCH_W(P.W, LS)
 #undef LS
+        }
         CU(cudaEventRecord(e1, st));
         out.launches += 1;
         CU(cudaMemcpyAsync(&out.ws, base + a_ws, sizeof(WorkState), cudaMemcpyDeviceToHost, st));
@@ -823,6 +860,7 @@ void fill_result(const RunOut& r, cubics_result* out) {
 }
 
 int pick_engine(const cubics_search_config& cfg, bool optimize_goal) {
+    if (cfg.engine == CUBICS_ENGINE_GRID) return CUBICS_ENGINE_GRID;
     if (cfg.engine == CUBICS_ENGINE_PARITY || cfg.engine == CUBICS_ENGINE_PARALLEL) {
         if (cfg.engine == CUBICS_ENGINE_PARALLEL &&
             (cfg.node_limit != 0 ||

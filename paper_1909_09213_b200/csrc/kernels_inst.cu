@@ -17,14 +17,14 @@ cudaError_t grant_smem(K k, size_t smem, size_t& granted) {
     if (e == cudaSuccess) granted = smem;
     return e;
 }
-size_t g_search_smem = 48 * 1024, g_prop_smem = 48 * 1024;
+size_t g_search_smem = 48 * 1024, g_prop_smem = 48 * 1024, g_grid_smem = 48 * 1024;
 } // namespace
 
 template <>
 cudaError_t launch_search<CUBICS_W>(const SearchParams& P, int grid, int block, size_t smem, cudaStream_t st) {
     // the generic block kernel also runs one-warp contexts: a __syncwarp-specialised variant
-    // (search_kernel<W, true>) measured slower on B200 (19.3 vs 14.0 ms on nq14; register spills)
-    auto k = dev::search_kernel<CUBICS_W, false>;
+    // measured slower on B200 (19.3 vs 14.0 ms on nq14; register spills at the 64-register cap)
+    auto k = dev::search_kernel<CUBICS_W>;
     cudaError_t e = grant_smem(k, smem, g_search_smem);
     if (e != cudaSuccess) return e;
     k<<<grid, block, smem, st>>>(P);
@@ -33,8 +33,26 @@ cudaError_t launch_search<CUBICS_W>(const SearchParams& P, int grid, int block, 
 
 template <>
 cudaError_t occupancy_search<CUBICS_W>(int block, size_t smem, int* out) {
-    auto k = dev::search_kernel<CUBICS_W, false>;
+    auto k = dev::search_kernel<CUBICS_W>;
     cudaError_t e = grant_smem(k, smem, g_search_smem);
+    if (e != cudaSuccess) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, k, block, smem);
+}
+
+template <>
+cudaError_t launch_search_grid<CUBICS_W>(const SearchParams& P, int grid, int block, size_t smem, cudaStream_t st) {
+    auto k = dev::search_kernel_grid<CUBICS_W>;
+    cudaError_t e = grant_smem(k, smem, g_grid_smem);
+    if (e != cudaSuccess) return e;
+    SearchParams p = P;
+    void* args[] = {&p};
+    return cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(block), args, smem, st);
+}
+
+template <>
+cudaError_t occupancy_search_grid<CUBICS_W>(int block, size_t smem, int* out) {
+    auto k = dev::search_kernel_grid<CUBICS_W>;
+    cudaError_t e = grant_smem(k, smem, g_grid_smem);
     if (e != cudaSuccess) return e;
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, k, block, smem);
 }

@@ -17,6 +17,7 @@
 
 #include "device_model.hpp"
 #include "layout.hpp"
+#include "scope.cuh"
 
 namespace cubics {
 namespace dev {
@@ -25,21 +26,6 @@ constexpr unsigned FULL = 0xffffffffu;
 typedef __int128 i128;
 
 enum RoundStatus : int { R_CHANGED = 0, R_STABLE = 1, R_FAILED = 2, R_ERROR = 3 };
-
-// Block-level primitives specialised for one-warp search contexts (ONE: blockDim.x == 32, the
-// throughput configuration): barriers become __syncwarp and block votes become warp votes.
-template <bool ONE>
-__device__ __forceinline__ int nthreads() { return ONE ? 32 : (int)blockDim.x; }
-template <bool ONE>
-__device__ __forceinline__ void bar() {
-    if constexpr (ONE) __syncwarp();
-    else __syncthreads();
-}
-template <bool ONE>
-__device__ __forceinline__ int bar_or(int x) {
-    if constexpr (ONE) return __any_sync(FULL, x);
-    else return __syncthreads_or(x);
-}
 
 // ------------------------------------------------------------------ bitset helpers
 template <int W>
@@ -991,10 +977,10 @@ __device__ __forceinline__ bool trig_bit(const uint32_t* t, int v) { return (t[v
 // untriggered propagator sees exactly the domains of its last evaluation, whose removals are
 // already applied, so skipping it changes no domain, no "changed" flag and no round count.
 // *s_err receives DERR_OVERFLOW.
-template <int W, bool ONE = false>
-__device__ __forceinline__ void run_propagators(const DevModel& M, const RoundCtx& R, int* s_err,
-                                                const uint32_t* trig) {
-    const int tid = threadIdx.x, T = nthreads<ONE>(), nw = T >> 5, warp = ONE ? 0 : tid >> 5, lane = tid & 31;
+template <int W, class SC>
+__device__ __forceinline__ void run_propagators(const DevModel& M, const RoundCtx& R, volatile int* s_err,
+                                                const uint32_t* trig, SC& sc) {
+    const int tid = sc.tid(), T = sc.nthreads(), nw = sc.nwarps(), warp = sc.warp(), lane = threadIdx.x & 31;
     const int ad_warps = M.na < nw ? M.na : nw;
     const int prop_threads = nw > ad_warps ? (nw - ad_warps) * 32 : T;
     if (tid < prop_threads) {
@@ -1059,7 +1045,7 @@ __device__ __forceinline__ void run_propagators(const DevModel& M, const RoundCt
         }
     }
     if (warp >= nw - ad_warps) {
-        const WarpScratch ws = warp_scratch<W>(R, warp);
+        const WarpScratch ws = warp_scratch<W>(R, threadIdx.x >> 5); // shared memory of this block
         for (int a = warp - (nw - ad_warps); a < M.na; a += ad_warps) {
             if (R.enabled && !R.enabled[M.nr + M.nl + a]) continue;
             if (trig) {
@@ -1069,7 +1055,7 @@ __device__ __forceinline__ void run_propagators(const DevModel& M, const RoundCt
                 if (!__any_sync(FULL, hit)) continue;
             }
             if (M.ad_uw[a] > 0) { // generic path: many members or a wide value universe
-                uint32_t* scratch = R.big + (size_t)warp * M.big_words;
+                uint32_t* scratch = R.big + (size_t)(SC::kGrid ? warp : (int)(threadIdx.x >> 5)) * M.big_words;
                 if (R.alldiff) prop_alldiff_gac_big<W>(M, a, R.dom, R.rm, R.mates + M.ad_start[a], scratch, lane, R.exact_wipe);
                 else prop_alldiff_fc_big<W>(M, a, R.dom, R.rm, scratch, lane);
             } else if (R.alldiff) {
@@ -1088,10 +1074,10 @@ __device__ __forceinline__ void run_propagators(const DevModel& M, const RoundCt
 
 // Phase B: dom &= ~rm. Returns R_CHANGED / R_STABLE / R_FAILED / R_ERROR.
 // failed_var (when non-null) receives the lowest empty var id on failure.
-template <int W, bool ONE = false>
-__device__ __forceinline__ int apply_removals(const DevModel& M, const RoundCtx& R, int* s_err, int* s_min,
-                                              int* failed_var, uint32_t* chg_out) {
-    const int tid = threadIdx.x, T = nthreads<ONE>();
+template <int W, class SC>
+__device__ __forceinline__ int apply_removals(const DevModel& M, const RoundCtx& R, volatile int* s_err,
+                                              volatile int* s_min, int* failed_var, uint32_t* chg_out, SC& sc) {
+    const int tid = sc.tid(), T = sc.nthreads();
     int changed = 0, empty_min = 0x7fffffff;
     for (int v = tid; v < M.n; v += T) {
         uint32_t* d = R.dom + (size_t)v * W;
@@ -1117,19 +1103,19 @@ __device__ __forceinline__ int apply_removals(const DevModel& M, const RoundCtx&
         }
         if (!any && v < empty_min) empty_min = v;
     }
-    const int ch = bar_or<ONE>(changed);
+    const int ch = sc.sync_or(changed);
     const int err = *s_err;
     if (err) return R_ERROR;
     if (!ch) return R_STABLE;
-    const int em = bar_or<ONE>(empty_min != 0x7fffffff);
+    const int em = sc.sync_or(empty_min != 0x7fffffff);
     if (!em) return R_CHANGED;
     if (failed_var) {
         if (tid == 0) *s_min = 0x7fffffff;
-        bar<ONE>();
-        if (empty_min != 0x7fffffff) atomicMin(s_min, empty_min);
-        bar<ONE>();
+        sc.sync();
+        if (empty_min != 0x7fffffff) atomicMin(const_cast<int*>(s_min), empty_min);
+        sc.sync();
         *failed_var = *s_min;
-        bar<ONE>();
+        sc.sync();
     }
     return R_FAILED;
 }
@@ -1137,10 +1123,10 @@ __device__ __forceinline__ int apply_removals(const DevModel& M, const RoundCtx&
 // propagate_fixpoint (propagation.cpp:516-532); *rounds counts every round including the last.
 // first_all: evaluate every propagator in round 1; otherwise round 1 is triggered by the vars
 // set in R.chg0 (the caller's branch decision). Both trigger buffers are left dirty.
-template <int W, bool ONE = false>
-__device__ int block_fixpoint(const DevModel& M, const RoundCtx& R, int* s_err, int* s_min, int max_rounds,
-                              int* rounds, int* failed_var, bool first_all) {
-    const int tid = threadIdx.x, T = nthreads<ONE>();
+template <int W, class SC>
+__device__ int block_fixpoint(const DevModel& M, const RoundCtx& R, volatile int* s_err, volatile int* s_min,
+                              int max_rounds, int* rounds, int* failed_var, bool first_all, SC& sc) {
+    const int tid = sc.tid(), T = sc.nthreads();
     const int nb = (M.n + 31) >> 5;
     uint32_t* cur = R.chg0;
     uint32_t* nxt = R.chg1;
@@ -1149,9 +1135,9 @@ __device__ int block_fixpoint(const DevModel& M, const RoundCtx& R, int* s_err, 
     for (;;) {
         if (nxt)
             for (int i = tid; i < nb; i += T) nxt[i] = 0;
-        run_propagators<W, ONE>(M, R, s_err, all ? nullptr : cur);
-        bar<ONE>();
-        const int st = apply_removals<W, ONE>(M, R, s_err, s_min, failed_var, nxt);
+        run_propagators<W>(M, R, s_err, all ? nullptr : cur, sc);
+        sc.sync();
+        const int st = apply_removals<W>(M, R, s_err, s_min, failed_var, nxt, sc);
         ++r;
         if (st != R_CHANGED || (max_rounds > 0 && r >= max_rounds)) {
             *rounds = r;

@@ -17,6 +17,7 @@
 
 #include "layout.hpp"
 #include "propagators.cuh"
+#include "scope.cuh"
 
 namespace cubics {
 namespace dev {
@@ -61,18 +62,16 @@ __device__ __forceinline__ void spin_unlock(int32_t* l) {
 }
 
 // block-wide copy of nwords/4 uint4 words
-template <bool ONE = false>
-__device__ __forceinline__ void copy4(uint32_t* dst, const uint32_t* src, size_t nwords) {
+__device__ __forceinline__ void copy4(uint32_t* dst, const uint32_t* src, size_t nwords, int tid, int T) {
     uint4* d = reinterpret_cast<uint4*>(dst);
     const uint4* s = reinterpret_cast<const uint4*>(src);
-    for (size_t i = threadIdx.x; i < nwords / 4; i += nthreads<ONE>()) d[i] = s[i];
+    for (size_t i = tid; i < nwords / 4; i += T) d[i] = s[i];
 }
 
-template <bool ONE = false>
-__device__ __forceinline__ void copy4_cg(uint32_t* dst, const uint32_t* src, size_t nwords) {
+__device__ __forceinline__ void copy4_cg(uint32_t* dst, const uint32_t* src, size_t nwords, int tid, int T) {
     uint4* d = reinterpret_cast<uint4*>(dst);
     const uint4* s = reinterpret_cast<const uint4*>(src);
-    for (size_t i = threadIdx.x; i < nwords / 4; i += nthreads<ONE>()) d[i] = __ldcg(s + i);
+    for (size_t i = tid; i < nwords / 4; i += T) d[i] = __ldcg(s + i);
 }
 
 // DFS path key: decision at depth d is bit (31 - d%32) of word d/32, so comparing the words as
@@ -88,9 +87,9 @@ __device__ __forceinline__ uint32_t path_right_word(uint32_t word, int i, int d)
 }
 
 // block argmin of (size, id) over unbound vars; -1 when every domain is a singleton
-template <int W, bool ONE = false>
-__device__ __forceinline__ int select_var(const DevModel& M, const uint32_t* dom, int first_fail, unsigned* s_red) {
-    const int tid = threadIdx.x, T = nthreads<ONE>(), lane = tid & 31, warp = tid >> 5, nw = T >> 5;
+template <int W, class SC>
+__device__ __forceinline__ int select_var(const DevModel& M, const uint32_t* dom, int first_fail, unsigned* red, SC& sc) {
+    const int tid = sc.tid(), T = sc.nthreads();
     unsigned best = 0xffffffffu;
     for (int v = tid; v < M.n; v += T) {
         const int sz = dom_size<W>(dom + (size_t)v * W);
@@ -99,31 +98,26 @@ __device__ __forceinline__ int select_var(const DevModel& M, const uint32_t* dom
             best = key < best ? key : best;
         }
     }
-    best = __reduce_min_sync(FULL, best);
-    if (!ONE && nw > 1) {
-        if (lane == 0) s_red[warp] = best;
-        __syncthreads();
-        unsigned x = lane < nw ? s_red[lane] : 0xffffffffu;
-        best = __reduce_min_sync(FULL, x);
-        __syncthreads();
-    }
+    best = sc.min_u32(best, red);
     return best == 0xffffffffu ? -1 : (int)(best & 0x1fffffu);
 }
 
-template <int W, bool ONE>
-__global__ void __launch_bounds__(ONE ? 32 : 1024, ONE ? 32 : 1) search_kernel(const SearchParams P) {
-    extern __shared__ __align__(16) uint8_t smem[];
-    __shared__ int s_err, s_min, s_flag, s_src;
-    __shared__ unsigned s_red[32];
-    __shared__ long long s_ll;
+template <int W, class SC>
+__device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& C, unsigned* red, uint8_t* smem) {
+    int& s_err = C.err;
+    int& s_min = C.min;
+    int& s_flag = C.flag;
+    int& s_src = C.src;
+    long long& s_ll = C.ll;
 
     const DevModel& M = P.M;
-    const int ctx = blockIdx.x, tid = threadIdx.x, T = nthreads<ONE>(), nw = T >> 5;
+    const int ctx = SC::kGrid ? 0 : (int)blockIdx.x, tid = sc.tid(), T = sc.nthreads(), nw = sc.nwarps();
     const bool parallel = P.mode == MODE_PARALLEL;
     const int n = M.n;
     const size_t NW = (size_t)n * W, NWP = round4(NW);
     const int KW = P.KW;
-    const SmemLayout L = smem_layout(W, n, M.total_members, nw, KW, P.dom_in_smem, M.na);
+    // shared memory is per block: its layout follows the block's warps, not the scope's
+    const SmemLayout L = smem_layout(W, n, M.total_members, (int)(blockDim.x >> 5), KW, P.dom_in_smem, M.na);
     uint32_t* dom = P.dom_in_smem ? reinterpret_cast<uint32_t*>(smem + L.dom) : P.gdom + (size_t)ctx * 2 * NWP;
     uint32_t* rm = P.dom_in_smem ? reinterpret_cast<uint32_t*>(smem + L.rm) : dom + NWP;
     int16_t* mates = reinterpret_cast<int16_t*>(smem + L.mates);
@@ -131,12 +125,13 @@ __global__ void __launch_bounds__(ONE ? 32 : 1024, ONE ? 32 : 1) search_kernel(c
     uint32_t* bestkey = reinterpret_cast<uint32_t*>(smem + L.bestkey);
     uint32_t* post = L.has_post ? reinterpret_cast<uint32_t*>(smem + L.post) : nullptr;
     int8_t* post_ok = reinterpret_cast<int8_t*>(smem + L.post_ok);
-    uint32_t* chg0 = L.has_chg ? reinterpret_cast<uint32_t*>(smem + L.chg) : nullptr;
-    uint32_t* chg1 = L.has_chg ? chg0 + ((n + 31) >> 5) : nullptr;
+    // the grid context keeps its trigger bitmaps in global memory (every block reads them)
+    uint32_t* chg0 = SC::kGrid ? P.grid_chg : (L.has_chg ? reinterpret_cast<uint32_t*>(smem + L.chg) : nullptr);
+    uint32_t* chg1 = chg0 ? chg0 + ((n + 31) >> 5) : nullptr;
     const int nbw = (n + 31) >> 5;
     RoundCtx R{dom,     rm,      mates,     post,
-               post_ok, chg0,    chg1,      L.has_chg,
-               P.big_scratch ? P.big_scratch + (size_t)ctx * nw * M.big_words : nullptr,
+               post_ok, chg0,    chg1,      chg0 != nullptr,
+               P.big_scratch ? P.big_scratch + (SC::kGrid ? 0 : (size_t)ctx * nw * M.big_words) : nullptr,
                smem + L.scratch, L.stride, nullptr, P.alldiff, P.exact_wipe};
     bool first_all = true; // the root's first round evaluates every propagator
     bool skip_node = false; // first mode: the task just taken lies right of the best solution
@@ -147,14 +142,16 @@ __global__ void __launch_bounds__(ONE ? 32 : 1024, ONE ? 32 : 1) search_kernel(c
     const size_t OS = NWP + round4((size_t)KW + 2); // outbox: domains | path key | depth | branch var
 
     for (size_t i = tid; i < NWP; i += T) rm[i] = 0;
-    for (int i = tid; i < M.total_members; i += T) mates[i] = -1;
+    // block-private shared memory is initialised with block-local indices
+    for (int i = threadIdx.x; i < M.total_members; i += blockDim.x) mates[i] = -1;
     if (L.has_post)
-        for (int i = tid; i < M.na; i += T) post_ok[i] = 0;
-    for (int i = tid; i < KW; i += T) {
+        for (int i = threadIdx.x; i < M.na; i += blockDim.x) post_ok[i] = 0;
+    for (int i = threadIdx.x; i < KW; i += blockDim.x) {
         path[i] = 0;
         bestkey[i] = 0xffffffffu;
     }
     if (tid == 0) s_err = 0;
+    if (SC::kGrid) sc.sync();
 
     unsigned long long nodes = 0, failures = 0, rounds = 0, sols = 0;
     int sp = 0, base = 0, depth = 0;
@@ -237,7 +234,7 @@ __global__ void __launch_bounds__(ONE ? 32 : 1024, ONE ? 32 : 1) search_kernel(c
             s_src = got;
             s_ll = (long long)t + 1; // segment id of the subtree published under ticket t
         }
-        bar<ONE>();
+        sc.sync();
         const int got = s_src;
         if (got < 0) return false;
         seg = s_ll;
@@ -245,13 +242,13 @@ __global__ void __launch_bounds__(ONE ? 32 : 1024, ONE ? 32 : 1) search_kernel(c
         seg_f0 = failures;
         seg_r0 = rounds;
         const uint32_t* ob = P.outbox + (size_t)got * OS;
-        copy4_cg<ONE>(dom, ob, NWP);
+        copy4_cg(dom, ob, NWP, tid, T);
         for (int i = tid; i < KW; i += T) path[i] = __ldcg(ob + NWP + i);
         depth = (int)__ldcg(ob + NWP + KW);
         const int tvar = (int)__ldcg(ob + NWP + KW + 1);
         if (chg0)
             for (int i = tid; i < 2 * nbw; i += T) chg0[i] = 0;
-        bar<ONE>();
+        sc.sync();
         if (tid == 0) {
             if (chg0) chg0[tvar >> 5] |= 1u << (tvar & 31);
             __threadfence();
@@ -267,7 +264,7 @@ __global__ void __launch_bounds__(ONE ? 32 : 1024, ONE ? 32 : 1) search_kernel(c
                 hot = ld_volatile_v4(reinterpret_cast<const uint4*>(&ws->hot));
                 s_flag = right_of_best(); // the whole subtree lies right of a known solution
             }
-            bar<ONE>();
+            sc.sync();
             if (s_flag) {
                 flush_seg();
                 skip_node = true; // zero nodes: the main loop's backtrack takes the next task
@@ -278,12 +275,12 @@ __global__ void __launch_bounds__(ONE ? 32 : 1024, ONE ? 32 : 1) search_kernel(c
 
     bool have_work;
     if (!parallel || (ctx == 0 && !P.n_seed)) {
-        copy4<ONE>(dom, M.init_dom, NWP);
+        copy4(dom, M.init_dom, NWP, tid, T);
         have_work = true;
     } else {
         have_work = get_work();
     }
-    bar<ONE>();
+    sc.sync();
 
     while (have_work) {
         bool backtrack = false;
@@ -293,11 +290,11 @@ __global__ void __launch_bounds__(ONE ? 32 : 1024, ONE ? 32 : 1) search_kernel(c
         } else if (P.split_depth >= 0 && depth >= P.split_depth) {
             // ============ frontier expansion: this open node becomes a task (counted by its shard)
             if (tid == 0) s_ll = (long long)atomicAdd((unsigned long long*)&ws->n_tasks, 1ull);
-            bar<ONE>();
+            sc.sync();
             const long long t = s_ll;
             if (t < P.task_cap) {
                 uint32_t* tb = P.tasks + (size_t)t * OS;
-                copy4<ONE>(tb, dom, NWP);
+                copy4(tb, dom, NWP, tid, T);
                 for (int i = tid; i < KW; i += T) tb[NWP + i] = path[i];
                 if (tid == 0) {
                     tb[NWP + KW] = (uint32_t)depth;
@@ -346,13 +343,13 @@ __global__ void __launch_bounds__(ONE ? 32 : 1024, ONE ? 32 : 1) search_kernel(c
                 }
                 s_flag = empty;
             }
-            bar<ONE>();
+            sc.sync();
             backtrack = s_flag != 0;
             if (backtrack) ++failures;
         }
         if (!backtrack) {
             int r = 0;
-            const int st = block_fixpoint<W, ONE>(M, R, &s_err, &s_min, 0, &r, nullptr, first_all);
+            const int st = block_fixpoint<W>(M, R, &s_err, &s_min, 0, &r, nullptr, first_all, sc);
             first_all = false;
             rounds += (unsigned long long)r;
             if (st == R_ERROR) {
@@ -369,7 +366,7 @@ __global__ void __launch_bounds__(ONE ? 32 : 1024, ONE ? 32 : 1) search_kernel(c
         }
         if (parallel && tid == 0) g_has_bound = (int)hot.w; // the prefetched bound pairs with this flag
         if (!backtrack) {
-            const int sel = select_var<W, ONE>(M, dom, P.var_heuristic, s_red);
+            const int sel = select_var<W>(M, dom, P.var_heuristic, red, sc);
             if (sel < 0) {
                 // ============ solution leaf (emit_solution, search.cpp:134-156)
                 if (tid == 0) {
@@ -379,7 +376,7 @@ __global__ void __launch_bounds__(ONE ? 32 : 1024, ONE ? 32 : 1) search_kernel(c
                         s_ll = parallel ? (long long)atomicAdd((unsigned long long*)&ws->sol_count, 1ull) : (long long)sols;
                     if (parallel) atomicMax(&ws->max_depth, depth);
                 }
-                bar<ONE>();
+                sc.sync();
                 const long long sidx = s_ll;
                 const unsigned long long idx = (unsigned long long)sidx;
                 ++sols;
@@ -394,7 +391,7 @@ __global__ void __launch_bounds__(ONE ? 32 : 1024, ONE ? 32 : 1) search_kernel(c
                     }
                 }
                 if (first_mode) {
-                    bar<ONE>();
+                    sc.sync();
                     if (tid == 0 && sidx >= 0 && idx < P.sol_cap) { // publish as the best if still the best
                         __threadfence();
                         spin_lock(&ws->best_lock);
@@ -424,7 +421,7 @@ __global__ void __launch_bounds__(ONE ? 32 : 1024, ONE ? 32 : 1) search_kernel(c
                             }
                         s_flag = less || !has_first;
                     }
-                    bar<ONE>();
+                    sc.sync();
                     if (s_flag) {
                         has_first = true;
                         for (int i = tid; i < KW; i += T) {
@@ -455,7 +452,7 @@ __global__ void __launch_bounds__(ONE ? 32 : 1024, ONE ? 32 : 1) search_kernel(c
                         g_has_bound = 1;
                     }
                 }
-                bar<ONE>();
+                sc.sync();
                 if (!parallel && sols >= P.max_solutions) {
                     if (tid == 0) {
                         ws->user_stop = 1;
@@ -474,7 +471,7 @@ __global__ void __launch_bounds__(ONE ? 32 : 1024, ONE ? 32 : 1) search_kernel(c
                     break;
                 }
                 const int bit = dom_first<W>(dom + (size_t)sel * W);
-                copy4<ONE>(frames + (size_t)sp * NWP, dom, NWP);
+                copy4(frames + (size_t)sp * NWP, dom, NWP, tid, T);
                 if (chg0)
                     for (int i = tid; i < 2 * nbw; i += T) chg0[i] = 0;
                 if (tid == 0) {
@@ -489,7 +486,7 @@ __global__ void __launch_bounds__(ONE ? 32 : 1024, ONE ? 32 : 1) search_kernel(c
                     if (first_mode && want == 1 && frame_right_of_best(meta[base * 4 + 2])) want = 3;
                     s_flag = want;
                 }
-                bar<ONE>();
+                sc.sync();
                 if (tid < W) dom[(size_t)sel * W + tid] = (tid == (bit >> 5)) ? (1u << (bit & 31)) : 0u;
                 if (tid == 0 && chg0) chg0[sel >> 5] |= 1u << (sel & 31);
                 trig_var = sel;
@@ -514,7 +511,7 @@ __global__ void __launch_bounds__(ONE ? 32 : 1024, ONE ? 32 : 1) search_kernel(c
                         ob[NWP + KW] = (uint32_t)(fdepth + 1);
                         ob[NWP + KW + 1] = (uint32_t)fvar;
                     }
-                    bar<ONE>();
+                    sc.sync();
                     if (tid == 0) {
                         P.outbox_busy[ctx] = 1;
                         atomicAdd(&ws->outstanding, 1);
@@ -524,7 +521,7 @@ __global__ void __launch_bounds__(ONE ? 32 : 1024, ONE ? 32 : 1) search_kernel(c
                         ++donations;
                     }
                 }
-                bar<ONE>();
+                sc.sync();
                 continue;
             }
         }
@@ -532,22 +529,22 @@ __global__ void __launch_bounds__(ONE ? 32 : 1024, ONE ? 32 : 1) search_kernel(c
         // ================= backtrack: right branch of the deepest pending frame (:122-131)
         if (parallel) {
             if (tid == 0) s_flag = hot.z;
-            bar<ONE>();
+            sc.sync();
             if (s_flag) break;
         }
         if (sp == base) {
             if (!parallel) break;
             flush_seg();
             have_work = get_work();
-            bar<ONE>();
+            sc.sync();
             continue;
         }
         --sp;
-        copy4<ONE>(dom, frames + (size_t)sp * NWP, NWP);
+        copy4(dom, frames + (size_t)sp * NWP, NWP, tid, T);
         if (chg0)
             for (int i = tid; i < 2 * nbw; i += T) chg0[i] = 0;
         const int var = meta[sp * 4 + 0], bit = meta[sp * 4 + 1], d = meta[sp * 4 + 2];
-        bar<ONE>();
+        sc.sync();
         if (tid == 0) {
             dom[(size_t)var * W + (bit >> 5)] &= ~(1u << (bit & 31));
             if (chg0) chg0[var >> 5] |= 1u << (var & 31);
@@ -559,14 +556,14 @@ __global__ void __launch_bounds__(ONE ? 32 : 1024, ONE ? 32 : 1) search_kernel(c
         }
         depth = d + 1;
         trig_var = var;
-        bar<ONE>();
+        sc.sync();
         if (first_mode && s_flag) {
             sp = base;
             skip_node = true;
         }
     }
     flush_seg();
-    bar<ONE>();
+    sc.sync();
     if (parallel && tid == 0 && have_work) {
         // unwound by stop: this context no longer counts as outstanding
         atomicSub(&ws->outstanding, 1);
@@ -584,11 +581,30 @@ __global__ void __launch_bounds__(ONE ? 32 : 1024, ONE ? 32 : 1) search_kernel(c
     }
 }
 
+template <int W>
+__global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ Ctl C;
+    __shared__ unsigned red[32];
+    BlockScope sc;
+    search_body<W>(P, sc, C, red, smem);
+}
+
+// one search context spanning the GPU (cooperative launch); see scope.cuh
+template <int W>
+__global__ void __launch_bounds__(1024) search_kernel_grid(const SearchParams P) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ unsigned red[32];
+    GridScope sc{P.grid_or, P.grid_min};
+    search_body<W>(P, sc, *P.grid_ctl, red, smem);
+}
+
 // cubics_propagate / cubics_removals: one block over caller-provided domains
 template <int W>
 __global__ void __launch_bounds__(1024) propagate_kernel(const PropParams P, uint32_t* gscratch, int dom_in_smem) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ int s_err, s_min;
+    BlockScope sc;
     const DevModel& M = P.M;
     const int tid = threadIdx.x, T = blockDim.x, nw = T >> 5;
     const size_t NW = (size_t)M.n * W, NWP = round4(NW);
@@ -607,14 +623,14 @@ __global__ void __launch_bounds__(1024) propagate_kernel(const PropParams P, uin
     if (tid == 0) s_err = 0;
     __syncthreads();
     if (P.removals_only) {
-        run_propagators<W>(M, R, &s_err, nullptr);
+        run_propagators<W>(M, R, &s_err, nullptr, sc);
         __syncthreads();
         for (size_t i = tid; i < NWP; i += T) P.out[i] = rm[i] & dom[i];
         if (tid == 0) P.result[4] = s_err;
         return;
     }
     int rounds = 0, fv = -1;
-    const int st = block_fixpoint<W>(M, R, &s_err, &s_min, P.max_rounds, &rounds, &fv, true);
+    const int st = block_fixpoint<W>(M, R, &s_err, &s_min, P.max_rounds, &rounds, &fv, true, sc);
     for (size_t i = tid; i < NWP; i += T) P.dom[i] = dom[i];
     if (tid == 0) {
         P.result[0] = st == R_FAILED;

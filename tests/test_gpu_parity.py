@@ -365,3 +365,28 @@ def test_table_random_csp_search_matches_oracle():
                 S.SearchConfig(max_solutions=1, node_limit=1500, var_heuristic=0, engine=PARITY)):
         r, ro = S.solve_satisfy(m, cfg), O.solve_satisfy(m, cfg)
         assert r.stats.as_tuple() == ro.stats.as_tuple()
+
+
+@pytest.mark.parametrize("key", ["nq8|--all", "nq8|--max 1", "nq10|--all --node-limit 1000", "golomb7", "magic3|--all",
+                                 "magic5|--max 1", "rcsp_10000|--max 1 --node-limit 200",
+                                 "rcsp_100000|--max 1 --node-limit 200"])
+def test_grid_context_matches_reference(key):
+    # one search context spanning the GPU (cooperative launch, grid barriers between phases)
+    g = G.goldens()[key]
+    stats, sol = gpu_case(key, A.ENGINE_GRID)
+    assert stats == G.expected_tuple(g)
+    assert sol == (g.get("best") if "best" in g else g.get("first"))
+
+
+def test_grid_context_tables_and_corpus():
+    for seed in range(0, 200, 7):
+        m = S.parse_model(models.corpus_instance(seed))
+        st, ost = S.SearchStats(), S.SearchStats()
+        got = [s.values for s in S.enumerate_solutions(m, S.SearchConfig(engine=A.ENGINE_GRID), st)]
+        exp = [s.values for s in O.enumerate_solutions(m, S.SearchConfig(), ost)]
+        assert got == exp and st.as_tuple() == ost.as_tuple(), seed
+    n = 200
+    t = models.phase_transition_tightness(n, 10, 2 * n) - 0.06
+    m = S.parse_model(models.random_binary_csp(n, 10, 2 * n, t, 5))
+    cfg = S.SearchConfig(max_solutions=1, node_limit=500, engine=A.ENGINE_GRID)
+    assert S.solve_satisfy(m, cfg).stats.as_tuple() == O.solve_satisfy(m, cfg).stats.as_tuple()
