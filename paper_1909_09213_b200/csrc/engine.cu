@@ -555,10 +555,12 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
         L = dev::smem_layout(P.W, n, P.total_members, nw, KW, false, P.na);
         if (L.total > kSmemBudget) throw StatusError{CUBICS_E_UNSUPPORTED, "search context does not fit in shared memory"};
     }
+    // propagator features the model needs: the lean kernel instantiations skip the rest
+    const int feat = (P.nl ? 1 : 0) | (P.ntb + P.ntn ? 2 : 0) | (P.big_words ? 4 : 0) | (first_mode ? 8 : 0);
     int n_ctx = 1;
     if (parallel) {
         int per_sm = 0;
-#define OCC(w) occupancy_search<w>(block, L.total, &per_sm)
+#define OCC(w) occupancy_search<w>(feat, block, L.total, &per_sm)
         CUBICS_DISPATCH_W(P.W, OCC)
 #undef OCC
         int sms = 0;
@@ -718,7 +720,7 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
             CUBICS_DISPATCH_W(P.W, LG)
 #undef LG
         } else {
-#define LS(w) launch_search<w>(S, n_ctx, block, L.total, st)
+#define LS(w) launch_search<w>(S, feat, n_ctx, block, L.total, st)
             CUBICS_DISPATCH_W(P.W, LS)
 #undef LS
         }

@@ -8,10 +8,11 @@
 
 namespace cubics {
 
+// feat: the model's propagator features (dev::Feature bits); a lean instantiation is chosen
 template <int W>
-cudaError_t launch_search(const SearchParams& P, int grid, int block, size_t smem, cudaStream_t st);
+cudaError_t launch_search(const SearchParams& P, int feat, int grid, int block, size_t smem, cudaStream_t st);
 template <int W>
-cudaError_t occupancy_search(int block, size_t smem, int* blocks_per_sm);
+cudaError_t occupancy_search(int feat, int block, size_t smem, int* blocks_per_sm);
 template <int W>
 cudaError_t launch_search_grid(const SearchParams& P, int grid, int block, size_t smem, cudaStream_t st);
 template <int W>

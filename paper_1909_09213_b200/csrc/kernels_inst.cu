@@ -18,23 +18,39 @@ cudaError_t grant_smem(K k, size_t smem, size_t& granted) {
     return e;
 }
 size_t g_search_smem = 48 * 1024, g_prop_smem = 48 * 1024, g_grid_smem = 48 * 1024;
+size_t g_search_smem0 = 48 * 1024, g_search_smem1 = 48 * 1024;
+} // namespace
+
+// lean instantiations for narrow domains: {RelBin + small alldiff}, {+ linear}; everything else
+// (tables, large alldifferents, the first-solution bookkeeping, wide domains) runs the full kernel
+namespace {
+using SearchFn = void (*)(const SearchParams);
+
+SearchFn pick_search(int feat) {
+    if constexpr (CUBICS_W <= 4) {
+        if (feat == 0) return dev::search_kernel<CUBICS_W, 0>;
+        if (feat == dev::F_LINEAR) return dev::search_kernel<CUBICS_W, dev::F_LINEAR>;
+    }
+    return dev::search_kernel<CUBICS_W, dev::F_ALL>;
+}
 } // namespace
 
 template <>
-cudaError_t launch_search<CUBICS_W>(const SearchParams& P, int grid, int block, size_t smem, cudaStream_t st) {
+cudaError_t launch_search<CUBICS_W>(const SearchParams& P, int feat, int grid, int block, size_t smem,
+                                    cudaStream_t st) {
     // the generic block kernel also runs one-warp contexts: a __syncwarp-specialised variant
     // measured slower on B200 (19.3 vs 14.0 ms on nq14; register spills at the 64-register cap)
-    auto k = dev::search_kernel<CUBICS_W>;
-    cudaError_t e = grant_smem(k, smem, g_search_smem);
+    SearchFn k = pick_search(feat);
+    cudaError_t e = grant_smem(k, smem, feat == 0 ? g_search_smem0 : (feat == dev::F_LINEAR ? g_search_smem1 : g_search_smem));
     if (e != cudaSuccess) return e;
     k<<<grid, block, smem, st>>>(P);
     return cudaGetLastError();
 }
 
 template <>
-cudaError_t occupancy_search<CUBICS_W>(int block, size_t smem, int* out) {
-    auto k = dev::search_kernel<CUBICS_W>;
-    cudaError_t e = grant_smem(k, smem, g_search_smem);
+cudaError_t occupancy_search<CUBICS_W>(int feat, int block, size_t smem, int* out) {
+    SearchFn k = pick_search(feat);
+    cudaError_t e = grant_smem(k, smem, feat == 0 ? g_search_smem0 : (feat == dev::F_LINEAR ? g_search_smem1 : g_search_smem));
     if (e != cudaSuccess) return e;
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, k, block, smem);
 }

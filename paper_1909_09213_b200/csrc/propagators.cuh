@@ -27,6 +27,11 @@ typedef __int128 i128;
 
 enum RoundStatus : int { R_CHANGED = 0, R_STABLE = 1, R_FAILED = 2, R_ERROR = 3 };
 
+// Compile-time propagator features of a kernel instantiation: a model without linear sums,
+// tables or large alldifferents runs a kernel without that code (register pressure decides the
+// occupancy of one-warp search contexts).
+enum Feature : int { F_LINEAR = 1, F_TABLE = 2, F_BIGAD = 4, F_FIRST = 8, F_ALL = 15 };
+
 // ------------------------------------------------------------------ bitset helpers
 template <int W>
 __device__ __forceinline__ bool dom_empty(const uint32_t* d) {
@@ -977,7 +982,7 @@ __device__ __forceinline__ bool trig_bit(const uint32_t* t, int v) { return (t[v
 // untriggered propagator sees exactly the domains of its last evaluation, whose removals are
 // already applied, so skipping it changes no domain, no "changed" flag and no round count.
 // *s_err receives DERR_OVERFLOW.
-template <int W, class SC>
+template <int W, int F, class SC>
 __device__ __forceinline__ void run_propagators(const DevModel& M, const RoundCtx& R, volatile int* s_err,
                                                 const uint32_t* trig, SC& sc) {
     const int tid = sc.tid(), T = sc.nthreads(), nw = sc.nwarps(), warp = sc.warp(), lane = threadIdx.x & 31;
@@ -1022,6 +1027,7 @@ __device__ __forceinline__ void run_propagators(const DevModel& M, const RoundCt
                 }
             }
         }
+        if constexpr ((F & F_LINEAR) != 0)
         for (int c = tid; c < M.nl; c += prop_threads) {
             if (R.enabled && !R.enabled[M.nr + c]) continue;
             if (trig) {
@@ -1031,10 +1037,12 @@ __device__ __forceinline__ void run_propagators(const DevModel& M, const RoundCt
             }
             if (!prop_linear<W>(M, c, R.dom, R.rm)) *s_err = DERR_OVERFLOW;
         }
+        if constexpr ((F & F_TABLE) != 0)
         for (int c = tid; c < M.ntb; c += prop_threads) {
             if (trig && !trig_bit(trig, M.tb_xy[2 * c]) && !trig_bit(trig, M.tb_xy[2 * c + 1])) continue;
             prop_table2<W>(M, c, R.dom, R.rm);
         }
+        if constexpr ((F & F_TABLE) != 0)
         for (int c = tid; c < M.ntn; c += prop_threads) {
             if (trig) {
                 bool hit = false;
@@ -1054,7 +1062,7 @@ __device__ __forceinline__ void run_propagators(const DevModel& M, const RoundCt
                 for (int t = b + lane; t < e; t += 32) hit |= trig_bit(trig, M.ad_var[t]);
                 if (!__any_sync(FULL, hit)) continue;
             }
-            if (M.ad_uw[a] > 0) { // generic path: many members or a wide value universe
+            if ((F & F_BIGAD) != 0 && M.ad_uw[a] > 0) { // generic path: many members or a wide universe
                 uint32_t* scratch = R.big + (size_t)(SC::kGrid ? warp : (int)(threadIdx.x >> 5)) * M.big_words;
                 if (R.alldiff) prop_alldiff_gac_big<W>(M, a, R.dom, R.rm, R.mates + M.ad_start[a], scratch, lane, R.exact_wipe);
                 else prop_alldiff_fc_big<W>(M, a, R.dom, R.rm, scratch, lane);
@@ -1123,7 +1131,7 @@ __device__ __forceinline__ int apply_removals(const DevModel& M, const RoundCtx&
 // propagate_fixpoint (propagation.cpp:516-532); *rounds counts every round including the last.
 // first_all: evaluate every propagator in round 1; otherwise round 1 is triggered by the vars
 // set in R.chg0 (the caller's branch decision). Both trigger buffers are left dirty.
-template <int W, class SC>
+template <int W, int F, class SC>
 __device__ int block_fixpoint(const DevModel& M, const RoundCtx& R, volatile int* s_err, volatile int* s_min,
                               int max_rounds, int* rounds, int* failed_var, bool first_all, SC& sc) {
     const int tid = sc.tid(), T = sc.nthreads();
@@ -1135,7 +1143,7 @@ __device__ int block_fixpoint(const DevModel& M, const RoundCtx& R, volatile int
     for (;;) {
         if (nxt)
             for (int i = tid; i < nb; i += T) nxt[i] = 0;
-        run_propagators<W>(M, R, s_err, all ? nullptr : cur, sc);
+        run_propagators<W, F>(M, R, s_err, all ? nullptr : cur, sc);
         sc.sync();
         const int st = apply_removals<W>(M, R, s_err, s_min, failed_var, nxt, sc);
         ++r;

@@ -102,7 +102,7 @@ __device__ __forceinline__ int select_var(const DevModel& M, const uint32_t* dom
     return best == 0xffffffffu ? -1 : (int)(best & 0x1fffffu);
 }
 
-template <int W, class SC>
+template <int W, int F, class SC>
 __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& C, unsigned* red, uint8_t* smem) {
     int& s_err = C.err;
     int& s_min = C.min;
@@ -169,7 +169,7 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
     long long idle_cyc = 0, steals = 0, donations = 0;
     const long long t_start = clock64();
     // first mode: current segment and the counters at its start; thread 0 caches the best key
-    const bool first_mode = P.first_mode != 0;
+    const bool first_mode = (F & F_FIRST) != 0 && P.first_mode != 0; // compile-time off in lean kernels
     long long seg = (!parallel || ctx == 0) && !P.n_seed ? 0 : -1;
     unsigned long long seg_n0 = 0, seg_f0 = 0, seg_r0 = 0;
     int gbest_idx = -1;
@@ -349,7 +349,7 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
         }
         if (!backtrack) {
             int r = 0;
-            const int st = block_fixpoint<W>(M, R, &s_err, &s_min, 0, &r, nullptr, first_all, sc);
+            const int st = block_fixpoint<W, F>(M, R, &s_err, &s_min, 0, &r, nullptr, first_all, sc);
             first_all = false;
             rounds += (unsigned long long)r;
             if (st == R_ERROR) {
@@ -581,13 +581,13 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
     }
 }
 
-template <int W>
+template <int W, int F>
 __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ Ctl C;
     __shared__ unsigned red[32];
     BlockScope sc;
-    search_body<W>(P, sc, C, red, smem);
+    search_body<W, F>(P, sc, C, red, smem);
 }
 
 // one search context spanning the GPU (cooperative launch); see scope.cuh
@@ -596,7 +596,7 @@ __global__ void __launch_bounds__(1024) search_kernel_grid(const SearchParams P)
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ unsigned red[32];
     GridScope sc{P.grid_or, P.grid_min};
-    search_body<W>(P, sc, *P.grid_ctl, red, smem);
+    search_body<W, F_ALL>(P, sc, *P.grid_ctl, red, smem);
 }
 
 // cubics_propagate / cubics_removals: one block over caller-provided domains
@@ -623,14 +623,14 @@ __global__ void __launch_bounds__(1024) propagate_kernel(const PropParams P, uin
     if (tid == 0) s_err = 0;
     __syncthreads();
     if (P.removals_only) {
-        run_propagators<W>(M, R, &s_err, nullptr, sc);
+        run_propagators<W, F_ALL>(M, R, &s_err, nullptr, sc);
         __syncthreads();
         for (size_t i = tid; i < NWP; i += T) P.out[i] = rm[i] & dom[i];
         if (tid == 0) P.result[4] = s_err;
         return;
     }
     int rounds = 0, fv = -1;
-    const int st = block_fixpoint<W>(M, R, &s_err, &s_min, P.max_rounds, &rounds, &fv, true, sc);
+    const int st = block_fixpoint<W, F_ALL>(M, R, &s_err, &s_min, P.max_rounds, &rounds, &fv, true, sc);
     for (size_t i = tid; i < NWP; i += T) P.dom[i] = dom[i];
     if (tid == 0) {
         P.result[0] = st == R_FAILED;
