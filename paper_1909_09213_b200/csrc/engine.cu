@@ -16,6 +16,7 @@
 #include <mutex>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -923,11 +924,8 @@ extern "C" void cubics_search_config_init(cubics_search_config* c) {
 
 namespace {
 // Search for every solution with records materialised (rerun once with an exact buffer when the
-// first guess overflowed), then hand each solution, in the reference's DFS order, to visit(i, row).
-template <class Visit>
-int satisfy_records(const HostModel& m, const cubics_search_config& cfg, bool record, cubics_result* out,
-                    Visit&& visit) {
-    const double t0 = now_ms();
+// first guess overflowed); the records come back in the reference's DFS order.
+RunOut satisfy_run(const HostModel& m, const cubics_search_config& cfg, bool record, cubics_result* out) {
     std::memset(out, 0, sizeof *out);
     // an objective makes the stream a sequence of incumbents, whose order only the reference
     // node order reproduces: AUTO picks the parity engine then
@@ -960,28 +958,39 @@ int satisfy_records(const HostModel& m, const cubics_search_config& cfg, bool re
         const size_t last = r.rec.count - 1;
         out->objective = m.offset[m.goal_var] + r.rec.vals[last * n + m.goal_var];
     }
-    if (record && r.rec.count) {
+    if (record && r.rec.count && !r.rec.ordered && r.KW) { // keyed records: host-side DFS order
+        const int KW = r.KW;
         std::vector<uint64_t> order(r.rec.count);
         std::iota(order.begin(), order.end(), 0);
-        if (!r.rec.ordered && r.KW) {
-            const int KW = r.KW;
-            const uint32_t* K = r.rec.keys.data();
-            std::sort(order.begin(), order.end(), [&](uint64_t a, uint64_t b) {
-                return std::lexicographical_compare(K + a * KW, K + (a + 1) * KW, K + b * KW, K + (b + 1) * KW);
-            });
-        }
-        for (uint64_t i = 0; i < order.size(); ++i) {
-            const uint64_t s = order[i];
-            if (!visit(i, r.rec.vals.data() + s * n)) {
-                if (!r.KW && !r.rec.stats.empty()) { // parity: the reference stops right here
-                    out->stats.nodes = r.rec.stats[s * 3 + 0];
-                    out->stats.failures = r.rec.stats[s * 3 + 1];
-                    out->stats.rounds = r.rec.stats[s * 3 + 2];
-                    out->stats.solutions = i + 1;
-                }
-                out->complete = 0;
-                break;
+        const uint32_t* K = r.rec.keys.data();
+        std::sort(order.begin(), order.end(), [&](uint64_t a, uint64_t b) {
+            return std::lexicographical_compare(K + a * KW, K + (a + 1) * KW, K + b * KW, K + (b + 1) * KW);
+        });
+        std::vector<uint16_t> v(r.rec.vals.size());
+        for (uint64_t i = 0; i < order.size(); ++i)
+            std::copy_n(r.rec.vals.begin() + order[i] * n, n, v.begin() + i * n);
+        r.rec.vals.swap(v);
+        r.rec.ordered = true;
+    }
+    return r;
+}
+
+template <class Visit>
+int satisfy_records(const HostModel& m, const cubics_search_config& cfg, bool record, cubics_result* out,
+                    Visit&& visit) {
+    const double t0 = now_ms();
+    RunOut r = satisfy_run(m, cfg, record, out);
+    const int n = m.n_vars();
+    for (uint64_t i = 0; record && i < r.rec.count; ++i) {
+        if (!visit(i, r.rec.vals.data() + i * n)) {
+            if (!r.KW && !r.rec.stats.empty()) { // parity: the reference stops right here
+                out->stats.nodes = r.rec.stats[i * 3 + 0];
+                out->stats.failures = r.rec.stats[i * 3 + 1];
+                out->stats.rounds = r.rec.stats[i * 3 + 2];
+                out->stats.solutions = i + 1;
             }
+            out->complete = 0;
+            break;
         }
     }
     out->total_ms = now_ms() - t0;
@@ -1008,23 +1017,32 @@ extern "C" int cubics_enumerate(const cubics_model* h, const cubics_search_confi
     if (!h || !cfg || !out || !sols) return CUBICS_E_INVALID;
     *sols = nullptr;
     return guarded([&] {
+        const double t0 = now_ms();
         const HostModel& m = h->m;
         const int n = m.n_vars();
+        RunOut r = satisfy_run(m, *cfg, !cfg->count_only, out);
         auto* S = new cubics_solutions{};
         S->n_vars = n;
-        std::vector<int64_t> buf;
-        int rc = satisfy_records(m, *cfg, !cfg->count_only, out, [&](uint64_t i, const uint16_t* row) {
-            if (buf.empty()) buf.resize(out->stats.solutions * (uint64_t)n);
-            int64_t* dst = buf.data() + i * n;
-            for (int v = 0; v < n; ++v) dst[v] = m.offset[v] + row[v];
-            return true;
-        });
-        S->count = buf.empty() ? 0 : out->stats.solutions;
-        S->values = new int64_t[std::max<size_t>(buf.size(), 1)];
-        std::memcpy(S->values, buf.data(), sizeof(int64_t) * buf.size());
+        S->count = r.rec.count;
+        const uint64_t total = r.rec.count * (uint64_t)n;
+        S->values = new int64_t[std::max<uint64_t>(total, 1)];
+        // offset conversion straight into the returned buffer, split over host threads
+        const unsigned nt = total > (1u << 20) ? std::max(1u, std::min(16u, std::thread::hardware_concurrency())) : 1u;
+        auto conv = [&](uint64_t lo, uint64_t hi) {
+            for (uint64_t i = lo; i < hi; ++i) {
+                const uint16_t* row = r.rec.vals.data() + i * n;
+                int64_t* dst = S->values + i * n;
+                for (int v = 0; v < n; ++v) dst[v] = m.offset[v] + row[v];
+            }
+        };
+        std::vector<std::thread> pool;
+        for (unsigned t = 1; t < nt; ++t)
+            pool.emplace_back(conv, r.rec.count * t / nt, r.rec.count * (t + 1) / nt);
+        conv(0, r.rec.count / nt);
+        for (auto& th : pool) th.join();
         *sols = S;
-        out->total_ms += 0;
-        return rc;
+        out->total_ms = now_ms() - t0;
+        return CUBICS_OK;
     });
 }
 

@@ -407,14 +407,15 @@ def enumerate_array(model: Model, cfg: SearchConfig | None = None):
     sols = C.POINTER(A.Solutions)()
     c = cfg.to_c()
     _check(lib().cubics_enumerate(model.handle, C.byref(c), C.byref(sols), C.byref(res)), "enumerate")
-    try:
-        cnt, nv = sols.contents.count, sols.contents.n_vars
-        if cnt and nv:
-            arr = np.ctypeslib.as_array(sols.contents.values, shape=(cnt, nv)).copy()
-        else:
-            arr = np.zeros((cnt, nv), dtype=np.int64)
-    finally:
+    cnt, nv = sols.contents.count, sols.contents.n_vars
+    if cnt and nv:
+        # zero-copy view of the library buffer; freed when the last view is collected
+        arr = np.ctypeslib.as_array(sols.contents.values, shape=(cnt, nv))
+        import weakref
+        weakref.finalize(arr, lib().cubics_solutions_free, sols)
+    else:
         lib().cubics_solutions_free(sols)
+        arr = np.zeros((cnt, nv), dtype=np.int64)
     return arr, SatisfyResult(_stats(res), bool(res.complete), res.engine, res.contexts, res.device_ms,
                               res.total_ms, res.h2d_bytes, res.d2h_bytes, res.kernel_launches)
 
