@@ -267,8 +267,9 @@ OptimizeResult solve_optimize(const Model& m, const SearchConfig& cfg) {
     return optimize_with(m, config_of(cfg)); // no objective -> std::logic_error via the ABI
 }
 
-// Large neighbourhood search (search.cpp:225-314): the host orchestrates; every first-solution
-// and neighbourhood search runs on the device. Semantics follow the reference: Rng::derive per
+// Large neighbourhood search (search.cpp:225-314): the host orchestrates; the first-solution
+// search runs on the device and all neighbourhoods of an iteration run as ONE batched launch
+// (cubics_solve_optimize_batch, one thread block per neighbourhood, each in reference order). Semantics follow the reference: Rng::derive per
 // (seed, neighbourhood, iteration), partial Fisher-Yates destroy set, incumbent frozen for the
 // iteration, deterministic lowest-index merge.
 LnsResult lns_optimize(const Model& m, const LnsConfig& cfg) {
@@ -290,10 +291,28 @@ LnsResult lns_optimize(const Model& m, const LnsConfig& cfg) {
     const int n = m.num_vars();
     const int destroy = std::min(n, std::max(1, static_cast<int>(std::ceil(cfg.destroy_rate * n))));
     auto better = [&](std::int64_t a, std::int64_t b) { return goal.minimizing ? a < b : a > b; };
+    // every neighbourhood of an iteration is one problem of ONE batched device launch
+    ModelHandle h(model_of(m));
+    size_t nw = 0;
+    std::vector<size_t> wstart(static_cast<size_t>(n) + 1, 0);
+    for (int v = 0; v < n; ++v) wstart[v + 1] = wstart[v] + static_cast<size_t>(m.domains[v].word_count());
+    nw = wstart[n];
+    std::vector<std::uint64_t> base(nw);
+    for (int v = 0; v < n; ++v) {
+        const auto& w = m.domains[v].words();
+        std::copy(w.begin(), w.end(), base.begin() + wstart[v]);
+    }
+    cubics_search_config k;
+    cubics_search_config_init(&k);
+    k.alldiff = cfg.alldiff == AlldiffLevel::ArcConsistent ? CUBICS_ARC_CONSISTENT : CUBICS_FORWARD_CHECKING;
+    k.node_limit = cfg.per_iteration_node_limit;
+    k.engine = CUBICS_ENGINE_PARITY;
+    const int nbs = std::max(0, cfg.neighborhoods);
     for (int iter = 0; iter < cfg.iterations; ++iter) {
         const Solution incumbent = *best;
-        std::vector<std::optional<Solution>> found(static_cast<size_t>(cfg.neighborhoods));
-        for (int nb = 0; nb < cfg.neighborhoods; ++nb) {
+        std::vector<std::optional<Solution>> found(static_cast<size_t>(nbs));
+        std::vector<std::uint64_t> words(nw * nbs);
+        for (int nb = 0; nb < nbs; ++nb) {
             Rng rng = Rng::derive(cfg.seed, static_cast<std::uint64_t>(nb), static_cast<std::uint64_t>(iter));
             std::vector<char> destroyed(static_cast<size_t>(n), 0);
             std::vector<int> ids(static_cast<size_t>(n));
@@ -303,26 +322,33 @@ LnsResult lns_optimize(const Model& m, const LnsConfig& cfg) {
                 std::swap(ids[static_cast<size_t>(i)], ids[static_cast<size_t>(j)]);
                 destroyed[static_cast<size_t>(ids[static_cast<size_t>(i)])] = 1;
             }
-            Model sub = m;
+            std::uint64_t* wd = words.data() + nw * nb;
+            std::copy(base.begin(), base.end(), wd);
             for (int v = 0; v < n; ++v)
-                if (!destroyed[static_cast<size_t>(v)]) {
-                    std::int64_t val = incumbent.values[static_cast<size_t>(v)];
-                    sub.domains[static_cast<size_t>(v)] = Domain(val, val);
+                if (!destroyed[static_cast<size_t>(v)]) { // neighborhood_model: Domain(val, val)
+                    const std::int64_t bit = incumbent.values[static_cast<size_t>(v)] - m.domains[v].offset();
+                    std::fill(wd + wstart[v], wd + wstart[v + 1], 0);
+                    wd[wstart[v] + bit / 64] = std::uint64_t{1} << (bit % 64);
                 }
-            cubics_search_config k;
-            cubics_search_config_init(&k);
-            k.alldiff = cfg.alldiff == AlldiffLevel::ArcConsistent ? CUBICS_ARC_CONSISTENT : CUBICS_FORWARD_CHECKING;
-            k.node_limit = cfg.per_iteration_node_limit;
-            k.engine = CUBICS_ENGINE_PARITY;
-            k.has_initial_bound = 1;
-            k.initial_bound = *incumbent.objective;
-            OptimizeResult r = optimize_with(sub, k);
-            found[static_cast<size_t>(nb)] = r.best;
+        }
+        std::vector<std::int64_t> bounds(static_cast<size_t>(nbs), *incumbent.objective);
+        std::vector<std::int64_t> vals(static_cast<size_t>(nbs) * std::max(1, n));
+        std::vector<cubics_result> rs(static_cast<size_t>(nbs));
+        if (nbs)
+            check(cubics_solve_optimize_batch(h.m, &k, nbs, words.data(), bounds.data(), nullptr, vals.data(), rs.data()));
+        for (int nb = 0; nb < nbs; ++nb) {
+            const cubics_result& r = rs[static_cast<size_t>(nb)];
+            if (r.has_solution) {
+                Solution s;
+                s.values.assign(vals.begin() + static_cast<size_t>(nb) * n, vals.begin() + static_cast<size_t>(nb + 1) * n);
+                s.objective = r.objective;
+                found[static_cast<size_t>(nb)] = s;
+            }
             res.stats.nodes += r.stats.nodes;
             res.stats.failures += r.stats.failures;
             res.stats.rounds += r.stats.rounds;
         }
-        for (int nb = 0; nb < cfg.neighborhoods; ++nb) {
+        for (int nb = 0; nb < nbs; ++nb) {
             const auto& cand = found[static_cast<size_t>(nb)];
             if (cand && better(*cand->objective, *best->objective)) best = cand;
         }

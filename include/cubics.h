@@ -12,6 +12,7 @@
  *   cubics_solve_satisfy       fd::solve_satisfy        include/fd/search.hpp:62, src/search.cpp:174-177
  *                              fd::enumerate_solutions  include/fd/search.hpp:65-66, src/search.cpp:179-189
  *   cubics_solve_optimize      fd::solve_optimize       include/fd/search.hpp:77, src/search.cpp:191-201
+ *   cubics_solve_optimize_batch  fd::lns_optimize's neighbourhood loop  src/search.cpp:250-295
  *   cubics_propagate           fd::propagate_fixpoint   include/fd/propagation.hpp:114-118, src/propagation.cpp:516-532
  *                              fd::propagate_round      include/fd/propagation.hpp:102-104 (max_rounds = 1)
  *   cubics_removals            fd::run_batch / fd::propagate_one / fd::prop_*
@@ -195,6 +196,18 @@ void cubics_solutions_free(cubics_solutions* s);
 /* best_values (n_vars entries, may be NULL) receives the optimal / last incumbent. */
 int cubics_solve_optimize(const cubics_model* m, const cubics_search_config* cfg,
                           int64_t* best_values, cubics_result* out);
+
+/* Many independent branch-and-bound searches of one model in ONE device launch (one thread block
+ * per problem, the reference's node order in each): the neighbourhoods of one fd::lns_optimize
+ * iteration (src/search.cpp:250-295, neighborhood_model :207-217, Dfs::set_initial_bound :282).
+ * Problem i starts from the domains words + i * W (desc packing of this model, W = its total
+ * 64-bit word count) and, when has_bounds == NULL ? bounds != NULL : has_bounds[i], the strict
+ * initial bound bounds[i]; cfg->node_limit applies to each problem. results[i] receives problem
+ * i's stats, complete, has_solution and objective (device_ms / transfers are the whole launch's);
+ * best_values (count * n_vars, may be NULL) its last incumbent. */
+int cubics_solve_optimize_batch(const cubics_model* m, const cubics_search_config* cfg, int32_t count,
+                                const uint64_t* words, const int64_t* bounds, const int32_t* has_bounds,
+                                int64_t* best_values, cubics_result* results);
 
 /* One rank's share of a multi-GPU search: the search tree is expanded
  * deterministically to a frontier of open subtrees; this call searches every subtree t with

@@ -110,7 +110,7 @@ EXPORTED = [
     "cubics_model_create", "cubics_model_parse", "cubics_model_free", "cubics_model_describe",
     "cubics_model_var_name", "cubics_model_validate", "cubics_search_config_init",
     "cubics_solve_satisfy", "cubics_enumerate", "cubics_solutions_free", "cubics_solve_optimize",
-    "cubics_solve_shard", "cubics_propagate",
+    "cubics_solve_optimize_batch", "cubics_solve_shard", "cubics_propagate",
     "cubics_removals", "cubics_last_error", "cubics_build_info", "cubics_device_count", "cubics_warmup",
 ]
 
@@ -140,6 +140,9 @@ def declare(lib):
     lib.cubics_solutions_free.restype = None
     lib.cubics_solve_optimize.argtypes = [C.c_void_p, P(SearchConfig), P(C.c_int64), P(Result)]
     lib.cubics_solve_optimize.restype = C.c_int
+    lib.cubics_solve_optimize_batch.argtypes = [C.c_void_p, P(SearchConfig), C.c_int32, P(C.c_uint64), P(C.c_int64),
+                                                P(C.c_int32), P(C.c_int64), P(Result)]
+    lib.cubics_solve_optimize_batch.restype = C.c_int
     lib.cubics_solve_shard.argtypes = [C.c_void_p, P(SearchConfig), C.c_int32, C.c_int32, KEYED_SOLUTION_CB,
                                        C.c_void_p, P(Result)]
     lib.cubics_solve_shard.restype = C.c_int

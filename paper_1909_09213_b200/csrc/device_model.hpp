@@ -160,6 +160,15 @@ struct SearchParams {
     unsigned* grid_or;     // [3]
     unsigned* grid_min;    // [3]
     uint32_t* grid_chg;    // [2 * ceil(n/32)]
+    // batch mode (parity engine): block c runs an independent search from its own initial domains
+    // and bound (LNS neighbourhoods, cubics_solve_optimize_batch)
+    int32_t batch;             // 0 off, else number of problems (= blocks)
+    const uint32_t* batch_dom; // [batch][NWP]
+    const int64_t* batch_bound;   // [batch] initial bounds
+    const int32_t* batch_has_bound;
+    uint64_t* batch_stats;     // [batch][4] nodes, failures, rounds, solutions
+    int32_t* batch_flags;      // [batch] bit0 limit hit, bit1 has incumbent
+    uint16_t* batch_inc;       // [batch][n] last incumbent (bit indices)
     int32_t first_mode;
     int64_t seg_cap;
     uint32_t* seg_key;     // [seg_cap][KW]

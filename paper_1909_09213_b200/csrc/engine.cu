@@ -506,6 +506,20 @@ struct ShardIO {
     const std::vector<int32_t>* seeds = nullptr; // seeded run: task indices of this shard
 };
 
+// Batched B&B (cubics_solve_optimize_batch): problem i = block i, reference node order.
+struct BatchIO {
+    int count = 0;
+    const uint64_t* words = nullptr; // [count][model words] desc packing
+    std::vector<uint32_t> dom;      // [count][NWP] device layout (filled by run_search)
+    std::vector<int64_t> bound;     // [count]
+    std::vector<int32_t> has_bound; // [count]
+    bool any_empty = false;
+    // out
+    std::vector<uint64_t> stats;    // [count][4]
+    std::vector<int32_t> flags;     // [count] bit0 limit hit, bit1 incumbent
+    std::vector<uint16_t> inc;      // [count][n]
+};
+
 __global__ void gather_tasks(const uint32_t* src, const int32_t* idx, int n, size_t os, uint32_t* dst) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < (size_t)n * os; i += (size_t)gridDim.x * blockDim.x)
         dst[i] = src[(size_t)idx[i / os] * os + i % os];
@@ -513,7 +527,7 @@ __global__ void gather_tasks(const uint32_t* src, const int32_t* idx, int n, siz
 
 // One device search: upload, launch, download.
 void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine, bool record, uint64_t sol_cap,
-                RunOut& out, bool want_keys = false, ShardIO* shard = nullptr) {
+                RunOut& out, bool want_keys = false, ShardIO* shard = nullptr, BatchIO* batch = nullptr) {
     const int dev = current_device(cfg.device);
     std::lock_guard<std::recursive_mutex> lock(g_dev_mu[dev]);
     Prepared P;
@@ -522,7 +536,22 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
     // AUTO: a large model searched with reference node order gets the grid-wide context
     // (measured on B200: tables weigh ~4 RelBins; rbcsp_10000 / rcsp_100000 gain 1.7x / 6.8x,
     // rcsp_10000 with 20k cheap != constraints is faster in one block)
-    if (engine == CUBICS_ENGINE_PARITY && cfg.engine == CUBICS_ENGINE_AUTO && !shard &&
+    if (batch) {
+        engine = CUBICS_ENGINE_PARITY;
+        record = false;
+        const size_t nw64 = hm.words.size();
+        batch->dom.assign(P.NWP * batch->count, 0);
+        for (int i = 0; i < batch->count; ++i) {
+            uint32_t* dst = batch->dom.data() + P.NWP * i;
+            for (int v = 0; v < n; ++v) {
+                words_to_u32(hm, v, batch->words + nw64 * i, dst, P.W);
+                int sz = 0;
+                for (int w = 0; w < P.W; ++w) sz += __builtin_popcount(dst[(size_t)v * P.W + w]);
+                if (!sz) batch->any_empty = true;
+            }
+        }
+    }
+    if (engine == CUBICS_ENGINE_PARITY && cfg.engine == CUBICS_ENGINE_AUTO && !shard && !batch &&
         ((long)P.nr + P.nl + 4L * (P.ntb + P.ntn) >= 40000 || P.n >= 50000))
         engine = CUBICS_ENGINE_GRID;
     const bool grid = engine == CUBICS_ENGINE_GRID;
@@ -558,7 +587,7 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
     }
     // propagator features the model needs: the lean kernel instantiations skip the rest
     const int feat = (P.nl ? 1 : 0) | (P.ntb + P.ntn ? 2 : 0) | (P.big_words ? 4 : 0) | (first_mode ? 8 : 0);
-    int n_ctx = 1;
+    int n_ctx = batch ? batch->count : 1;
     if (parallel) {
         int per_sm = 0;
 #define OCC(w) occupancy_search<w>(feat, block, L.total, &per_sm)
@@ -624,6 +653,13 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
     const size_t a_segk = take(sizeof(uint32_t) * KW * seg_cap);
     const size_t a_segs = take(sizeof(uint64_t) * 3 * seg_cap);
     const size_t a_sseg = take(first_mode ? sizeof(int32_t) * sol_cap : 0);
+    const int nb = batch ? batch->count : 0;
+    const size_t a_bdom = take(sizeof(uint32_t) * NWP * nb);
+    const size_t a_bbound = take(sizeof(int64_t) * nb);
+    const size_t a_bhas = take(sizeof(int32_t) * nb);
+    const size_t a_bstats = take(sizeof(uint64_t) * 4 * nb);
+    const size_t a_bflags = take(sizeof(int32_t) * nb);
+    const size_t a_binc = take(sizeof(uint16_t) * n * nb);
     uint8_t* base = device_arena(dev, off);
 
     cudaStream_t st = g_dev[dev].stream;
@@ -662,6 +698,13 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
             out.launches += 1;
         }
 
+        if (batch) {
+            CU(cudaMemcpyAsync(base + a_bdom, batch->dom.data(), sizeof(uint32_t) * NWP * nb, cudaMemcpyHostToDevice, st));
+            CU(cudaMemcpyAsync(base + a_bbound, batch->bound.data(), sizeof(int64_t) * nb, cudaMemcpyHostToDevice, st));
+            CU(cudaMemcpyAsync(base + a_bhas, batch->has_bound.data(), sizeof(int32_t) * nb, cudaMemcpyHostToDevice, st));
+            CU(cudaMemsetAsync(base + a_bflags, 0, sizeof(int32_t) * nb, st));
+            out.h2d += (sizeof(uint32_t) * NWP + sizeof(int64_t) + sizeof(int32_t)) * nb;
+        }
         SearchParams S{};
         S.M = P.bind(base + a_blob);
         S.M.goal = hm.goal;
@@ -669,8 +712,8 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
         S.mode = parallel ? MODE_PARALLEL : MODE_PARITY;
         S.var_heuristic = cfg.var_heuristic == CUBICS_FIRST_FAIL ? 1 : 0;
         S.alldiff = cfg.alldiff == CUBICS_FORWARD_CHECKING ? 0 : 1;
-        S.exact_wipe = P.has_empty ? 1 : 0;
-        S.max_solutions = cfg.max_solutions;
+        S.exact_wipe = P.has_empty || (batch && batch->any_empty) ? 1 : 0;
+        S.max_solutions = batch ? std::numeric_limits<uint64_t>::max() : cfg.max_solutions;
         S.node_limit = cfg.node_limit;
         S.n_ctx = n_ctx;
         S.frame_cap = frame_cap;
@@ -714,6 +757,13 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
         S.seg_key = reinterpret_cast<uint32_t*>(base + a_segk);
         S.seg_stats = reinterpret_cast<uint64_t*>(base + a_segs);
         S.sol_seg = reinterpret_cast<int32_t*>(base + a_sseg);
+        S.batch = nb;
+        S.batch_dom = reinterpret_cast<const uint32_t*>(base + a_bdom);
+        S.batch_bound = reinterpret_cast<const int64_t*>(base + a_bbound);
+        S.batch_has_bound = reinterpret_cast<const int32_t*>(base + a_bhas);
+        S.batch_stats = reinterpret_cast<uint64_t*>(base + a_bstats);
+        S.batch_flags = reinterpret_cast<int32_t*>(base + a_bflags);
+        S.batch_inc = reinterpret_cast<uint16_t*>(base + a_binc);
 
         CU(cudaEventRecord(e0, st));
         if (grid) {
@@ -826,6 +876,16 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
                                    sizeof(uint16_t) * n, cudaMemcpyDeviceToHost, st));
                 out.d2h += sizeof(uint16_t) * n;
             }
+        }
+        if (batch) {
+            batch->stats.resize((size_t)4 * nb);
+            batch->flags.resize(nb);
+            batch->inc.resize((size_t)n * nb);
+            CU(cudaMemcpyAsync(batch->stats.data(), base + a_bstats, sizeof(uint64_t) * 4 * nb, cudaMemcpyDeviceToHost, st));
+            CU(cudaMemcpyAsync(batch->flags.data(), base + a_bflags, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, st));
+            if (n)
+                CU(cudaMemcpyAsync(batch->inc.data(), base + a_binc, sizeof(uint16_t) * n * nb, cudaMemcpyDeviceToHost, st));
+            out.d2h += (sizeof(uint64_t) * 4 + sizeof(int32_t) + sizeof(uint16_t) * n) * nb;
         }
         if (shard) shard->n_tasks = (uint64_t)out.ws.n_tasks;
         if (parallel && hm.goal != CUBICS_SATISFY && n) {
@@ -1083,6 +1143,50 @@ extern "C" int cubics_solve_optimize(const cubics_model* h, const cubics_search_
                 for (int v = 0; v < n; ++v) best_values[v] = m.offset[v] + best[v];
         }
         out->total_ms = now_ms() - t0;
+        return CUBICS_OK;
+    });
+}
+
+extern "C" int cubics_solve_optimize_batch(const cubics_model* h, const cubics_search_config* cfg, int32_t count,
+                                           const uint64_t* words, const int64_t* bounds, const int32_t* has_bounds,
+                                           int64_t* best_values, cubics_result* results) {
+    if (!h || !cfg || count < 0 || (count > 0 && (!words || !results))) return CUBICS_E_INVALID;
+    return guarded([&] {
+        const double t0 = now_ms();
+        const HostModel& m = h->m;
+        if (m.goal == CUBICS_SATISFY) throw StatusError{CUBICS_E_NO_OBJECTIVE, "solve_optimize requires a minimize or maximize goal"};
+        if (count == 0) return CUBICS_OK;
+        std::memset(results, 0, sizeof(cubics_result) * count);
+        const int n = m.n_vars();
+        BatchIO b;
+        b.count = count;
+        b.words = words;
+        b.bound.assign(count, 0);
+        b.has_bound.assign(count, 0);
+        for (int i = 0; i < count; ++i) {
+            b.has_bound[i] = has_bounds ? has_bounds[i] != 0 : (bounds != nullptr);
+            b.bound[i] = bounds ? bounds[i] : 0;
+        }
+        RunOut r;
+        run_search(m, *cfg, CUBICS_ENGINE_PARITY, false, 0, r, false, nullptr, &b);
+        for (int i = 0; i < count; ++i) {
+            cubics_result& o = results[i];
+            fill_result(r, &o);
+            o.stats.nodes = b.stats[4 * i + 0];
+            o.stats.failures = b.stats[4 * i + 1];
+            o.stats.rounds = b.stats[4 * i + 2];
+            o.stats.solutions = b.stats[4 * i + 3];
+            o.complete = !(b.flags[i] & 1);
+            o.has_solution = (b.flags[i] & 2) != 0 || (n == 0 && o.stats.solutions > 0);
+            if (b.flags[i] & 2) {
+                const uint16_t* inc = b.inc.data() + (size_t)n * i;
+                o.objective = m.offset[m.goal_var] + inc[m.goal_var];
+                if (best_values)
+                    for (int v = 0; v < n; ++v) best_values[(size_t)n * i + v] = m.offset[v] + inc[v];
+            }
+            o.contexts = count;
+            o.total_ms = now_ms() - t0;
+        }
         return CUBICS_OK;
     });
 }

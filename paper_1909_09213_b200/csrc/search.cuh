@@ -155,8 +155,9 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
 
     unsigned long long nodes = 0, failures = 0, rounds = 0, sols = 0;
     int sp = 0, base = 0, depth = 0;
-    bool has_bound = P.has_init_bound != 0;
-    long long bound = P.init_bound;
+    const bool batch = P.batch != 0;
+    bool has_bound = batch ? P.batch_has_bound[ctx] != 0 : P.has_init_bound != 0;
+    long long bound = batch ? P.batch_bound[ctx] : P.init_bound;
     bool has_first = false;
     const bool optimizing = M.goal != 0, minimizing = M.goal == 1;
     const int obj = M.goal_var;
@@ -275,7 +276,7 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
 
     bool have_work;
     if (!parallel || (ctx == 0 && !P.n_seed)) {
-        copy4(dom, M.init_dom, NWP, tid, T);
+        copy4(dom, batch ? P.batch_dom + (size_t)ctx * NWP : M.init_dom, NWP, tid, T);
         have_work = true;
     } else {
         have_work = get_work();
@@ -307,8 +308,12 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
         ++nodes;
         if (P.node_limit && nodes > P.node_limit) {
             if (tid == 0) {
-                ws->limit_hit = 1;
-                ws->hot.stop = 1;
+                if (batch) { // per-problem flag: the other problems keep searching
+                    P.batch_flags[ctx] |= 1;
+                } else {
+                    ws->limit_hit = 1;
+                    ws->hot.stop = 1;
+                }
             }
             break;
         }
@@ -437,6 +442,11 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
                     const long long val = M.off[obj] + dom_first<W>(dom + (size_t)obj * W);
                     has_bound = true;
                     bound = val;
+                    if (batch) {
+                        for (int v = tid; v < n; v += T)
+                            P.batch_inc[(size_t)ctx * n + v] = (uint16_t)dom_first<W>(dom + (size_t)v * W);
+                        if (tid == 0) P.batch_flags[ctx] |= 2;
+                    }
                     if (parallel && tid == 0) {
                         spin_lock(&ws->inc_lock);
                         volatile long long* gb = reinterpret_cast<volatile long long*>(&ws->bound);
@@ -574,6 +584,12 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
         atomicAdd((unsigned long long*)&ws->idle_cycles, (unsigned long long)idle_cyc);
         atomicAdd((unsigned long long*)&ws->steals, (unsigned long long)steals);
         atomicAdd((unsigned long long*)&ws->donations, (unsigned long long)donations);
+        if (batch) {
+            P.batch_stats[(size_t)ctx * 4 + 0] = nodes;
+            P.batch_stats[(size_t)ctx * 4 + 1] = failures;
+            P.batch_stats[(size_t)ctx * 4 + 2] = rounds;
+            P.batch_stats[(size_t)ctx * 4 + 3] = sols;
+        }
         atomicAdd((unsigned long long*)&ws->stats[0], nodes);
         atomicAdd((unsigned long long*)&ws->stats[1], failures);
         atomicAdd((unsigned long long*)&ws->stats[2], rounds);

@@ -270,10 +270,34 @@ def phase_transition_tightness(n: int, d: int, m: int) -> float:
     return 1.0 - d ** (-n / m)
 
 
+def assignment(n: int, seed: int, forbid: int | None = None) -> str:
+    """Weighted assignment: a permutation x of 1..n minimising sum c_i * x_i under random
+    forbidden offsets x_i != x_j + k. An optimisation model whose LNS neighbourhoods (free
+    variables re-permuted under the incumbent's bound) are real searches, unlike golomb's."""
+    rnd = random.Random(seed)
+    c = [rnd.randint(1, 9) for _ in range(n)]
+    lo = sum(a * b for a, b in zip(sorted(c), range(n, 0, -1)))
+    hi = sum(a * b for a, b in zip(sorted(c), range(1, n + 1)))
+    hi = min(hi, lo + 1023)
+    out = [f"var x{i} in 1..{n};" for i in range(1, n + 1)]
+    out.append(f"var cost in {lo}..{hi};")
+    out.append("constraint alldifferent(" + ", ".join(f"x{i}" for i in range(1, n + 1)) + ");")
+    for _ in range(forbid if forbid is not None else 2 * n):
+        i, j = rnd.sample(range(1, n + 1), 2)
+        k = rnd.randint(1, 3)
+        out.append(f"constraint x{i} != x{j} + {k};")
+    out.append("constraint " + " + ".join(f"{c[i - 1]}*x{i}" for i in range(1, n + 1)) + " - cost = 0;")
+    out.append("solve minimize cost;")
+    return "\n".join(out) + "\n"
+
+
 def named_instance(name: str) -> str:
     """The model text of a named benchmark instance (nqN, golombM, magicN, rcsp_N)."""
     if name.startswith("nq"):
         return gen_nqueens(int(name[2:]))
+    if name.startswith("assign"):  # assign<n> or assign<n>_<seed>
+        a, _, b = name[len("assign"):].partition("_")
+        return assignment(int(a), int(b or 1))
     if name.startswith("golomb"):
         m = int(name[len("golomb"):])
         return golomb(m, m * m)

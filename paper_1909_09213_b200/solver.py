@@ -8,6 +8,8 @@ the reference's own tests:
     fd::solve_satisfy        -> solve_satisfy(model, cfg, cb)   (search.hpp:62)
     fd::enumerate_solutions  -> enumerate_solutions(model, cfg) (search.hpp:65)
     fd::solve_optimize       -> solve_optimize(model, cfg)      (search.hpp:77)
+    fd::lns_optimize         -> lns_optimize(model, LnsConfig)  (search.hpp:92; neighbourhoods
+                                batched into one launch by optimize_batch)
     fd::propagate_fixpoint   -> propagate_fixpoint(model, doms) (propagation.hpp:114)
     fd::propagate_round      -> propagate_round(model, doms)    (propagation.hpp:102)
     fd::run_batch / prop_*   -> removals(model, doms, cons)     (propagation.hpp:78-89)
@@ -305,7 +307,9 @@ class Model:
         return model_from_desc(arr["desc"])
 
     def with_domains(self, domains):
-        arr = build_desc(self.offsets, self.widths, domains, self.con_kind, self.con_op, self.con_value,
+        """A copy of this model with new initial domains (each keeps its own offset and width,
+        as fd::Model::domains does, e.g. the Domain(val, val) of neighborhood_model)."""
+        arr = build_desc([d.offset for d in domains], [d.width for d in domains], domains, self.con_kind, self.con_op, self.con_value,
                          self.con_start, self.term_var, self.term_coeff, self.goal, self.goal_var,
                          self.table_start, self.table_data)
         return model_from_desc(arr["desc"])
@@ -439,6 +443,125 @@ def solve_optimize(model: Model, cfg: SearchConfig | None = None) -> OptimizeRes
     if res.has_solution:
         sol = Solution([best[i] for i in range(model.n_vars)], res.objective)
     return OptimizeResult(sol, bool(res.complete), _stats(res), res.engine, res.contexts, res.device_ms, res.total_ms)
+
+
+def optimize_batch(model: Model, domain_words, bounds=None, cfg: SearchConfig | None = None):
+    """cubics_solve_optimize_batch: one branch-and-bound search per row of ``domain_words``
+    (uint64 [count, model words], desc packing), all in one device launch. ``bounds`` (None or a
+    sequence of int / None) gives each problem's strict initial bound. Returns [OptimizeResult]."""
+    import numpy as np
+
+    cfg = cfg or SearchConfig()
+    nw = max(1, model.word_start[-1])
+    words = np.ascontiguousarray(np.asarray(domain_words, dtype=np.uint64).reshape(-1, nw))
+    count = words.shape[0]
+    if count == 0:
+        return []
+    b = np.zeros(count, dtype=np.int64)
+    hb = np.zeros(count, dtype=np.int32)
+    if bounds is not None:
+        for i, x in enumerate(bounds):
+            if x is not None:
+                b[i], hb[i] = x, 1
+    n = model.n_vars
+    best = np.zeros((count, max(1, n)), dtype=np.int64)
+    res = (A.Result * count)()
+    c = cfg.to_c()
+    P = C.POINTER
+    _check(lib().cubics_solve_optimize_batch(
+        model.handle, C.byref(c), count, words.ctypes.data_as(P(C.c_uint64)), b.ctypes.data_as(P(C.c_int64)),
+        hb.ctypes.data_as(P(C.c_int32)), best.ctypes.data_as(P(C.c_int64)), res), "solve_optimize_batch")
+    out = []
+    for i in range(count):
+        r = res[i]
+        sol = Solution(best[i, :n].tolist(), r.objective) if r.has_solution else None
+        out.append(OptimizeResult(sol, bool(r.complete), _stats(r), r.engine, r.contexts, r.device_ms, r.total_ms))
+    return out
+
+
+@dataclass
+class LnsConfig:
+    """fd::LnsConfig (search.hpp:29-37)."""
+    destroy_rate: float = 0.3
+    iterations: int = 10
+    neighborhoods: int = 1
+    seed: int = 0
+    per_iteration_node_limit: int = 0
+    thread_count: int = 1
+    alldiff: int = A.ARC_CONSISTENT
+
+
+@dataclass
+class LnsResult:
+    """fd::LnsResult (search.hpp:79-84): best, summed stats, per-iteration trajectory."""
+    best: Solution | None
+    stats: SearchStats
+    trajectory: list
+    initial_complete: bool
+    device_ms: float = 0.0
+
+
+def lns_optimize(model: Model, cfg: LnsConfig | None = None) -> LnsResult:
+    """fd::lns_optimize (search.cpp:225-314): first solution, then ``iterations`` rounds of
+    ``neighborhoods`` destroy-and-repair searches against the frozen incumbent. Each iteration's
+    neighbourhoods run as ONE batched device launch (optimize_batch); destroy sets follow
+    Rng::derive(seed, nb, iter) with the reference's partial Fisher-Yates, merge is lowest-index-wins."""
+    import math
+
+    import numpy as np
+
+    from .models import Rng
+
+    cfg = cfg or LnsConfig()
+    if model.goal == A.SATISFY:
+        raise LogicError("lns_optimize requires a minimize or maximize goal")
+    minimizing = model.goal == A.MINIMIZE
+    found = []
+    first = solve_satisfy(model, SearchConfig(max_solutions=1, thread_count=cfg.thread_count, alldiff=cfg.alldiff),
+                          lambda s: (found.append(s), False)[1])
+    stats = SearchStats(*first.stats.as_tuple())
+    best = None
+    if found:
+        best = Solution(found[0].values, found[0].values[model.goal_var])
+    res = LnsResult(None, stats, [], first.complete or best is not None)
+    if best is None:
+        return res
+    n = model.n_vars
+    destroy = min(n, max(1, math.ceil(cfg.destroy_rate * n)))
+    nw = max(1, model.word_start[-1])
+    base = np.zeros(nw, dtype=np.uint64)
+    base_words = model.words_of(model.domains)
+    base[:] = np.ctypeslib.as_array(base_words)[:nw]
+    scfg = SearchConfig(alldiff=cfg.alldiff, node_limit=cfg.per_iteration_node_limit, engine=A.ENGINE_PARITY)
+    for it in range(cfg.iterations):
+        inc = best
+        words = np.tile(base, (cfg.neighborhoods, 1))
+        for nb in range(cfg.neighborhoods):
+            rng = Rng.derive(cfg.seed, nb, it)
+            ids = list(range(n))
+            destroyed = [False] * n
+            for i in range(destroy):
+                j = i + rng.below(n - i)
+                ids[i], ids[j] = ids[j], ids[i]
+                destroyed[ids[i]] = True
+            for v in range(n):
+                if not destroyed[v]:  # neighborhood_model (search.cpp:207-217): fixed to the incumbent
+                    ws, we = model.word_start[v], model.word_start[v + 1]
+                    words[nb, ws:we] = 0
+                    bit = inc.values[v] - model.offsets[v]
+                    words[nb, ws + bit // 64] = np.uint64(1 << (bit % 64))
+        out = optimize_batch(model, words, [inc.objective] * cfg.neighborhoods, scfg)
+        res.device_ms += out[0].device_ms  # one launch for the whole iteration
+        for r in out:
+            stats.nodes += r.stats.nodes
+            stats.failures += r.stats.failures
+            stats.rounds += r.stats.rounds
+            if r.best is not None and (r.best.objective < best.objective if minimizing
+                                       else r.best.objective > best.objective):
+                best = r.best
+        res.trajectory.append(best.objective)
+    res.best = best
+    return res
 
 
 def solve_shard(model: Model, cfg: SearchConfig, shard_index: int, shard_count: int, cb=None):

@@ -25,6 +25,12 @@ CASES = [
     ["solve", f"{M}/golomb7.fd", "--stats"],
     ["solve", f"{M}/golomb6.fd", "--lns", "--iters", "3", "--neighborhoods", "2", "--seed", "3", "--stats"],
     ["solve", f"{M}/golomb6.fd", "--lns", "--iters", "2", "--destroy", "0.5", "--node-limit", "40", "--json"],
+    ["solve", f"{M}/golomb7.fd", "--lns", "--iters", "4", "--neighborhoods", "16", "--seed", "11", "--stats"],
+    ["solve", f"{M}/golomb7.fd", "--lns", "--iters", "3", "--neighborhoods", "9", "--destroy", "0.6",
+     "--node-limit", "150", "--json"],
+    ["solve", f"{M}/assign20.fd", "--lns", "--iters", "5", "--neighborhoods", "32", "--destroy", "0.4", "--stats"],
+    ["solve", f"{M}/assign30.fd", "--lns", "--iters", "3", "--neighborhoods", "64", "--destroy", "0.35",
+     "--node-limit", "1000", "--seed", "4", "--json", "--stats"],
     ["solve", f"{M}/magic3.fd", "--all", "--json"],
     ["solve", f"{M}/magic4.fd", "--stats"],
     ["gen-nqueens", "6"],
