@@ -204,6 +204,19 @@ def run_extras(S, A, device):
             out[name] = rec
         except Exception as e:  # noqa: BLE001 - reported, never hidden
             out[name] = {"what": what, "error": repr(e)}
+    # LNS with every neighbourhood of an iteration in ONE batched launch
+    # (cubics_solve_optimize_batch); reference-identical trajectory (tests/test_gpu_lns.py)
+    try:
+        from paper_1909_09213_b200 import models as MD
+        m = S.parse_model(MD.named_instance("assign30"))
+        lc = S.LnsConfig(destroy_rate=0.35, iterations=5, neighborhoods=592, seed=1, per_iteration_node_limit=1000)
+        r = S.lns_optimize(m, lc)
+        out["lns_assign30"] = {"what": "LNS 5 iterations x 592 neighbourhoods, node limit 1000, one launch per iteration",
+                               "device_ms": round(r.device_ms, 3), "nodes": r.stats.nodes,
+                               "nodes_per_s": r.stats.nodes / (r.device_ms / 1e3) if r.device_ms else None,
+                               "objective": r.best.objective if r.best else None, "trajectory": r.trajectory}
+    except Exception as e:  # noqa: BLE001
+        out["lns_assign30"] = {"error": repr(e)}
     return out
 
 

@@ -33,6 +33,7 @@ struct DevModel {
     int32_t W;           // u32 words per domain (power of two)
     const int64_t* off;  // [n]
     const uint32_t* init_dom; // [n*W]
+    const int32_t* vw;        // [n] words a variable's own width needs (<= W; bits beyond are 0)
     int32_t nr;
     const RelBinRec* rb;         // generic records first, then the var-form != records
     int32_t nr_gen;              // records [0, nr_gen) are not var-form !=
@@ -44,11 +45,12 @@ struct DevModel {
     const int64_t* lin_bound; // [nl]
     const int32_t* lin_var;
     const int64_t* lin_coeff;
+    int32_t lin_g;            // lanes per linear constraint (1: one thread each; 2..32: lane groups)
     int32_t na;
     const int32_t* ad_start;  // [na+1]
     const int32_t* ad_var;
     const int32_t* ad_shift;
-    const int32_t* ad_uw;        // [na] 0: fast warp path (<= 64 members, universe in W words);
+    const int32_t* ad_uw;        // [na] <= 0: fast warp path (<= 64 members), universe of -ad_uw words;
                                  //      > 0: generic path over a uw-word universe (big_words scratch)
     int32_t big_words;           // u32 words of per-warp scratch the generic path needs (0: none)
     // positive table constraints (extension, BASELINE config 5)

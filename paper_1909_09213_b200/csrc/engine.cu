@@ -111,11 +111,14 @@ struct Prepared {
     bool has_empty = false;
     uint64_t depth_bound = 0; // sum(|D| - 1): max binary-tree depth
     Blob blob;
+    size_t o_vw = 0;
+    bool mixed_width = false; // some variable needs <= W/4 words: per-variable word counts pay
     size_t o_off, o_dom, o_rb, o_ls, o_lo, o_lb, o_lv, o_lc, o_as, o_av, o_ash, o_nes, o_nee, o_auw;
     size_t o_tbxy, o_tboff, o_tbsup, o_tns, o_tnv, o_tnn, o_tno, o_tnd;
     int ntb = 0, ntn = 0;
     size_t big_words = 0;
     int nr_gen = 0;
+    int lin_g = 1;
     std::vector<int> kind_index; // constraint index -> kind-local index (rb | nr+lin | nr+nl+ad)
     std::vector<int64_t> offsets;
     DevModel bind(const uint8_t* base) const {
@@ -124,6 +127,7 @@ struct Prepared {
         M.W = W;
         M.off = reinterpret_cast<const int64_t*>(base + o_off);
         M.init_dom = reinterpret_cast<const uint32_t*>(base + o_dom);
+        M.vw = mixed_width ? reinterpret_cast<const int32_t*>(base + o_vw) : nullptr;
         M.nr = nr;
         M.rb = reinterpret_cast<const RelBinRec*>(base + o_rb);
         M.nr_gen = nr_gen;
@@ -135,6 +139,7 @@ struct Prepared {
         M.lin_bound = reinterpret_cast<const int64_t*>(base + o_lb);
         M.lin_var = reinterpret_cast<const int32_t*>(base + o_lv);
         M.lin_coeff = reinterpret_cast<const int64_t*>(base + o_lc);
+        M.lin_g = lin_g;
         M.na = na;
         M.ad_start = reinterpret_cast<const int32_t*>(base + o_as);
         M.ad_var = reinterpret_cast<const int32_t*>(base + o_av);
@@ -268,7 +273,7 @@ void prepare(const HostModel& m, const uint64_t* words, Prepared& P) {
             throw StatusError{CUBICS_E_UNSUPPORTED, "alldifferent value universe wider than 32768 values"};
         if (e - b <= kFastAllDiffMembers && span <= 32 * 32) {
             need = std::max(need, static_cast<int>(uwords));
-            auw.push_back(0);
+            auw.push_back(-static_cast<int32_t>(std::max(1L, uwords))); // fast path, universe words
         } else {
             auw.push_back(static_cast<int32_t>(uwords));
             big_words = std::max(big_words, dev::big_scratch_words(e - b, static_cast<int>(uwords)));
@@ -310,6 +315,13 @@ void prepare(const HostModel& m, const uint64_t* words, Prepared& P) {
     P.ntn = static_cast<int>(tn_nt.size());
     P.nr = static_cast<int>(rb.size());
     P.nl = static_cast<int>(lo.size());
+    // lanes per linear sum: one thread for short sums, else a lane group of pow2ceil(max terms)
+    // (<= 32; longer sums loop over 32-term chunks) scanning its terms in parallel
+    int max_terms = 0;
+    for (int c = 0; c < P.nl; ++c) max_terms = std::max(max_terms, ls[c + 1] - ls[c]);
+    P.lin_g = 1;
+    if (max_terms > 4)
+        while (P.lin_g < max_terms && P.lin_g < 32) P.lin_g *= 2;
     P.na = static_cast<int>(as.size()) - 1;
     P.total_members = static_cast<int>(av.size());
     std::vector<uint32_t> dom(P.NWP, 0);
@@ -341,6 +353,14 @@ void prepare(const HostModel& m, const uint64_t* words, Prepared& P) {
     P.offsets = m.offset;
     P.o_off = P.blob.add(m.offset.data(), m.offset.size());
     P.o_dom = P.blob.add(dom.data(), dom.size());
+    {
+        std::vector<int32_t> vw(std::max(n, 1), 1);
+        for (int v = 0; v < n; ++v) {
+            vw[v] = std::max(1, std::min(W, (m.width[v] + 31) / 32));
+            if (W > 2 && vw[v] * 4 <= W) P.mixed_width = true;
+        }
+        P.o_vw = P.blob.add(vw.data(), vw.size());
+    }
     P.o_rb = P.blob.add(rb.data(), rb.size());
     P.o_ls = P.blob.add(ls.data(), ls.size());
     P.o_lo = P.blob.add(lo.data(), lo.size());
@@ -576,7 +596,7 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
                                 ? 128
                                 : (P.W >= 8 || P.nr + P.nl + P.ntb + P.ntn > 256 ? 64 : 32))
                          : parity_block(P);
-    block = std::min(std::max(block, 32), 1024);
+    block = std::min(std::max(block, 32), batch ? 512 : 1024);
     const int nw = block / 32;
     bool in_smem = !grid; // the grid context keeps its domains in L2/HBM
     dev::SmemLayout L = dev::smem_layout(P.W, n, P.total_members, nw, KW, in_smem, P.na);

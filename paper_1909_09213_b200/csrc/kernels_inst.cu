@@ -18,7 +18,7 @@ cudaError_t grant_smem(K k, size_t smem, size_t& granted) {
     return e;
 }
 size_t g_search_smem = 48 * 1024, g_prop_smem = 48 * 1024, g_grid_smem = 48 * 1024;
-size_t g_search_smem0 = 48 * 1024, g_search_smem1 = 48 * 1024;
+size_t g_search_smem0 = 48 * 1024, g_search_smem1 = 48 * 1024, g_parity_smem = 48 * 1024;
 } // namespace
 
 // lean instantiations for narrow domains: {RelBin + small alldiff}, {+ linear}; everything else
@@ -40,6 +40,14 @@ cudaError_t launch_search<CUBICS_W>(const SearchParams& P, int feat, int grid, i
                                     cudaStream_t st) {
     // the generic block kernel also runs one-warp contexts: a __syncwarp-specialised variant
     // measured slower on B200 (19.3 vs 14.0 ms on nq14; register spills at the 64-register cap)
+    if (P.mode == MODE_PARITY && block <= 512) {
+        auto k = dev::search_kernel_parity<CUBICS_W>;
+        cudaError_t e = grant_smem(k, smem, g_parity_smem);
+        if (e != cudaSuccess) return e;
+        k<<<grid, block, smem, st>>>(P);
+        return cudaGetLastError();
+    }
+    if (P.batch) return cudaErrorInvalidConfiguration; // batched B&B runs in the parity kernel only
     SearchFn k = pick_search(feat);
     cudaError_t e = grant_smem(k, smem, feat == 0 ? g_search_smem0 : (feat == dev::F_LINEAR ? g_search_smem1 : g_search_smem));
     if (e != cudaSuccess) return e;

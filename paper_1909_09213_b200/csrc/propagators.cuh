@@ -30,7 +30,9 @@ enum RoundStatus : int { R_CHANGED = 0, R_STABLE = 1, R_FAILED = 2, R_ERROR = 3 
 // Compile-time propagator features of a kernel instantiation: a model without linear sums,
 // tables or large alldifferents runs a kernel without that code (register pressure decides the
 // occupancy of one-warp search contexts).
-enum Feature : int { F_LINEAR = 1, F_TABLE = 2, F_BIGAD = 4, F_FIRST = 8, F_ALL = 15 };
+// F_PARITY marks a kernel that only runs the reference-order engines (parity block, batched
+// B&B, grid context): the parallel engine's work sharing compiles out of it.
+enum Feature : int { F_LINEAR = 1, F_TABLE = 2, F_BIGAD = 4, F_FIRST = 8, F_ALL = 15, F_PARITY = 16 };
 
 // ------------------------------------------------------------------ bitset helpers
 template <int W>
@@ -106,6 +108,57 @@ __device__ __forceinline__ void or_bit(uint32_t* rmv, const uint32_t* dv, int bi
     const int b = bit;
     uint32_t m = (1u << (b & 31)) & dv[b >> 5];
     if (m) atomicOr(rmv + (b >> 5), m);
+}
+
+// Runtime-width variants: a variable's bits live in its first vwords(v) <= W words (the rest
+// stay 0), so mixed-width models (e.g. a wide objective next to narrow decision variables) do
+// not pay W words per operation on every variable.
+template <int W>
+__device__ __forceinline__ int vwords(const DevModel& M, int v) {
+    if constexpr (W <= 2) return W;
+    else return M.vw ? M.vw[v] : W; // vw == null: no variable is much narrower than W
+}
+template <int W>
+__device__ __forceinline__ bool dom_empty_n(const uint32_t* d, int n) {
+    if (W <= 2 || n == W) return dom_empty<W>(d);
+    uint32_t o = 0;
+    for (int i = 0; i < n; ++i) o |= d[i];
+    return o == 0;
+}
+template <int W>
+__device__ __forceinline__ int dom_first_n(const uint32_t* d, int n) {
+    if (W <= 2 || n == W) return dom_first<W>(d);
+    for (int i = 0; i < n; ++i)
+        if (d[i]) return i * 32 + __ffs(d[i]) - 1;
+    return -1;
+}
+template <int W>
+__device__ __forceinline__ int dom_last_n(const uint32_t* d, int n) {
+    if (W <= 2 || n == W) return dom_last<W>(d);
+    for (int i = n - 1; i >= 0; --i)
+        if (d[i]) return i * 32 + 31 - __clz(d[i]);
+    return -1;
+}
+template <int W>
+__device__ __forceinline__ int dom_size_n(const uint32_t* d, int n) {
+    if (W <= 2 || n == W) return dom_size<W>(d);
+    int s = 0;
+    for (int i = 0; i < n; ++i) s += __popc(d[i]);
+    return s;
+}
+template <int W>
+__device__ __forceinline__ void or_range_n(uint32_t* rmv, const uint32_t* dv, long long lo, long long hi, int n) {
+    if (W <= 2 || n == W) {
+        or_range<W>(rmv, dv, lo, hi);
+    } else {
+        if (lo > hi) return;
+        const int w0 = lo < 0 ? 0 : (int)(lo >> 5);
+        const int w1 = (int)((hi >> 5) < (long long)(n - 1) ? (hi >> 5) : (long long)(n - 1));
+        for (int w = w0; w <= w1; ++w) {
+            const uint32_t m = range_word(w, lo, hi) & dv[w];
+            if (m) atomicOr(rmv + w, m);
+        }
+    }
 }
 
 __device__ __forceinline__ long long wrap_add(long long a, long long b) {
@@ -222,9 +275,10 @@ __device__ bool filter_le(const DevModel& M, int b, int e, long long sign, long 
     for (int t = b; t < e; ++t) { // :217-224
         const int v = M.lin_var[t];
         const uint32_t* d = dom + (size_t)v * W;
-        if (dom_empty<W>(d)) return true;
+        const int nv = vwords<W>(M, v);
+        if (dom_empty_n<W>(d, nv)) return true;
         const long long a = sign * M.lin_coeff[t];
-        const long long val = M.off[v] + (a > 0 ? dom_first<W>(d) : dom_last<W>(d));
+        const long long val = M.off[v] + (a > 0 ? dom_first_n<W>(d, nv) : dom_last_n<W>(d, nv));
         i128 tm = (i128)a * val;
         if (!fits64(tm)) return false;
         i128 s = (i128)total + tm;
@@ -234,21 +288,111 @@ __device__ bool filter_le(const DevModel& M, int b, int e, long long sign, long 
     for (int t = b; t < e; ++t) { // :225-235
         const int v = M.lin_var[t];
         const uint32_t* d = dom + (size_t)v * W;
+        const int nv = vwords<W>(M, v);
         const long long a = sign * M.lin_coeff[t];
         const long long offv = M.off[v];
-        const long long tm = a * (offv + (a > 0 ? dom_first<W>(d) : dom_last<W>(d)));
+        const long long tm = a * (offv + (a > 0 ? dom_first_n<W>(d, nv) : dom_last_n<W>(d, nv)));
         i128 rest = (i128)total + (i128)wrap_add(0, -tm); // checked_add(total, -term_min)
         if (!fits64(rest)) return false;
         const i128 budget = (i128)bound - rest;
         uint32_t* rv = rm + (size_t)v * W;
         if (a > 0) { // remove v > floor(budget / a)
             i128 thr = a == 1 ? budget : floor_div(budget, a);
-            or_range<W>(rv, d, clampbit(thr + 1 - offv, NB), NB);
+            or_range_n<W>(rv, d, clampbit(thr + 1 - offv, NB), NB, nv);
         } else {     // remove v < budget / a, i.e. v <= ceil(budget / a) - 1
             i128 thr = a == -1 ? -budget - 1 : ceil_div(budget, a) - 1;
-            or_range<W>(rv, d, -1, clampbit(thr - offv, NB));
+            or_range_n<W>(rv, d, -1, clampbit(thr - offv, NB), nv);
         }
     }
+    return true;
+}
+
+__device__ __forceinline__ i128 shfl_up_i128(unsigned mask, i128 v, int d, int width) {
+    const unsigned long long lo = __shfl_up_sync(mask, (unsigned long long)v, d, width);
+    const long long hi = __shfl_up_sync(mask, (long long)(v >> 64), d, width);
+    return (i128)(((unsigned __int128)(unsigned long long)hi << 64) | lo);
+}
+__device__ __forceinline__ i128 shfl_i128(unsigned mask, i128 v, int src, int width) {
+    const unsigned long long lo = __shfl_sync(mask, (unsigned long long)v, src, width);
+    const long long hi = __shfl_sync(mask, (long long)(v >> 64), src, width);
+    return (i128)(((unsigned __int128)(unsigned long long)hi << 64) | lo);
+}
+
+// filter_le by a group of G lanes (G = 2..32, a power of two; the whole warp calls it, each
+// group on its own constraint, gl = lane within the group). Terms are spread over the lanes; the
+// running total is an exact i128 segmented scan, so the first event in term order decides the
+// outcome exactly as the sequential loop does: an empty domain first -> no-op (true), an int64
+// overflow of a term or of a prefix sum first -> false. Pass 2 filters every term in parallel.
+// Returns false on overflow (the caller aborts the search, so partial removals do not matter).
+template <int W>
+__device__ bool filter_le_group(const DevModel& M, int b, int e, long long sign, long long bound,
+                                const uint32_t* dom, uint32_t* rm, int G, int gl, unsigned gmask) {
+    constexpr int NB = W * 32;
+    i128 carry = 0;
+    for (int base = b; base < e; base += G) { // pass 1 (:217-224)
+        const int t = base + gl;
+        i128 tm = 0;
+        int kind = 0; // 1 empty, 2 overflow
+        if (t < e) {
+            const int v = M.lin_var[t];
+            const uint32_t* d = dom + (size_t)v * W;
+            const int nv = vwords<W>(M, v);
+            if (dom_empty_n<W>(d, nv)) {
+                kind = 1;
+            } else {
+                const long long a = sign * M.lin_coeff[t];
+                tm = (i128)a * (M.off[v] + (a > 0 ? dom_first_n<W>(d, nv) : dom_last_n<W>(d, nv)));
+                if (!fits64(tm)) kind = 2;
+            }
+        }
+        i128 ps = kind ? (i128)0 : tm;
+        for (int o = 1; o < G; o <<= 1) {
+            const i128 y = shfl_up_i128(gmask, ps, o, G);
+            if (gl >= o) ps += y;
+        }
+        ps += carry;
+        if (!kind && t < e && !fits64(ps)) kind = 2;
+        const unsigned ev = __ballot_sync(gmask, kind != 0) & gmask;
+        if (ev) {
+            const int first = __ffs(ev) - 1; // lowest lane = earliest term
+            return __shfl_sync(gmask, kind, first & (G - 1), G) == 1;
+        }
+        carry = shfl_i128(gmask, ps, G - 1, G);
+    }
+    const long long total = (long long)carry;
+    bool ok = true;
+    for (int t = b + gl; t < e; t += G) { // pass 2 (:225-235)
+        const int v = M.lin_var[t];
+        const uint32_t* d = dom + (size_t)v * W;
+        const int nv = vwords<W>(M, v);
+        const long long a = sign * M.lin_coeff[t];
+        const long long offv = M.off[v];
+        const long long tm = a * (offv + (a > 0 ? dom_first_n<W>(d, nv) : dom_last_n<W>(d, nv)));
+        const i128 rest = (i128)total + (i128)wrap_add(0, -tm);
+        if (!fits64(rest)) {
+            ok = false;
+            continue;
+        }
+        const i128 budget = (i128)bound - rest;
+        uint32_t* rv = rm + (size_t)v * W;
+        if (a > 0) {
+            const i128 thr = a == 1 ? budget : floor_div(budget, a);
+            or_range_n<W>(rv, d, clampbit(thr + 1 - offv, NB), NB, nv);
+        } else {
+            const i128 thr = a == -1 ? -budget - 1 : ceil_div(budget, a) - 1;
+            or_range_n<W>(rv, d, -1, clampbit(thr - offv, NB), nv);
+        }
+    }
+    return !(__ballot_sync(gmask, !ok) & gmask);
+}
+
+template <int W>
+__device__ __forceinline__ bool prop_linear_group(const DevModel& M, int c, const uint32_t* dom, uint32_t* rm, int G,
+                                                  int gl, unsigned gmask) {
+    const int b = M.lin_start[c], e = M.lin_start[c + 1];
+    const long long bound = M.lin_bound[c];
+    if (!filter_le_group<W>(M, b, e, 1, bound, dom, rm, G, gl, gmask)) return false;
+    if (M.lin_op[c] == 1 && !filter_le_group<W>(M, b, e, -1, -bound, dom, rm, G, gl, gmask)) return false;
     return true;
 }
 
@@ -442,13 +586,13 @@ __device__ bool gac_augment(int r, const uint32_t (&D0)[W], const uint32_t (&D1)
 // exact_wipe we recompute the matching greedily in member order, which leaves the same first
 // member unmatched (transversal-matroid greedy basis), and wipe it.
 // TWO = false: <= 32 members, one per lane, 32-bit member sets; TWO = true: <= 64 members.
-template <int W, bool TWO>
+template <int W, int U, bool TWO>
 __device__ void prop_alldiff_gac(const DevModel& M, int a, const uint32_t* dom, uint32_t* rm, int16_t* mates,
                                  const WarpScratch& ws, int lane, int exact_wipe, uint32_t* post, int8_t* post_ok) {
     using MS = MemberSet<TWO>;
     const int b = M.ad_start[a], n = M.ad_start[a + 1] - b;
     const bool h0 = lane < n, h1 = TWO && lane + 32 < n;
-    uint32_t D0[W], D1[W];
+    uint32_t D0[U], D1[U]; // member domains in universe coordinates (U <= W words)
     int v0 = -1, v1 = -1, s0 = 0, s1 = 0;
     if (h0) {
         v0 = M.ad_var[b + lane];
@@ -459,32 +603,40 @@ __device__ void prop_alldiff_gac(const DevModel& M, int a, const uint32_t* dom, 
         s1 = M.ad_shift[b + lane + 32];
     }
 #pragma unroll
-    for (int w = 0; w < W; ++w) {
+    for (int w = 0; w < U; ++w) {
         D0[w] = h0 ? (s0 ? shifted_word<W>(dom + (size_t)v0 * W, w, s0) : dom[(size_t)v0 * W + w]) : 0u;
         D1[w] = h1 ? (s1 ? shifted_word<W>(dom + (size_t)v1 * W, w, s1) : dom[(size_t)v1 * W + w]) : 0u;
     }
     if (post) { // idempotence: the post-state of the last evaluation is GAC-consistent
         bool same = true;
+        if constexpr (U == W) { // variable coordinates
 #pragma unroll
-        for (int w = 0; w < W; ++w) {
-            if (h0) same &= dom[(size_t)v0 * W + w] == post[(size_t)lane * W + w];
-            if (h1) same &= dom[(size_t)v1 * W + w] == post[(size_t)(lane + 32) * W + w];
+            for (int w = 0; w < W; ++w) {
+                if (h0) same &= dom[(size_t)v0 * W + w] == post[(size_t)lane * W + w];
+                if (h1) same &= dom[(size_t)v1 * W + w] == post[(size_t)(lane + 32) * W + w];
+            }
+        } else { // universe coordinates (the shift is injective on member values)
+#pragma unroll
+            for (int w = 0; w < U; ++w) {
+                if (h0) same &= D0[w] == post[(size_t)lane * W + w];
+                if (h1) same &= D1[w] == post[(size_t)(lane + 32) * W + w];
+            }
         }
         if (__all_sync(FULL, same) && *post_ok) return;
     }
     int m0 = h0 ? mates[lane] : -1, m1 = h1 ? mates[lane + 32] : -1;
-    if (m0 >= 0 && !testbit_r<W>(D0, m0)) m0 = -1; // warm start: keep still-valid edges
-    if (m1 >= 0 && !testbit_r<W>(D1, m1)) m1 = -1;
-    uint32_t MV[W];
+    if (m0 >= 0 && !testbit_r<U>(D0, m0)) m0 = -1; // warm start: keep still-valid edges
+    if (m1 >= 0 && !testbit_r<U>(D1, m1)) m1 = -1;
+    uint32_t MV[U];
 #pragma unroll
-    for (int w = 0; w < W; ++w) MV[w] = __reduce_or_sync(FULL, bitword(m0, w) | bitword(m1, w));
+    for (int w = 0; w < U; ++w) MV[w] = __reduce_or_sync(FULL, bitword(m0, w) | bitword(m1, w));
 
     MS unm = ballot_m<TWO>(h0 && m0 < 0, h1 && m1 < 0);
     int fail = -1;
     while (unm) {
         const int r = ffs_m<TWO>(unm);
         unm &= unm - 1;
-        if (!gac_augment<W, TWO>(r, D0, D1, h0, h1, m0, m1, MV, lane)) {
+        if (!gac_augment<U, TWO>(r, D0, D1, h0, h1, m0, m1, MV, lane)) {
             fail = r;
             break;
         }
@@ -493,9 +645,9 @@ __device__ void prop_alldiff_gac(const DevModel& M, int a, const uint32_t* dom, 
         if (exact_wipe) { // greedy matching in member order: its first failure is Kuhn's
             m0 = m1 = -1;
 #pragma unroll
-            for (int w = 0; w < W; ++w) MV[w] = 0;
+            for (int w = 0; w < U; ++w) MV[w] = 0;
             for (int r = 0; r < n; ++r)
-                if (!gac_augment<W, TWO>(r, D0, D1, h0, h1, m0, m1, MV, lane)) {
+                if (!gac_augment<U, TWO>(r, D0, D1, h0, h1, m0, m1, MV, lane)) {
                     fail = r;
                     break;
                 }
@@ -524,11 +676,11 @@ __device__ void prop_alldiff_gac(const DevModel& M, int a, const uint32_t* dom, 
     }
     __syncwarp();
     // free values F = U & ~MV ; pred(k) = { m : mate(m) in D(k) }
-    uint32_t F[W];
+    uint32_t F[U];
     MS p0 = 0, p1 = 0;
     bool sd0 = false, sd1 = false;
 #pragma unroll
-    for (int w = 0; w < W; ++w) {
+    for (int w = 0; w < U; ++w) {
         F[w] = __reduce_or_sync(FULL, D0[w] | D1[w]) & ~MV[w];
         sd0 |= (D0[w] & F[w]) != 0;
         sd1 |= (D1[w] & F[w]) != 0;
@@ -547,7 +699,7 @@ __device__ void prop_alldiff_gac(const DevModel& M, int a, const uint32_t* dom, 
     }
     // Warshall: anc(k) = members that reach k. A singleton member has no in-edge (its only value
     // is its own mate), so it is never interior to a path: only non-singletons serve as pivots.
-    const MS pivots = ballot_m<TWO>(h0 && dom_size<W>(D0) > 1, h1 && dom_size<W>(D1) > 1);
+    const MS pivots = ballot_m<TWO>(h0 && dom_size<U>(D0) > 1, h1 && dom_size<U>(D1) > 1);
     for (MS q = pivots; q; q &= q - 1) {
         const int p = ffs_m<TWO>(q);
         const MS ap = __shfl_sync(FULL, (p >> 5) ? p1 : p0, p & 31);
@@ -558,9 +710,9 @@ __device__ void prop_alldiff_gac(const DevModel& M, int a, const uint32_t* dom, 
     // members reached from free values (seeds: D(k) meets F)
     const MS S = ballot_m<TWO>(h0 && sd0, h1 && sd1);
     const bool r0 = h0 && (p0 & S), r1 = h1 && (p1 & S);
-    uint32_t KEEP[W];
+    uint32_t KEEP[U];
 #pragma unroll
-    for (int w = 0; w < W; ++w) KEEP[w] = F[w] | __reduce_or_sync(FULL, (r0 ? bitword(m0, w) : 0u) | (r1 ? bitword(m1, w) : 0u));
+    for (int w = 0; w < U; ++w) KEEP[w] = F[w] | __reduce_or_sync(FULL, (r0 ? bitword(m0, w) : 0u) | (r1 ? bitword(m1, w) : 0u));
     ws.anc[lane] = p0;
     if constexpr (TWO) ws.anc[lane + 32] = p1;
     __syncwarp();
@@ -571,10 +723,10 @@ __device__ void prop_alldiff_gac(const DevModel& M, int a, const uint32_t* dom, 
         if (!h) continue;
         const int k = lane + 32 * sl, mk = sl ? m1 : m0, v = sl ? v1 : v0, sh = sl ? s1 : s0;
         const MS ak = sl ? p1 : p0;
-        uint32_t rem[W];
+        uint32_t rem[U];
         bool anyr = false;
 #pragma unroll
-        for (int w = 0; w < W; ++w) {
+        for (int w = 0; w < U; ++w) {
             uint32_t cand = (sl ? D1[w] : D0[w]) & ~KEEP[w] & ~bitword(mk, w);
             uint32_t x = cand;
             while (x) {
@@ -587,15 +739,23 @@ __device__ void prop_alldiff_gac(const DevModel& M, int a, const uint32_t* dom, 
             anyr |= cand != 0;
         }
         if (anyr) {
+            const int nvw = vwords<W>(M, v);
 #pragma unroll
             for (int w = 0; w < W; ++w) { // back to the member's own bit positions
-                uint32_t mword = sh ? shifted_word<W>(rem, w, -sh) : rem[w];
+                if (w >= nvw) break;      // (unrolled: rem[] stays in registers)
+                const uint32_t mword = sh ? shifted_word<U>(rem, w, -sh) : (w < U ? rem[w] : 0u);
                 if (mword) atomicOr(rm + (size_t)v * W + w, mword);
-                if (post) post[(size_t)k * W + w] = dom[(size_t)v * W + w] & ~mword;
             }
-        } else if (post) {
+        }
+        if (post) {
+            if constexpr (U == W) {
 #pragma unroll
-            for (int w = 0; w < W; ++w) post[(size_t)k * W + w] = dom[(size_t)v * W + w];
+                for (int w = 0; w < W; ++w)
+                    post[(size_t)k * W + w] = dom[(size_t)v * W + w] & ~(sh ? shifted_word<U>(rem, w, -sh) : rem[w]);
+            } else {
+#pragma unroll
+                for (int w = 0; w < U; ++w) post[(size_t)k * W + w] = (sl ? D1[w] : D0[w]) & ~rem[w];
+            }
         }
     }
     if (post && lane == 0) *post_ok = 1;
@@ -1009,7 +1169,8 @@ __device__ __forceinline__ void run_propagators(const DevModel& M, const RoundCt
                 int b = -1;
                 if (v < M.n && (!trig || trig_bit(trig, v)) && M.ne_start[v] < M.ne_start[v + 1]) {
                     const uint32_t* dv = R.dom + (size_t)v * W;
-                    if (dom_size<W>(dv) == 1) b = dom_first<W>(dv);
+                    const int nv = vwords<W>(M, v);
+                    if (dom_size_n<W>(dv, nv) == 1) b = dom_first_n<W>(dv, nv);
                 }
                 unsigned ev = __ballot_sync(FULL, b >= 0);
                 while (ev) {
@@ -1027,15 +1188,33 @@ __device__ __forceinline__ void run_propagators(const DevModel& M, const RoundCt
                 }
             }
         }
-        if constexpr ((F & F_LINEAR) != 0)
-        for (int c = tid; c < M.nl; c += prop_threads) {
-            if (R.enabled && !R.enabled[M.nr + c]) continue;
-            if (trig) {
-                bool hit = false;
-                for (int t = M.lin_start[c]; t < M.lin_start[c + 1] && !hit; ++t) hit = trig_bit(trig, M.lin_var[t]);
-                if (!hit) continue;
+        if constexpr ((F & F_LINEAR) != 0) {
+            const int G = M.lin_g;
+            if (G == 1) {
+                for (int c = tid; c < M.nl; c += prop_threads) {
+                    if (R.enabled && !R.enabled[M.nr + c]) continue;
+                    if (trig) {
+                        bool hit = false;
+                        for (int t = M.lin_start[c]; t < M.lin_start[c + 1] && !hit; ++t) hit = trig_bit(trig, M.lin_var[t]);
+                        if (!hit) continue;
+                    }
+                    if (!prop_linear<W>(M, c, R.dom, R.rm)) *s_err = DERR_OVERFLOW;
+                }
+            } else { // lane groups of G: every lane of the warp iterates the same number of times
+                const int gl = lane & (G - 1);
+                const unsigned gmask = (G == 32 ? FULL : ((1u << G) - 1u)) << (lane & ~(G - 1));
+                const int groups = prop_threads / G;
+                for (int c0 = 0; c0 < M.nl; c0 += groups) {
+                    const int c = c0 + tid / G;
+                    bool run = c < M.nl && !(R.enabled && !R.enabled[M.nr + c]);
+                    if (run && trig) {
+                        bool hit = false;
+                        for (int t = M.lin_start[c] + gl; t < M.lin_start[c + 1]; t += G) hit |= trig_bit(trig, M.lin_var[t]);
+                        run = (__ballot_sync(gmask, hit) & gmask) != 0;
+                    }
+                    if (run && !prop_linear_group<W>(M, c, R.dom, R.rm, G, gl, gmask) && gl == 0) *s_err = DERR_OVERFLOW;
+                }
             }
-            if (!prop_linear<W>(M, c, R.dom, R.rm)) *s_err = DERR_OVERFLOW;
         }
         if constexpr ((F & F_TABLE) != 0)
         for (int c = tid; c < M.ntb; c += prop_threads) {
@@ -1068,12 +1247,21 @@ __device__ __forceinline__ void run_propagators(const DevModel& M, const RoundCt
                 else prop_alldiff_fc_big<W>(M, a, R.dom, R.rm, scratch, lane);
             } else if (R.alldiff) {
                 uint32_t* post = R.post ? R.post + (size_t)M.ad_start[a] * W : nullptr;
-                if (M.ad_start[a + 1] - M.ad_start[a] <= 32)
-                    prop_alldiff_gac<W, false>(M, a, R.dom, R.rm, R.mates + M.ad_start[a], ws, lane, R.exact_wipe, post,
-                                               R.post_ok + a);
-                else
-                    prop_alldiff_gac<W, true>(M, a, R.dom, R.rm, R.mates + M.ad_start[a], ws, lane, R.exact_wipe, post,
-                                              R.post_ok + a);
+                const bool two = M.ad_start[a + 1] - M.ad_start[a] > 32;
+                if (W > 1 && M.ad_uw[a] == -1) { // one-word universe under a wider W
+                    if (!two)
+                        prop_alldiff_gac<W, 1, false>(M, a, R.dom, R.rm, R.mates + M.ad_start[a], ws, lane, R.exact_wipe,
+                                                      post, R.post_ok + a);
+                    else
+                        prop_alldiff_gac<W, 1, true>(M, a, R.dom, R.rm, R.mates + M.ad_start[a], ws, lane, R.exact_wipe,
+                                                     post, R.post_ok + a);
+                } else if (!two) {
+                    prop_alldiff_gac<W, W, false>(M, a, R.dom, R.rm, R.mates + M.ad_start[a], ws, lane, R.exact_wipe, post,
+                                                  R.post_ok + a);
+                } else {
+                    prop_alldiff_gac<W, W, true>(M, a, R.dom, R.rm, R.mates + M.ad_start[a], ws, lane, R.exact_wipe, post,
+                                                 R.post_ok + a);
+                }
             }
             else prop_alldiff_fc<W>(M, a, R.dom, R.rm, lane);
         }
@@ -1092,8 +1280,10 @@ __device__ __forceinline__ int apply_removals(const DevModel& M, const RoundCtx&
         uint32_t* r = R.rm + (size_t)v * W;
         uint32_t any = 0;
         bool vch = false;
+        const int nv = vwords<W>(M, v);
 #pragma unroll
         for (int w = 0; w < W; ++w) {
+            if (W > 2 && w >= nv) break;
             uint32_t rw = r[w], dw = d[w];
             if (rw) {
                 if (dw & rw) {

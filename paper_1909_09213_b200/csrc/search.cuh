@@ -92,7 +92,7 @@ __device__ __forceinline__ int select_var(const DevModel& M, const uint32_t* dom
     const int tid = sc.tid(), T = sc.nthreads();
     unsigned best = 0xffffffffu;
     for (int v = tid; v < M.n; v += T) {
-        const int sz = dom_size<W>(dom + (size_t)v * W);
+        const int sz = dom_size_n<W>(dom + (size_t)v * W, vwords<W>(M, v));
         if (sz > 1) {
             const unsigned key = first_fail ? ((unsigned)sz << 21) | (unsigned)v : (unsigned)v;
             best = key < best ? key : best;
@@ -112,7 +112,7 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
 
     const DevModel& M = P.M;
     const int ctx = SC::kGrid ? 0 : (int)blockIdx.x, tid = sc.tid(), T = sc.nthreads(), nw = sc.nwarps();
-    const bool parallel = P.mode == MODE_PARALLEL;
+    const bool parallel = (F & F_PARITY) == 0 && P.mode == MODE_PARALLEL;
     const int n = M.n;
     const size_t NW = (size_t)n * W, NWP = round4(NW);
     const int KW = P.KW;
@@ -155,7 +155,7 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
 
     unsigned long long nodes = 0, failures = 0, rounds = 0, sols = 0;
     int sp = 0, base = 0, depth = 0;
-    const bool batch = P.batch != 0;
+    const bool batch = (F & F_PARITY) != 0 && P.batch != 0; // parity kernels only
     bool has_bound = batch ? P.batch_has_bound[ctx] != 0 : P.has_init_bound != 0;
     long long bound = batch ? P.batch_bound[ctx] : P.init_bound;
     bool has_first = false;
@@ -170,7 +170,7 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
     long long idle_cyc = 0, steals = 0, donations = 0;
     const long long t_start = clock64();
     // first mode: current segment and the counters at its start; thread 0 caches the best key
-    const bool first_mode = (F & F_FIRST) != 0 && P.first_mode != 0; // compile-time off in lean kernels
+    const bool first_mode = (F & F_FIRST) != 0 && (F & F_PARITY) == 0 && P.first_mode != 0; // compile-time off in lean kernels
     long long seg = (!parallel || ctx == 0) && !P.n_seed ? 0 : -1;
     unsigned long long seg_n0 = 0, seg_f0 = 0, seg_r0 = 0;
     int gbest_idx = -1;
@@ -612,7 +612,18 @@ __global__ void __launch_bounds__(1024) search_kernel_grid(const SearchParams P)
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ unsigned red[32];
     GridScope sc{P.grid_or, P.grid_min};
-    search_body<W, F_ALL>(P, sc, *P.grid_ctl, red, smem);
+    search_body<W, F_ALL | F_PARITY>(P, sc, *P.grid_ctl, red, smem);
+}
+
+// the parity engine and batched B&B: one block per problem, reference node order; no parallel
+// work sharing compiled in, and up to 128 registers per thread (<= 512 threads)
+template <int W>
+__global__ void __launch_bounds__(512, 1) search_kernel_parity(const SearchParams P) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ Ctl C;
+    __shared__ unsigned red[32];
+    BlockScope sc;
+    search_body<W, F_ALL | F_PARITY>(P, sc, C, red, smem);
 }
 
 // cubics_propagate / cubics_removals: one block over caller-provided domains
