@@ -357,7 +357,7 @@ void prepare(const HostModel& m, const uint64_t* words, Prepared& P) {
         std::vector<int32_t> vw(std::max(n, 1), 1);
         for (int v = 0; v < n; ++v) {
             vw[v] = std::max(1, std::min(W, (m.width[v] + 31) / 32));
-            if (W > 2 && vw[v] * 4 <= W) P.mixed_width = true;
+            if (W >= 8 && vw[v] * 4 <= W) P.mixed_width = true;
         }
         P.o_vw = P.blob.add(vw.data(), vw.size());
     }

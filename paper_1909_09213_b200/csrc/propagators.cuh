@@ -115,40 +115,40 @@ __device__ __forceinline__ void or_bit(uint32_t* rmv, const uint32_t* dv, int bi
 // not pay W words per operation on every variable.
 template <int W>
 __device__ __forceinline__ int vwords(const DevModel& M, int v) {
-    if constexpr (W <= 2) return W;
+    if constexpr (W <= 4) return W; // short unrolled loops beat a per-variable bound
     else return M.vw ? M.vw[v] : W; // vw == null: no variable is much narrower than W
 }
 template <int W>
 __device__ __forceinline__ bool dom_empty_n(const uint32_t* d, int n) {
-    if (W <= 2 || n == W) return dom_empty<W>(d);
+    if (W <= 4 || n == W) return dom_empty<W>(d);
     uint32_t o = 0;
     for (int i = 0; i < n; ++i) o |= d[i];
     return o == 0;
 }
 template <int W>
 __device__ __forceinline__ int dom_first_n(const uint32_t* d, int n) {
-    if (W <= 2 || n == W) return dom_first<W>(d);
+    if (W <= 4 || n == W) return dom_first<W>(d);
     for (int i = 0; i < n; ++i)
         if (d[i]) return i * 32 + __ffs(d[i]) - 1;
     return -1;
 }
 template <int W>
 __device__ __forceinline__ int dom_last_n(const uint32_t* d, int n) {
-    if (W <= 2 || n == W) return dom_last<W>(d);
+    if (W <= 4 || n == W) return dom_last<W>(d);
     for (int i = n - 1; i >= 0; --i)
         if (d[i]) return i * 32 + 31 - __clz(d[i]);
     return -1;
 }
 template <int W>
 __device__ __forceinline__ int dom_size_n(const uint32_t* d, int n) {
-    if (W <= 2 || n == W) return dom_size<W>(d);
+    if (W <= 4 || n == W) return dom_size<W>(d);
     int s = 0;
     for (int i = 0; i < n; ++i) s += __popc(d[i]);
     return s;
 }
 template <int W>
 __device__ __forceinline__ void or_range_n(uint32_t* rmv, const uint32_t* dv, long long lo, long long hi, int n) {
-    if (W <= 2 || n == W) {
+    if (W <= 4 || n == W) {
         or_range<W>(rmv, dv, lo, hi);
     } else {
         if (lo > hi) return;
@@ -302,6 +302,90 @@ __device__ bool filter_le(const DevModel& M, int b, int e, long long sign, long 
         } else {     // remove v < budget / a, i.e. v <= ceil(budget / a) - 1
             i128 thr = a == -1 ? -budget - 1 : ceil_div(budget, a) - 1;
             or_range_n<W>(rv, d, -1, clampbit(thr - offv, NB), nv);
+        }
+    }
+    return true;
+}
+
+// Sums of <= 4 terms, one thread: each term's bounds are read once, and the cuts of both
+// directions of an equality become one keep-window per variable. Event order, overflow checks
+// and thresholds are filter_le's (the first empty domain in term order makes a direction a
+// no-op; any overflow returns false).
+template <int W>
+__device__ bool prop_linear_small(const DevModel& M, int c, const uint32_t* dom, uint32_t* rm) {
+    constexpr int NB = W * 32;
+    const int b = M.lin_start[c], k = M.lin_start[c + 1] - b;
+    const long long bound = M.lin_bound[c];
+    const int ndir = M.lin_op[c] == 1 ? 2 : 1;
+    int v[4], lo[4], hi[4];
+    long long co[4], of[4], cutlo[4], cuthi[4]; // remove bits <= cutlo and bits >= cuthi
+    int first_empty = 4;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        v[t] = 0;
+        co[t] = of[t] = 0;
+        lo[t] = hi[t] = 0;
+        cutlo[t] = -1;
+        cuthi[t] = NB;
+        if (t < k) {
+            v[t] = M.lin_var[b + t];
+            co[t] = M.lin_coeff[b + t];
+            of[t] = M.off[v[t]];
+            const uint32_t* d = dom + (size_t)v[t] * W;
+            lo[t] = dom_first<W>(d);
+            hi[t] = dom_last<W>(d);
+            if (lo[t] < 0 && first_empty == 4) first_empty = t;
+        }
+    }
+#pragma unroll
+    for (int dir = 0; dir < 2; ++dir) {
+        if (dir >= ndir) break;
+        const long long sg = dir ? -1 : 1, bnd = dir ? -bound : bound;
+        long long total = 0;
+        bool noop = false;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) { // :217-224
+            if (t >= k || noop) continue;
+            if (t == first_empty) {
+                noop = true;
+                continue;
+            }
+            const long long a = sg * co[t];
+            const i128 tm = (i128)a * (of[t] + (a > 0 ? lo[t] : hi[t]));
+            if (!fits64(tm)) return false;
+            const i128 sum = (i128)total + tm;
+            if (!fits64(sum)) return false;
+            total = (long long)sum;
+        }
+        if (noop) continue;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) { // :225-235
+            if (t >= k) continue;
+            const long long a = sg * co[t];
+            const long long tm = a * (of[t] + (a > 0 ? lo[t] : hi[t]));
+            const i128 rest = (i128)total + (i128)wrap_add(0, -tm);
+            if (!fits64(rest)) return false;
+            const i128 budget = (i128)bnd - rest;
+            if (a > 0) {
+                const i128 thr = a == 1 ? budget : floor_div(budget, a);
+                const long long f = clampbit(thr + 1 - of[t], NB);
+                cuthi[t] = f < cuthi[t] ? f : cuthi[t];
+            } else {
+                const i128 thr = a == -1 ? -budget - 1 : ceil_div(budget, a) - 1;
+                const long long u = clampbit(thr - of[t], NB);
+                cutlo[t] = u > cutlo[t] ? u : cutlo[t];
+            }
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        if (t >= k || (cutlo[t] < 0 && cuthi[t] >= NB)) continue;
+        const uint32_t* dv = dom + (size_t)v[t] * W;
+        uint32_t* rv = rm + (size_t)v[t] * W;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            const uint32_t m = (range_word(w, -1, cutlo[t]) | range_word(w, cuthi[t], NB)) & dv[w];
+            if (m) atomicOr(rv + w, m);
         }
     }
     return true;
@@ -1198,7 +1282,7 @@ __device__ __forceinline__ void run_propagators(const DevModel& M, const RoundCt
                         for (int t = M.lin_start[c]; t < M.lin_start[c + 1] && !hit; ++t) hit = trig_bit(trig, M.lin_var[t]);
                         if (!hit) continue;
                     }
-                    if (!prop_linear<W>(M, c, R.dom, R.rm)) *s_err = DERR_OVERFLOW;
+                    if (!prop_linear_small<W>(M, c, R.dom, R.rm)) *s_err = DERR_OVERFLOW;
                 }
             } else { // lane groups of G: every lane of the warp iterates the same number of times
                 const int gl = lane & (G - 1);
@@ -1283,7 +1367,7 @@ __device__ __forceinline__ int apply_removals(const DevModel& M, const RoundCtx&
         const int nv = vwords<W>(M, v);
 #pragma unroll
         for (int w = 0; w < W; ++w) {
-            if (W > 2 && w >= nv) break;
+            if (W > 4 && w >= nv) break;
             uint32_t rw = r[w], dw = d[w];
             if (rw) {
                 if (dw & rw) {
