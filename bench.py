@@ -225,13 +225,32 @@ def impl_ours(args):
     from paper_1909_09213_b200 import solver as S
 
     rank, world, local = dist_env()
+    import torch
+
+    dist = None
     if world > 1:
-        import torch
         import torch.distributed as dist
 
+        # one process per GPU over NCCL; CUBICS_BENCH_BACKEND=gloo with fewer GPUs than ranks is
+        # a functional check of this code path only (ranks then share a device)
+        backend = os.environ.get("CUBICS_BENCH_BACKEND", "nccl")
+        local = local % max(1, torch.cuda.device_count())
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group(backend)
     device = local if world > 1 else 0
+    coll_dev = f"cuda:{local}" if (dist is None or dist.get_backend() == "nccl") else "cpu"
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize(device)
+
+    def max_over_ranks(vals):
+        if dist is None:
+            return list(vals)
+        t = torch.tensor(list(vals), dtype=torch.float64, device=coll_dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.tolist()
     text = open(os.path.join(MODELS, args.instance + ".fd")).read()
     model = S.parse_model(text)
     cfg = S.SearchConfig(engine=A.ENGINE_PARALLEL, device=device, count_only=True, contexts=args.contexts,
@@ -243,8 +262,6 @@ def impl_ours(args):
             return S.solve_shard(model, c, rank, world)
         return S.solve_satisfy(model, c, (lambda s: True) if not count_only else None)
 
-    import torch
-
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{device}")  # > 126 MB L2
 
     def flush_l2():
@@ -253,45 +270,63 @@ def impl_ours(args):
 
     for _ in range(args.warmup):
         one_step()
-    if world > 1:
-        dist.barrier()
     stats0 = None
     dev_ms = []
     with ClockSampler(device) as clk:
         for _ in range(args.steps):
             flush_l2()
+            barrier()  # every rank starts the step together; device time is CUDA events
             r = one_step()
             dev_ms.append(r.device_ms)
             stats0 = r.stats
-    # e2e: through the public C ABI (cubics_enumerate) with host buffers: model upload, search,
-    # device-side DFS ordering, and every solution copied back into a host int64 array
+    barrier()
+    dev_ms = max_over_ranks(dev_ms)  # per step, the slowest rank
+    tot = S.SearchStats(*stats0.as_tuple())
+    if dist is not None:  # whole-job stats: one all-reduce (sum) of the shards' partial stats
+        t = torch.tensor(list(stats0.as_tuple()), dtype=torch.int64, device=coll_dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        tot = S.SearchStats(*[int(x) for x in t.tolist()])
     e2e_ms, h2d, d2h, e2e_launches = [], 0, 0, 0
-    for _ in range(max(1, min(args.steps, 3))):
-        flush_l2()
-        t0 = time.perf_counter()
-        arr, r2 = S.enumerate_array(model, S.SearchConfig(**{**cfg.__dict__, "count_only": False}))
-        e2e_ms.append((time.perf_counter() - t0) * 1e3)
-        h2d, d2h, e2e_launches = r2.h2d_bytes, r2.d2h_bytes, r2.kernel_launches
-        assert arr.shape[0] == r2.stats.solutions
+    if world == 1:
+        # e2e: through the public C ABI (cubics_enumerate) with host buffers: model upload, search,
+        # device-side DFS ordering, and every solution copied back into a host int64 array
+        for _ in range(max(1, min(args.steps, 3))):
+            flush_l2()
+            t0 = time.perf_counter()
+            arr, r2 = S.enumerate_array(model, S.SearchConfig(**{**cfg.__dict__, "count_only": False}))
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+            h2d, d2h, e2e_launches = r2.h2d_bytes, r2.d2h_bytes, r2.kernel_launches
+            assert arr.shape[0] == r2.stats.solutions
+        e2e_api = "cubics_enumerate (all solutions in DFS order into a host int64 array)"
+    else:
+        # e2e at N GPUs: the public multi-GPU API (distributed.solve_distributed -> cubics_solve_shard
+        # + one all-reduce of the stats), wall time per rank, max over ranks
+        from paper_1909_09213_b200 import distributed as D
+
+        for _ in range(max(1, min(args.steps, 3))):
+            flush_l2()
+            barrier()
+            t0 = time.perf_counter()
+            st, _, _ = D.solve_distributed(model, cfg, rank, world, collect=False, device=coll_dev)
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+            assert tuple(st) == tot.as_tuple()
+        e2e_ms = max_over_ranks(e2e_ms)
+        h2d, d2h = r.h2d_bytes, r.d2h_bytes
+        e2e_launches = r.kernel_launches
+        e2e_api = "distributed.solve_distributed (cubics_solve_shard per rank + all-reduce of the stats)"
     extras = run_extras(S, A, device) if (rank == 0 and not args.no_extras) else None
-    ms = max(dev_ms) if dev_ms else 0.0
-    nodes = stats0.nodes
-    if world > 1:
-        t = torch.tensor([ms, nodes], dtype=torch.float64, device=f"cuda:{local}")
-        mx = t.clone()
-        dist.all_reduce(mx[0:1], op=dist.ReduceOp.MAX)
-        dist.all_reduce(t[1:2], op=dist.ReduceOp.SUM)
-        ms, nodes = float(mx[0]), int(t[1])
+    nodes = tot.nodes
     if rank != 0:
+        dist.destroy_process_group()
         return 0
     mean_ms = sum(dev_ms) / len(dev_ms)
     value = nodes / (mean_ms / 1e3)
-    A_bytes, S_, V = algorithmic_bytes(model, stats0)
+    A_bytes, S_, V = algorithmic_bytes(model, tot)
     peak, peak_kind = load_peaks()
     achieved = A_bytes / (mean_ms / 1e3) / 1e9
     # CPU baseline: the unmodified reference on this host, bounded sample
     cpu = None
-    if os.path.exists(REF_DRIVER) and not args.no_cpu:
+    if os.path.exists(REF_DRIVER) and not args.no_cpu and world == 1:
         v, out = cpu_sample(args.instance, args.cpu_node_limit, 1)
         cpu = {"value": v, "unit": "nodes/s", "cores": 1, "kind": "reference",
                "sample": f"first {args.cpu_node_limit} nodes of the {args.instance} all-solutions DFS "
@@ -303,12 +338,11 @@ def impl_ours(args):
         "vs_baseline": None, "dtype": "int64", "data": "synthetic",
         "config": {"workload": f"{args.instance} all solutions (N-Queens n=14, BASELINE configs[1])",
                    "engine": "parallel", "contexts": r.contexts, "l2": "flushed (256 MiB write) before every timed step",
-                   "stats": {"nodes": stats0.nodes, "failures": stats0.failures, "rounds": stats0.rounds,
-                             "solutions": stats0.solutions}},
+                   "stats": {"nodes": tot.nodes, "failures": tot.failures, "rounds": tot.rounds,
+                             "solutions": tot.solutions}},
         "time_to_all_solutions_ms": mean_ms,
         "e2e": {"value": nodes / (e2e_best / 1e3), "unit": "nodes/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "time_to_all_solutions_ms": e2e_best,
-                "api": "cubics_enumerate (all solutions in DFS order into a host int64 array)",
+                "d2h_bytes_per_step": d2h, "time_to_all_solutions_ms": e2e_best, "api": e2e_api,
                 "gpu_launches": e2e_launches},
         "gpu_launches": r.kernel_launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -320,7 +354,7 @@ def impl_ours(args):
         "other_configs": extras,
     }
     print(json.dumps(line))
-    if world > 1:
+    if dist is not None:
         dist.destroy_process_group()
     return 0
 
