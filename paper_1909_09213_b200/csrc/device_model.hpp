@@ -47,6 +47,8 @@ struct DevModel {
     const int64_t* lin_coeff;
     int32_t lin_g;            // lanes per linear constraint (1: one thread each; 2..32: lane groups)
     int32_t na;
+    uint32_t ad_full_mask;    // bit a (a < 32): alldifferent a's scope is every variable, so it is
+                              // triggered in every round (the trigger scan is skipped)
     const int32_t* ad_start;  // [na+1]
     const int32_t* ad_var;
     const int32_t* ad_shift;

@@ -119,6 +119,7 @@ struct Prepared {
     size_t big_words = 0;
     int nr_gen = 0;
     int lin_g = 1;
+    uint32_t ad_full_mask = 0;
     std::vector<int> kind_index; // constraint index -> kind-local index (rb | nr+lin | nr+nl+ad)
     std::vector<int64_t> offsets;
     DevModel bind(const uint8_t* base) const {
@@ -141,6 +142,7 @@ struct Prepared {
         M.lin_coeff = reinterpret_cast<const int64_t*>(base + o_lc);
         M.lin_g = lin_g;
         M.na = na;
+        M.ad_full_mask = ad_full_mask;
         M.ad_start = reinterpret_cast<const int32_t*>(base + o_as);
         M.ad_var = reinterpret_cast<const int32_t*>(base + o_av);
         M.ad_shift = reinterpret_cast<const int32_t*>(base + o_ash);
@@ -323,6 +325,17 @@ void prepare(const HostModel& m, const uint64_t* words, Prepared& P) {
     if (max_terms > 4)
         while (P.lin_g < max_terms && P.lin_g < 32) P.lin_g *= 2;
     P.na = static_cast<int>(as.size()) - 1;
+    P.ad_full_mask = 0;
+    for (int a = 0; a < P.na && a < 32; ++a) {
+        std::vector<char> seen(n, 0);
+        int cnt = 0;
+        for (int t = as[a]; t < as[a + 1]; ++t)
+            if (!seen[av[t]]) {
+                seen[av[t]] = 1;
+                ++cnt;
+            }
+        if (cnt == n) P.ad_full_mask |= 1u << a;
+    }
     P.total_members = static_cast<int>(av.size());
     std::vector<uint32_t> dom(P.NWP, 0);
     P.depth_bound = 0;
@@ -606,7 +619,8 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
         if (L.total > kSmemBudget) throw StatusError{CUBICS_E_UNSUPPORTED, "search context does not fit in shared memory"};
     }
     // propagator features the model needs: the lean kernel instantiations skip the rest
-    const int feat = (P.nl ? 1 : 0) | (P.ntb + P.ntn ? 2 : 0) | (P.big_words ? 4 : 0) | (first_mode ? 8 : 0);
+    const int feat = (P.nl ? 1 : 0) | (P.ntb + P.ntn ? 2 : 0) | (P.big_words ? 4 : 0) | (first_mode ? 8 : 0) |
+                     (P.lin_g > 1 ? dev::F_LONG : 0);
     int n_ctx = batch ? batch->count : 1;
     if (parallel) {
         int per_sm = 0;

@@ -13,6 +13,19 @@
 namespace cubics {
 namespace dev {
 
+// Compile-time propagator features of a kernel instantiation: a model without linear sums,
+// tables or large alldifferents runs a kernel without that code (register pressure decides the
+// occupancy of one-warp search contexts).
+// F_PARITY marks a kernel that only runs the reference-order engines (parity block, batched
+// B&B, grid context): the parallel engine's work sharing compiles out of it.
+// F_REGS marks the 128-register parity kernel: register-hungry fast paths are compiled in only
+// there (in the 64-register kernels they cost more in spills than they save).
+// F_LONG: linear sums of more than 4 terms (lane-group form); lean kernels compile it out.
+enum Feature : int {
+    F_LINEAR = 1, F_TABLE = 2, F_BIGAD = 4, F_FIRST = 8, F_LONG = 64, F_ALL = 15 | 64, F_PARITY = 16, F_REGS = 32
+};
+
+
 CUBICS_HD constexpr size_t round4(size_t x) { return (x + 3) & ~size_t(3); }
 
 // per-warp alldifferent scratch: BFS layers [66] + ancestor sets [64] (u64) + value owners [W*32] (u8)

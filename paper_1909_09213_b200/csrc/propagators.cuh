@@ -27,12 +27,6 @@ typedef __int128 i128;
 
 enum RoundStatus : int { R_CHANGED = 0, R_STABLE = 1, R_FAILED = 2, R_ERROR = 3 };
 
-// Compile-time propagator features of a kernel instantiation: a model without linear sums,
-// tables or large alldifferents runs a kernel without that code (register pressure decides the
-// occupancy of one-warp search contexts).
-// F_PARITY marks a kernel that only runs the reference-order engines (parity block, batched
-// B&B, grid context): the parallel engine's work sharing compiles out of it.
-enum Feature : int { F_LINEAR = 1, F_TABLE = 2, F_BIGAD = 4, F_FIRST = 8, F_ALL = 15, F_PARITY = 16 };
 
 // ------------------------------------------------------------------ bitset helpers
 template <int W>
@@ -1273,7 +1267,7 @@ __device__ __forceinline__ void run_propagators(const DevModel& M, const RoundCt
             }
         }
         if constexpr ((F & F_LINEAR) != 0) {
-            const int G = M.lin_g;
+            const int G = (F & F_LONG) != 0 ? M.lin_g : 1; // lean kernels: thread per sum, any arity
             if (G == 1) {
                 for (int c = tid; c < M.nl; c += prop_threads) {
                     if (R.enabled && !R.enabled[M.nr + c]) continue;
@@ -1282,7 +1276,9 @@ __device__ __forceinline__ void run_propagators(const DevModel& M, const RoundCt
                         for (int t = M.lin_start[c]; t < M.lin_start[c + 1] && !hit; ++t) hit = trig_bit(trig, M.lin_var[t]);
                         if (!hit) continue;
                     }
-                    if (!prop_linear_small<W>(M, c, R.dom, R.rm)) *s_err = DERR_OVERFLOW;
+                    const bool ok = (F & F_REGS) != 0 && M.lin_g == 1 ? prop_linear_small<W>(M, c, R.dom, R.rm)
+                                                                         : prop_linear<W>(M, c, R.dom, R.rm);
+                    if (!ok) *s_err = DERR_OVERFLOW;
                 }
             } else { // lane groups of G: every lane of the warp iterates the same number of times
                 const int gl = lane & (G - 1);
@@ -1319,7 +1315,9 @@ __device__ __forceinline__ void run_propagators(const DevModel& M, const RoundCt
         const WarpScratch ws = warp_scratch<W>(R, threadIdx.x >> 5); // shared memory of this block
         for (int a = warp - (nw - ad_warps); a < M.na; a += ad_warps) {
             if (R.enabled && !R.enabled[M.nr + M.nl + a]) continue;
-            if (trig) {
+            // a round only runs after some variable changed, so an alldifferent over every
+            // variable is always triggered
+            if (trig && !(a < 32 && ((M.ad_full_mask >> a) & 1u))) {
                 const int b = M.ad_start[a], e = M.ad_start[a + 1];
                 bool hit = false;
                 for (int t = b + lane; t < e; t += 32) hit |= trig_bit(trig, M.ad_var[t]);

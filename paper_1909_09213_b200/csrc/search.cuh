@@ -623,7 +623,7 @@ __global__ void __launch_bounds__(512, 1) search_kernel_parity(const SearchParam
     __shared__ Ctl C;
     __shared__ unsigned red[32];
     BlockScope sc;
-    search_body<W, F_ALL | F_PARITY>(P, sc, C, red, smem);
+    search_body<W, F_ALL | F_PARITY | F_REGS>(P, sc, C, red, smem);
 }
 
 // cubics_propagate / cubics_removals: one block over caller-provided domains
