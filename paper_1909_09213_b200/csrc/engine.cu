@@ -6,6 +6,7 @@
 // There is no CPU fallback: without a usable sm_100 device every entry point returns
 // CUBICS_E_CUDA with the CUDA error text in cubics_last_error().
 #include <cuda_runtime.h>
+#include <sys/mman.h>
 
 #include <algorithm>
 #include <chrono>
@@ -63,7 +64,7 @@ struct Arena {
 // one search at a time per device: the arenas below are reused by every call
 std::recursive_mutex g_dev_mu[64];
 Arena g_arena[2][64];
-Arena g_pinned[64];
+Arena g_pinned[2][64];
 
 // slot 0: per-call search state; slot 1: solution-ordering scratch (kept apart so growing one
 // never invalidates the other while both are live)
@@ -79,8 +80,9 @@ uint8_t* device_arena(int dev, size_t bytes, int slot = 0) {
     return static_cast<uint8_t*>(a.ptr);
 }
 
-uint8_t* pinned_arena(int dev, size_t bytes) {
-    Arena& a = g_pinned[dev];
+// slot 0: upload staging; slot 1: solution download (read by the caller under the device lock)
+uint8_t* pinned_arena(int dev, size_t bytes, int slot = 0) {
+    Arena& a = g_pinned[slot][dev];
     if (a.cap < bytes) {
         if (a.ptr) cudaFreeHost(a.ptr);
         a.ptr = nullptr;
@@ -512,6 +514,12 @@ struct Records { // solutions copied back from the device
     uint64_t count = 0;
     bool ordered = false; // vals already in the reference's DFS order
     std::vector<uint16_t> vals;
+    const uint16_t* pinned = nullptr; // when set, the rows live in pinned slot 1 instead of vals
+    const uint16_t* rows() const { return pinned ? pinned : vals.data(); }
+    void materialize(size_t n) {
+        if (pinned) vals.assign(pinned, pinned + count * n);
+        pinned = nullptr;
+    }
     std::vector<uint32_t> keys;
     std::vector<uint64_t> stats;
 };
@@ -524,6 +532,7 @@ struct RunOut {
     int KW = 0;
     double device_ms = 0;
     uint64_t h2d = 0, d2h = 0, launches = 0;
+    bool pinned_rows = false; // in: download solution rows into pinned slot 1 (cubics_enumerate)
     std::vector<uint16_t> inc_vals;
     std::vector<uint32_t> first_key;  // parallel: DFS-first solution key/values
     std::vector<uint16_t> first_vals;
@@ -863,7 +872,14 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
         uint64_t recorded = parallel ? got : std::min<uint64_t>(out.ws.stats[3], sol_cap);
         if (!recorded_first_done) out.rec.count = recorded;
         if (recorded && !recorded_first_done) {
-            out.rec.vals.resize(recorded * n);
+            uint16_t* dst;
+            if (out.pinned_rows) {
+                dst = reinterpret_cast<uint16_t*>(pinned_arena(dev, sizeof(uint16_t) * n * recorded, 1));
+                out.rec.pinned = dst;
+            } else {
+                out.rec.vals.resize(recorded * n);
+                dst = out.rec.vals.data();
+            }
             const uint16_t* src = reinterpret_cast<const uint16_t*>(base + a_svals);
             if (parallel && KW && n && recorded > 1 && !want_keys) {
                 const int used = std::max(1, std::min(KW, (out.ws.max_depth + 31) / 32));
@@ -871,7 +887,7 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
                                       st, &out.launches);
                 out.rec.ordered = true;
             }
-            CU(cudaMemcpyAsync(out.rec.vals.data(), src, sizeof(uint16_t) * n * recorded, cudaMemcpyDeviceToHost, st));
+            CU(cudaMemcpyAsync(dst, src, sizeof(uint16_t) * n * recorded, cudaMemcpyDeviceToHost, st));
             out.d2h += sizeof(uint16_t) * n * recorded;
             if (!parallel) out.rec.ordered = true;
             if (KW && want_keys) {
@@ -1019,13 +1035,15 @@ extern "C" void cubics_search_config_init(cubics_search_config* c) {
 namespace {
 // Search for every solution with records materialised (rerun once with an exact buffer when the
 // first guess overflowed); the records come back in the reference's DFS order.
-RunOut satisfy_run(const HostModel& m, const cubics_search_config& cfg, bool record, cubics_result* out) {
+RunOut satisfy_run(const HostModel& m, const cubics_search_config& cfg, bool record, cubics_result* out,
+                   bool pinned_rows = false) {
     std::memset(out, 0, sizeof *out);
     // an objective makes the stream a sequence of incumbents, whose order only the reference
     // node order reproduces: AUTO picks the parity engine then
     int engine = pick_engine(cfg, m.goal != CUBICS_SATISFY);
     uint64_t cap = default_sol_cap(m, cfg);
     RunOut r;
+    r.pinned_rows = pinned_rows;
     try {
         run_search(m, cfg, engine, record, cap, r);
     } catch (const StatusError& e) {
@@ -1034,10 +1052,12 @@ RunOut satisfy_run(const HostModel& m, const cubics_search_config& cfg, bool rec
         if (e.code != CUBICS_E_CAPACITY || engine != CUBICS_ENGINE_PARALLEL || cfg.max_solutions != 1) throw;
         engine = CUBICS_ENGINE_PARITY;
         r = RunOut{};
+        r.pinned_rows = pinned_rows;
         run_search(m, cfg, engine, record, cap, r);
     }
     if (record && r.ws.stats[3] > r.rec.count && r.rec.count == cap) { // buffer overflow: rerun exact
         RunOut r2;
+        r2.pinned_rows = pinned_rows;
         run_search(m, cfg, engine, record, r.ws.stats[3], r2);
         r2.h2d += r.h2d;
         r2.d2h += r.d2h;
@@ -1050,9 +1070,10 @@ RunOut satisfy_run(const HostModel& m, const cubics_search_config& cfg, bool rec
     out->has_solution = r.ws.stats[3] > 0;
     if (m.goal != CUBICS_SATISFY && r.rec.count) {
         const size_t last = r.rec.count - 1;
-        out->objective = m.offset[m.goal_var] + r.rec.vals[last * n + m.goal_var];
+        out->objective = m.offset[m.goal_var] + r.rec.rows()[last * n + m.goal_var];
     }
     if (record && r.rec.count && !r.rec.ordered && r.KW) { // keyed records: host-side DFS order
+        r.rec.materialize(n);
         const int KW = r.KW;
         std::vector<uint64_t> order(r.rec.count);
         std::iota(order.begin(), order.end(), 0);
@@ -1106,6 +1127,21 @@ extern "C" int cubics_solve_satisfy(const cubics_model* h, const cubics_search_c
     });
 }
 
+// Solution arrays: 2 MiB-aligned and advised as huge pages when large, so filling a 40 MB result
+// costs tens of page faults instead of ten thousand. Freed with free() (cubics_solutions_free).
+int64_t* alloc_values(uint64_t count) {
+    const size_t bytes = sizeof(int64_t) * count;
+    void* p = nullptr;
+    if (bytes >= (size_t(4) << 20)) {
+        const size_t huge = size_t(2) << 20;
+        if (posix_memalign(&p, huge, (bytes + huge - 1) / huge * huge) != 0) p = nullptr;
+        if (p) madvise(p, (bytes + huge - 1) / huge * huge, MADV_HUGEPAGE);
+    }
+    if (!p) p = std::malloc(std::max<size_t>(bytes, 8));
+    if (!p) throw std::bad_alloc();
+    return static_cast<int64_t*>(p);
+}
+
 extern "C" int cubics_enumerate(const cubics_model* h, const cubics_search_config* cfg, cubics_solutions** sols,
                                 cubics_result* out) {
     if (!h || !cfg || !out || !sols) return CUBICS_E_INVALID;
@@ -1114,17 +1150,20 @@ extern "C" int cubics_enumerate(const cubics_model* h, const cubics_search_confi
         const double t0 = now_ms();
         const HostModel& m = h->m;
         const int n = m.n_vars();
-        RunOut r = satisfy_run(m, *cfg, !cfg->count_only, out);
+        // the rows arrive in the device's pinned download buffer: hold the device until converted
+        std::lock_guard<std::recursive_mutex> lock(g_dev_mu[current_device(cfg->device)]);
+        RunOut r = satisfy_run(m, *cfg, !cfg->count_only, out, true);
+        const double t1 = now_ms();
         auto* S = new cubics_solutions{};
         S->n_vars = n;
         S->count = r.rec.count;
         const uint64_t total = r.rec.count * (uint64_t)n;
-        S->values = new int64_t[std::max<uint64_t>(total, 1)];
+        S->values = alloc_values(std::max<uint64_t>(total, 1));
         // offset conversion straight into the returned buffer, split over host threads
         const unsigned nt = total > (1u << 20) ? std::max(1u, std::min(16u, std::thread::hardware_concurrency())) : 1u;
         auto conv = [&](uint64_t lo, uint64_t hi) {
             for (uint64_t i = lo; i < hi; ++i) {
-                const uint16_t* row = r.rec.vals.data() + i * n;
+                const uint16_t* row = r.rec.rows() + i * n;
                 int64_t* dst = S->values + i * n;
                 for (int v = 0; v < n; ++v) dst[v] = m.offset[v] + row[v];
             }
@@ -1136,13 +1175,16 @@ extern "C" int cubics_enumerate(const cubics_model* h, const cubics_search_confi
         for (auto& th : pool) th.join();
         *sols = S;
         out->total_ms = now_ms() - t0;
+        if (std::getenv("CUBICS_DEBUG"))
+            std::fprintf(stderr, "[cubics] enumerate: search+download %.3f ms (device %.3f), convert %.3f ms, %llu rows\n",
+                         t1 - t0, out->device_ms, now_ms() - t1, (unsigned long long)r.rec.count);
         return CUBICS_OK;
     });
 }
 
 extern "C" void cubics_solutions_free(cubics_solutions* s) {
     if (!s) return;
-    delete[] s->values;
+    std::free(s->values);
     delete s;
 }
 
