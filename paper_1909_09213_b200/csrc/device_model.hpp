@@ -190,6 +190,11 @@ struct PropParams {
     uint32_t* out;         // removals output (removals_only)
     uint32_t* big_scratch; // [warps][M.big_words]
     int32_t* result;       // failed, failed_var, rounds, last_status, error
+    // grid-wide fixpoint (cooperative launch, large models): control, vote slots, triggers
+    dev_ctl_t* grid_ctl;
+    unsigned* grid_or;     // [3]
+    unsigned* grid_min;    // [3]
+    uint32_t* grid_chg;    // [2 * ceil(n/32)]
 };
 
 } // namespace cubics

@@ -1414,14 +1414,29 @@ int run_prop(const cubics_model* h, const uint64_t* words_in, uint64_t* words_ou
         }
         use = &sub;
     }
+    const double tp0 = now_ms();
     prepare(*use, words_in, P);
+    const double tp1 = now_ms();
     const size_t NWP = P.NWP;
-    const int block = parity_block(P);
-    bool in_smem = true;
-    dev::SmemLayout L = dev::smem_layout(P.W, P.n, P.total_members, block / 32, 0, true, P.na);
+    // many alldifferents (more than one block's warps) or a large model: a grid-wide fixpoint
+    const bool grid = P.na > 8 || (long)P.nr + P.nl + 4L * (P.ntb + P.ntn) >= 40000 || P.n >= 50000;
+    const int block = grid ? 512 : parity_block(P);
+    bool in_smem = !grid;
+    dev::SmemLayout L = dev::smem_layout(P.W, P.n, P.total_members, block / 32, 0, in_smem, P.na);
     if (L.total > kSmemBudget) {
         in_smem = false;
         L = dev::smem_layout(P.W, P.n, P.total_members, block / 32, 0, false, P.na);
+        if (grid && L.total > kSmemBudget) throw StatusError{CUBICS_E_UNSUPPORTED, "propagation context does not fit in shared memory"};
+    }
+    int grid_blocks = 1;
+    if (grid) {
+        int per_sm = 0, sms = 0;
+#define OPG(w) occupancy_propagate_grid<w>(block, L.total, &per_sm)
+        CUBICS_DISPATCH_W(P.W, OPG)
+#undef OPG
+        CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        if (per_sm < 1) throw StatusError{CUBICS_E_UNSUPPORTED, "grid propagation does not fit on an SM"};
+        grid_blocks = std::min(per_sm, 2) * sms;
     }
     size_t off = 0;
     auto take = [&](size_t bytes) {
@@ -1434,7 +1449,10 @@ int run_prop(const cubics_model* h, const uint64_t* words_in, uint64_t* words_ou
     const size_t a_out = take(sizeof(uint32_t) * NWP);
     const size_t a_res = take(sizeof(int32_t) * 8);
     const size_t a_scr = take(in_smem ? 0 : sizeof(uint32_t) * 2 * NWP);
-    const size_t a_big = take(sizeof(uint32_t) * P.big_words * (size_t)(block / 32));
+    const size_t a_big = take(sizeof(uint32_t) * P.big_words * (size_t)(block / 32) * grid_blocks);
+    const size_t a_gctl = take(grid ? 256 : 0);
+    const size_t a_gslots = take(grid ? 6 * sizeof(unsigned) : 0);
+    const size_t a_gchg = take(grid ? sizeof(uint32_t) * 2 * (((size_t)P.n + 31) / 32) : 0);
     uint8_t* base = device_arena(dev, off);
     const size_t stage_bytes = a_dom + sizeof(uint32_t) * NWP;
     uint8_t* stage = pinned_arena(dev, stage_bytes);
@@ -1453,15 +1471,38 @@ int run_prop(const cubics_model* h, const uint64_t* words_in, uint64_t* words_ou
     PP.result = reinterpret_cast<int32_t*>(base + a_res);
     PP.big_scratch = P.big_words ? reinterpret_cast<uint32_t*>(base + a_big) : nullptr;
     uint32_t* scr = reinterpret_cast<uint32_t*>(base + a_scr);
+    if (grid) {
+        const unsigned init[6] = {0, 0, 0, 0xffffffffu, 0xffffffffu, 0xffffffffu};
+        CU(cudaMemcpyAsync(base + a_gslots, init, sizeof init, cudaMemcpyHostToDevice, st));
+        CU(cudaMemsetAsync(base + a_gctl, 0, 256, st));
+        PP.grid_ctl = reinterpret_cast<dev_ctl_t*>(base + a_gctl);
+        PP.grid_or = reinterpret_cast<unsigned*>(base + a_gslots);
+        PP.grid_min = PP.grid_or + 3;
+        PP.grid_chg = reinterpret_cast<uint32_t*>(base + a_gchg);
+    }
+    CU(cudaEventRecord(g_dev[dev].e0, st));
+    if (grid) {
+#define LPG(w) launch_propagate_grid<w>(PP, grid_blocks, block, L.total, st, scr)
+        CUBICS_DISPATCH_W(P.W, LPG)
+#undef LPG
+    } else {
 #define LP(w) launch_propagate<w>(PP, block, L.total, st, scr, in_smem ? 1 : 0)
-    CUBICS_DISPATCH_W(P.W, LP)
+        CUBICS_DISPATCH_W(P.W, LP)
 #undef LP
+    }
+    CU(cudaEventRecord(g_dev[dev].e1, st));
     std::vector<uint32_t> res32(NWP);
     int32_t res[8] = {0};
     CU(cudaMemcpyAsync(res32.data(), removals_only ? (void*)PP.out : (void*)PP.dom, sizeof(uint32_t) * NWP,
                        cudaMemcpyDeviceToHost, st));
     CU(cudaMemcpyAsync(res, PP.result, sizeof res, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
+    if (std::getenv("CUBICS_DEBUG")) {
+        float kms = 0;
+        CU(cudaEventElapsedTime(&kms, g_dev[dev].e0, g_dev[dev].e1));
+        std::fprintf(stderr, "[cubics] propagate: %s blocks=%d block=%d prepare %.3f ms, kernel %.3f ms, rounds %d, total %.3f ms\n",
+                     grid ? "grid" : "block", grid_blocks, block, tp1 - tp0, kms, res[2], now_ms() - tp0);
+    }
     if (res[4] == DERR_OVERFLOW) throw StatusError{CUBICS_E_OVERFLOW, "overflow in linear propagation"};
     // back to the u64 reference layout
     for (int v = 0; v < m.n_vars(); ++v) {

@@ -18,6 +18,11 @@ cudaError_t launch_search_grid(const SearchParams& P, int grid, int block, size_
 template <int W>
 cudaError_t occupancy_search_grid(int block, size_t smem, int* blocks_per_sm);
 template <int W>
+cudaError_t launch_propagate_grid(const PropParams& P, int grid, int block, size_t smem, cudaStream_t st,
+                                  uint32_t* scratch);
+template <int W>
+cudaError_t occupancy_propagate_grid(int block, size_t smem, int* blocks_per_sm);
+template <int W>
 cudaError_t launch_propagate(const PropParams& P, int block, size_t smem, cudaStream_t st, uint32_t* scratch,
                              int in_smem);
 

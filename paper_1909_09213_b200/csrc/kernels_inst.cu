@@ -19,6 +19,7 @@ cudaError_t grant_smem(K k, size_t smem, size_t& granted) {
 }
 size_t g_search_smem = 48 * 1024, g_prop_smem = 48 * 1024, g_grid_smem = 48 * 1024;
 size_t g_search_smem0 = 48 * 1024, g_search_smem1 = 48 * 1024, g_parity_smem = 48 * 1024;
+size_t g_propgrid_smem = 48 * 1024;
 } // namespace
 
 // lean instantiations for narrow domains: {RelBin + small alldiff}, {+ linear}; everything else
@@ -89,6 +90,25 @@ cudaError_t launch_propagate<CUBICS_W>(const PropParams& P, int block, size_t sm
     if (e != cudaSuccess) return e;
     k<<<1, block, smem, st>>>(P, scratch, in_smem);
     return cudaGetLastError();
+}
+
+template <>
+cudaError_t launch_propagate_grid<CUBICS_W>(const PropParams& P, int grid, int block, size_t smem, cudaStream_t st,
+                                            uint32_t* scratch) {
+    auto k = dev::propagate_kernel_grid<CUBICS_W>;
+    cudaError_t e = grant_smem(k, smem, g_propgrid_smem);
+    if (e != cudaSuccess) return e;
+    PropParams p = P;
+    void* args[] = {&p, &scratch};
+    return cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(block), args, smem, st);
+}
+
+template <>
+cudaError_t occupancy_propagate_grid<CUBICS_W>(int block, size_t smem, int* out) {
+    auto k = dev::propagate_kernel_grid<CUBICS_W>;
+    cudaError_t e = grant_smem(k, smem, g_propgrid_smem);
+    if (e != cudaSuccess) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, k, block, smem);
 }
 
 } // namespace cubics

@@ -668,5 +668,49 @@ __global__ void __launch_bounds__(1024) propagate_kernel(const PropParams P, uin
     }
 }
 
+// cubics_propagate / cubics_removals for large models: one fixpoint spanning the GPU
+// (cooperative launch). Domains and removals live in L2/HBM (gscratch); every warp of the grid
+// takes propagators, so hundreds of alldifferents run side by side instead of a few per block.
+template <int W>
+__global__ void __launch_bounds__(1024) propagate_kernel_grid(const PropParams P, uint32_t* gscratch) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    GridScope sc{P.grid_or, P.grid_min};
+    Ctl& C = *P.grid_ctl;
+    const DevModel& M = P.M;
+    const int tid = sc.tid(), T = sc.nthreads();
+    const size_t NW = (size_t)M.n * W, NWP = round4(NW);
+    const SmemLayout L = smem_layout(W, M.n, M.total_members, (int)(blockDim.x >> 5), 0, false, M.na);
+    uint32_t* dom = gscratch;
+    uint32_t* rm = gscratch + NWP;
+    int16_t* mates = reinterpret_cast<int16_t*>(smem + L.mates);
+    uint32_t* chg0 = P.grid_chg;
+    RoundCtx R{dom, rm, mates, nullptr, nullptr, chg0, chg0 + ((M.n + 31) >> 5), false,
+               P.big_scratch, smem + L.scratch, L.stride, P.enabled, P.alldiff, 1};
+    for (size_t i = tid; i < NWP; i += T) {
+        dom[i] = P.dom[i];
+        rm[i] = 0;
+    }
+    for (int i = threadIdx.x; i < M.total_members; i += blockDim.x) mates[i] = -1;
+    if (tid == 0) C.err = 0;
+    sc.sync();
+    if (P.removals_only) {
+        run_propagators<W, F_ALL>(M, R, &C.err, nullptr, sc);
+        sc.sync();
+        for (size_t i = tid; i < NWP; i += T) P.out[i] = rm[i] & dom[i];
+        if (tid == 0) P.result[4] = C.err;
+        return;
+    }
+    int rounds = 0, fv = -1;
+    const int st = block_fixpoint<W, F_ALL>(M, R, &C.err, &C.min, P.max_rounds, &rounds, &fv, true, sc);
+    for (size_t i = tid; i < NWP; i += T) P.dom[i] = dom[i];
+    if (tid == 0) {
+        P.result[0] = st == R_FAILED;
+        P.result[1] = st == R_FAILED ? fv : -1;
+        P.result[2] = rounds;
+        P.result[3] = st == R_ERROR ? 0 : st;
+        P.result[4] = C.err;
+    }
+}
+
 } // namespace dev
 } // namespace cubics
