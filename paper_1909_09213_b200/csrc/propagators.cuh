@@ -954,15 +954,32 @@ __device__ inline bool big_augment(int r, int n, int uw, const BigScratch& S, in
         const int32_t* fr = S.fl + (size_t)cur * n;
         bool any = false;
         int found = 0x7fffffff;
-        for (int w = lane; w < uw; w += 32) {
-            uint32_t acc = 0;
-            for (int i = 0; i < c; ++i) acc |= S.D[(size_t)fr[i] * uw + w];
-            const uint32_t x = acc & ~vis[w];
-            nv[w] = x;
-            vis[w] |= x;
-            any |= x != 0;
-            const uint32_t f = x & ~MV[w];
-            if (f && found == 0x7fffffff) found = w * 32 + __ffs(f) - 1;
+        if (uw <= 4) { // narrow universe: frontier members over the lanes, one word at a time
+            for (int w = 0; w < uw; ++w) {
+                uint32_t acc = 0;
+                for (int i = lane; i < c; i += 32) acc |= S.D[(size_t)fr[i] * uw + w];
+                acc = __reduce_or_sync(FULL, acc);
+                const uint32_t x = acc & ~vis[w];
+                __syncwarp();
+                if (lane == 0) {
+                    nv[w] = x;
+                    vis[w] |= x;
+                }
+                any |= x != 0;
+                const uint32_t f = x & ~MV[w];
+                if (f && found == 0x7fffffff) found = w * 32 + __ffs(f) - 1;
+            }
+        } else {
+            for (int w = lane; w < uw; w += 32) {
+                uint32_t acc = 0;
+                for (int i = 0; i < c; ++i) acc |= S.D[(size_t)fr[i] * uw + w];
+                const uint32_t x = acc & ~vis[w];
+                nv[w] = x;
+                vis[w] |= x;
+                any |= x != 0;
+                const uint32_t f = x & ~MV[w];
+                if (f && found == 0x7fffffff) found = w * 32 + __ffs(f) - 1;
+            }
         }
         any = __any_sync(FULL, any);
         found = __reduce_min_sync(FULL, (unsigned)found);
@@ -1039,14 +1056,18 @@ __device__ void prop_alldiff_gac_big(const DevModel& M, int a, const uint32_t* d
     big_load<W>(M, a, dom, S, n, uw, lane);
     for (int w = lane; w < uw; w += 32) MV[w] = 0;
     __syncwarp();
+    bool kept = false;
     for (int k = lane; k < n; k += 32) { // warm start: keep still-valid matched edges
         int m = mates[k];
         if (m >= 0 && !bit_of(S.D + (size_t)k * uw, m)) m = mates[k] = -1;
         if (m >= 0) {
             atomicOr(MV + (m >> 5), 1u << (m & 31));
             S.owner[m] = k;
+            kept = true;
         }
     }
+    // from an empty matching the loop below IS the greedy in member order (Kuhn's first failure)
+    kept = __any_sync(FULL, kept);
     __syncwarp();
     int fail = -1;
     for (int base = 0; base < n && fail < 0; base += 32) {
@@ -1061,7 +1082,7 @@ __device__ void prop_alldiff_gac_big(const DevModel& M, int a, const uint32_t* d
         }
     }
     if (fail >= 0) {
-        if (exact_wipe) { // greedy matching in member order: its first failure is Kuhn's
+        if (exact_wipe && kept) { // greedy matching in member order: its first failure is Kuhn's
             for (int k = lane; k < n; k += 32) mates[k] = -1;
             for (int w = lane; w < uw; w += 32) MV[w] = 0;
             __syncwarp();
@@ -1082,11 +1103,23 @@ __device__ void prop_alldiff_gac_big(const DevModel& M, int a, const uint32_t* d
         return;
     }
     // free values, predecessor rows, seeds, pivots
-    for (int w = lane; w < uw; w += 32) {
-        uint32_t u = 0;
-        for (int k = 0; k < n; ++k) u |= S.D[(size_t)k * uw + w];
-        F[w] = u & ~MV[w];
-        KEEP[w] = F[w];
+    if (uw <= 4) {
+        for (int w = 0; w < uw; ++w) {
+            uint32_t u = 0;
+            for (int k = lane; k < n; k += 32) u |= S.D[(size_t)k * uw + w];
+            u = __reduce_or_sync(FULL, u);
+            if (lane == 0) {
+                F[w] = u & ~MV[w];
+                KEEP[w] = F[w];
+            }
+        }
+    } else {
+        for (int w = lane; w < uw; w += 32) {
+            uint32_t u = 0;
+            for (int k = 0; k < n; ++k) u |= S.D[(size_t)k * uw + w];
+            F[w] = u & ~MV[w];
+            KEEP[w] = F[w];
+        }
     }
     for (int i = lane; i < 2 * nwm; i += 32) S.mset[i] = 0;
     __syncwarp();
