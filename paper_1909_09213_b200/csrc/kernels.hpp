@@ -14,6 +14,8 @@ cudaError_t launch_search(const SearchParams& P, int feat, int grid, int block, 
 template <int W>
 cudaError_t occupancy_search(int feat, int block, size_t smem, int* blocks_per_sm);
 template <int W>
+cudaError_t launch_search_parity(const SearchParams& P, int grid, int block, size_t smem, cudaStream_t st);
+template <int W>
 cudaError_t launch_search_grid(const SearchParams& P, int grid, int block, size_t smem, cudaStream_t st);
 template <int W>
 cudaError_t occupancy_search_grid(int block, size_t smem, int* blocks_per_sm);

@@ -5,6 +5,12 @@
 #ifndef CUBICS_W
 #error "compile with -DCUBICS_W=<1|2|4|8|16|32>"
 #endif
+// CUBICS_PART splits one W into translation units by kernel family (the W=32 kernels take
+// minutes each in ptxas): 0 generic search, 1 parity search, 2 grid search, 3 propagation.
+#ifndef CUBICS_PART
+#define CUBICS_PART -1 // everything
+#endif
+#define CUBICS_HAS_PART(p) (CUBICS_PART < 0 || CUBICS_PART == (p))
 
 namespace cubics {
 
@@ -22,6 +28,7 @@ size_t g_search_smem0 = 48 * 1024, g_search_smem1 = 48 * 1024, g_parity_smem = 4
 size_t g_propgrid_smem = 48 * 1024;
 } // namespace
 
+#if CUBICS_HAS_PART(0)
 // lean instantiations for narrow domains: {RelBin + small alldiff}, {+ linear}; everything else
 // (tables, large alldifferents, the first-solution bookkeeping, wide domains) runs the full kernel
 namespace {
@@ -41,13 +48,7 @@ cudaError_t launch_search<CUBICS_W>(const SearchParams& P, int feat, int grid, i
                                     cudaStream_t st) {
     // the generic block kernel also runs one-warp contexts: a __syncwarp-specialised variant
     // measured slower on B200 (19.3 vs 14.0 ms on nq14; register spills at the 64-register cap)
-    if (P.mode == MODE_PARITY && block <= 512) {
-        auto k = dev::search_kernel_parity<CUBICS_W>;
-        cudaError_t e = grant_smem(k, smem, g_parity_smem);
-        if (e != cudaSuccess) return e;
-        k<<<grid, block, smem, st>>>(P);
-        return cudaGetLastError();
-    }
+    if (P.mode == MODE_PARITY && block <= 512) return launch_search_parity<CUBICS_W>(P, grid, block, smem, st);
     if (P.batch) return cudaErrorInvalidConfiguration; // batched B&B runs in the parity kernel only
     SearchFn k = pick_search(feat);
     cudaError_t e = grant_smem(k, smem, feat == 0 ? g_search_smem0 : (feat == dev::F_LINEAR ? g_search_smem1 : g_search_smem));
@@ -63,7 +64,20 @@ cudaError_t occupancy_search<CUBICS_W>(int feat, int block, size_t smem, int* ou
     if (e != cudaSuccess) return e;
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, k, block, smem);
 }
+#endif
 
+#if CUBICS_HAS_PART(1)
+template <>
+cudaError_t launch_search_parity<CUBICS_W>(const SearchParams& P, int grid, int block, size_t smem, cudaStream_t st) {
+    auto k = dev::search_kernel_parity<CUBICS_W>;
+    cudaError_t e = grant_smem(k, smem, g_parity_smem);
+    if (e != cudaSuccess) return e;
+    k<<<grid, block, smem, st>>>(P);
+    return cudaGetLastError();
+}
+#endif
+
+#if CUBICS_HAS_PART(2)
 template <>
 cudaError_t launch_search_grid<CUBICS_W>(const SearchParams& P, int grid, int block, size_t smem, cudaStream_t st) {
     auto k = dev::search_kernel_grid<CUBICS_W>;
@@ -82,6 +96,9 @@ cudaError_t occupancy_search_grid<CUBICS_W>(int block, size_t smem, int* out) {
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, k, block, smem);
 }
 
+#endif
+
+#if CUBICS_HAS_PART(3)
 template <>
 cudaError_t launch_propagate<CUBICS_W>(const PropParams& P, int block, size_t smem, cudaStream_t st,
                                        uint32_t* scratch, int in_smem) {
@@ -110,5 +127,7 @@ cudaError_t occupancy_propagate_grid<CUBICS_W>(int block, size_t smem, int* out)
     if (e != cudaSuccess) return e;
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, k, block, smem);
 }
+
+#endif
 
 } // namespace cubics
