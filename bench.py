@@ -256,10 +256,26 @@ def impl_ours(args):
     cfg = S.SearchConfig(engine=A.ENGINE_PARALLEL, device=device, count_only=True, contexts=args.contexts,
                          block_threads=args.block)
 
+    # N > 1: frontier subtrees are claimed dynamically through one counter in rank 0's HBM that
+    # every rank maps over NVLink (CUDA IPC); CUBICS_BENCH_STATIC=1 selects the static t % N split
+    queue = None
+    if world > 1 and os.environ.get("CUBICS_BENCH_STATIC", "0") != "1":
+        from paper_1909_09213_b200 import distributed as D
+
+        try:  # collective; every rank gets the same outcome
+            queue = D.shared_task_queue(rank, world, device)
+        except S.EngineUnavailable as e:
+            if rank == 0:
+                print(f"shared task queue unavailable, static split: {e}", file=sys.stderr)
+
     def one_step(count_only=True):
         c = S.SearchConfig(**{**cfg.__dict__, "count_only": count_only})
         if world > 1:
-            return S.solve_shard(model, c, rank, world)
+            if queue is not None:
+                if rank == 0:
+                    queue.reset()
+                dist.barrier()
+            return S.solve_shard(model, c, rank, world, queue=queue)
         return S.solve_satisfy(model, c, (lambda s: True) if not count_only else None)
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{device}")  # > 126 MB L2
@@ -307,13 +323,14 @@ def impl_ours(args):
             flush_l2()
             barrier()
             t0 = time.perf_counter()
-            st, _, _ = D.solve_distributed(model, cfg, rank, world, collect=False, device=coll_dev)
+            st, _, _ = D.solve_distributed(model, cfg, rank, world, collect=False, device=coll_dev, queue=queue)
             e2e_ms.append((time.perf_counter() - t0) * 1e3)
             assert tuple(st) == tot.as_tuple()
         e2e_ms = max_over_ranks(e2e_ms)
         h2d, d2h = r.h2d_bytes, r.d2h_bytes
         e2e_launches = r.kernel_launches
-        e2e_api = "distributed.solve_distributed (cubics_solve_shard per rank + all-reduce of the stats)"
+        e2e_api = ("distributed.solve_distributed (cubics_solve_shard%s per rank + all-reduce of the stats)"
+                   % ("_shared" if queue is not None else ""))
     extras = run_extras(S, A, device) if (rank == 0 and not args.no_extras) else None
     nodes = tot.nodes
     if rank != 0:
@@ -338,6 +355,10 @@ def impl_ours(args):
         "vs_baseline": None, "dtype": "int64", "data": "synthetic",
         "config": {"workload": f"{args.instance} all solutions (N-Queens n=14, BASELINE configs[1])",
                    "engine": "parallel", "contexts": r.contexts, "l2": "flushed (256 MiB write) before every timed step",
+                   "balancing": ("in-GPU work-sharing ring" if world == 1 else
+                                 "shared subtree queue (claim counter in rank 0 HBM, CUDA IPC over NVLink) + "
+                                 "in-GPU work-sharing ring" if queue is not None else
+                                 "static t % N frontier split + in-GPU work-sharing ring"),
                    "stats": {"nodes": tot.nodes, "failures": tot.failures, "rounds": tot.rounds,
                              "solutions": tot.solutions}},
         "time_to_all_solutions_ms": mean_ms,

@@ -20,6 +20,8 @@
  *   cubics_model_parse         fd::parse_model          include/fd/parser.hpp:38 (host-side loader)
  *   cubics_model_validate      fd::model_validate       include/fd/model.hpp:93
  *   cubics_solve_shard         (new) one rank's share of a multi-GPU search; SURVEY.md 8(e)
+ *   cubics_solve_shard_shared  (new) the same, subtrees claimed dynamically from a shared
+ *   cubics_task_queue_*              queue over NVLink peer memory; SURVEY.md 8(e)
  *
  * Threading: every call is synchronous and blocks until the device finishes. Calls on
  * different models may run from different host threads. Error details for the last failing
@@ -219,6 +221,28 @@ typedef int32_t (*cubics_keyed_solution_cb)(void* user, const uint32_t* key, int
 int cubics_solve_shard(const cubics_model* m, const cubics_search_config* cfg,
                        int32_t shard_index, int32_t shard_count,
                        cubics_keyed_solution_cb cb, void* user, cubics_result* out);
+
+/* Dynamic cross-GPU balancing: a shared task queue is one claim counter in the
+ * owner GPU's HBM. Rank 0 creates it and sends the CUBICS_TASK_QUEUE_HANDLE_BYTES-byte handle
+ * to the other ranks (any transport; torch.distributed in distributed.py), which open it: CUDA
+ * IPC maps it into their address space and the driver enables NVLink peer access.
+ * cubics_solve_shard_shared then seeds EVERY frontier subtree on every rank (DFS order) and an
+ * idle search context claims the next one with a system-scope atomicAdd on the counter over
+ * NVLink; once the counter passes the task count the contexts fall back to the in-GPU
+ * work-sharing ring. Each subtree is searched exactly once across the ranks, so stats sum
+ * exactly as for cubics_solve_shard. The counter must be reset (cubics_task_queue_reset on the
+ * owner, then a barrier) before every search that uses it. A queue opened in the creating
+ * process is not supported by CUDA IPC: pass the creator's queue to every local call instead. */
+#define CUBICS_TASK_QUEUE_HANDLE_BYTES 64
+typedef struct cubics_task_queue cubics_task_queue; /* opaque */
+int cubics_task_queue_create(int32_t device, cubics_task_queue** out, uint8_t* handle /* may be NULL */);
+int cubics_task_queue_open(int32_t device, const uint8_t* handle, cubics_task_queue** out);
+int cubics_task_queue_reset(cubics_task_queue* q);
+int cubics_task_queue_claims(cubics_task_queue* q, uint64_t* claims); /* claim attempts so far */
+int cubics_task_queue_destroy(cubics_task_queue* q);
+int cubics_solve_shard_shared(const cubics_model* m, const cubics_search_config* cfg,
+                              int32_t shard_index, int32_t shard_count, cubics_task_queue* queue,
+                              cubics_keyed_solution_cb cb, void* user, cubics_result* out);
 
 /* ---- propagation (kernel-level API) ------------------------------------------------------ */
 typedef struct cubics_fixpoint_result { /* fd::FixpointResult (propagation.hpp:106-110) */

@@ -155,6 +155,10 @@ struct SearchParams {
     uint32_t* tasks;          // [task_cap][OS] same layout as an outbox slot
     // seeded parallel run: outbox slots [n_ctx, n_ctx + n_seed) hold pre-published tasks
     int32_t n_seed;
+    // shared task queue (cubics_solve_shard_shared): the n_seed tasks are NOT pre-published;
+    // an idle context claims seed i = atomicAdd_system(task_claim, 1) (a counter that may live
+    // in a peer GPU's memory, mapped over NVLink) until i >= n_seed, then joins the ring
+    unsigned int* task_claim;
     // exact parallel first solution (max_solutions == 1): every subtree handed out ("segment",
     // id = ring ticket + 1; the root is segment 0) records its root path key and its own stats;
     // solutions record their segment and segment-local stats; subtrees right of the best

@@ -546,6 +546,7 @@ struct ShardIO {
     uint32_t* task_dev = nullptr; // [task_cap][OS] device buffer (arena slot 1)
     uint64_t n_tasks = 0;         // out: tasks emitted
     const std::vector<int32_t>* seeds = nullptr; // seeded run: task indices of this shard
+    unsigned int* claim = nullptr; // shared queue: seeds are claimed through this counter instead
 };
 
 // Batched B&B (cubics_solve_optimize_batch): problem i = block i, reference node order.
@@ -711,10 +712,11 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
     {
         // staging: blob + initial WorkState in pinned memory, one H2D copy
         WorkState w0{};
-        w0.outstanding = n_ctx + n_seed;
+        const bool shared_q = shard && shard->claim;
+        w0.outstanding = n_ctx + (shared_q ? 0 : n_seed);
         w0.hot.has_bound = first_mode ? -1 : (cfg.has_initial_bound ? 1 : 0);
         w0.bound = cfg.initial_bound;
-        w0.hot.push_ticket = (uint32_t)n_seed;
+        w0.hot.push_ticket = shared_q ? 0u : (uint32_t)n_seed;
         const size_t stage_bytes = a_ws + sizeof(WorkState);
         uint8_t* stage = pinned_arena(dev, stage_bytes);
         std::memset(stage, 0, stage_bytes);
@@ -728,11 +730,14 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
             CU(cudaMemsetAsync(base + a_segs, 0, sizeof(uint64_t) * 3 * seg_cap, st));
         }
         if (n_seed) { // pre-published tasks: ring tickets 0..n_seed-1 point at outbox slots n_ctx+i
-            std::vector<unsigned long long> ring0(n_seed);
-            for (int i = 0; i < n_seed; ++i) ring0[i] = ((unsigned long long)(i + 1) << 32) | (unsigned)(n_ctx + i);
-            CU(cudaMemcpyAsync(base + a_queue, ring0.data(), sizeof(unsigned long long) * n_seed, cudaMemcpyHostToDevice, st));
+            if (!shared_q) {
+                std::vector<unsigned long long> ring0(n_seed);
+                for (int i = 0; i < n_seed; ++i) ring0[i] = ((unsigned long long)(i + 1) << 32) | (unsigned)(n_ctx + i);
+                CU(cudaMemcpyAsync(base + a_queue, ring0.data(), sizeof(unsigned long long) * n_seed, cudaMemcpyHostToDevice, st));
+                out.h2d += sizeof(unsigned long long) * n_seed;
+            }
             CU(cudaMemcpyAsync(base + a_seedidx, shard->seeds->data(), sizeof(int32_t) * n_seed, cudaMemcpyHostToDevice, st));
-            out.h2d += (sizeof(unsigned long long) + sizeof(int32_t)) * n_seed;
+            out.h2d += sizeof(int32_t) * n_seed;
             const size_t total = (size_t)n_seed * OS;
             gather_tasks<<<(int)std::min<size_t>(4096, (total + 255) / 256), 256, 0, st>>>(
                 shard->task_dev, reinterpret_cast<const int32_t*>(base + a_seedidx), n_seed, OS,
@@ -795,6 +800,7 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
         S.task_cap = shard ? (int64_t)shard->task_cap : 0;
         S.tasks = shard ? shard->task_dev : nullptr;
         S.n_seed = n_seed;
+        S.task_claim = shard ? shard->claim : nullptr;
         S.first_mode = first_mode ? 1 : 0;
         S.seg_cap = seg_cap;
         S.seg_key = reinterpret_cast<uint32_t*>(base + a_segk);
@@ -1267,8 +1273,12 @@ extern "C" int cubics_solve_optimize_batch(const cubics_model* h, const cubics_s
     });
 }
 
-extern "C" int cubics_solve_shard(const cubics_model* h, const cubics_search_config* cfg, int32_t shard_index,
-                                  int32_t shard_count, cubics_keyed_solution_cb cb, void* user, cubics_result* out) {
+namespace {
+// claim == nullptr: static split (task t goes to shard t % shard_count); otherwise every shard
+// seeds all tasks in DFS order and claims them dynamically through the shared counter
+int solve_shard_impl(const cubics_model* h, const cubics_search_config* cfg, int32_t shard_index,
+                     int32_t shard_count, unsigned int* claim, cubics_keyed_solution_cb cb, void* user,
+                     cubics_result* out) {
     if (!h || !cfg || !out || shard_count < 1 || shard_index < 0 || shard_index >= shard_count) return CUBICS_E_INVALID;
     return guarded([&]() -> int {
         const double t0 = now_ms();
@@ -1335,13 +1345,17 @@ extern "C" int cubics_solve_shard(const cubics_model* h, const cubics_search_con
                                                 keys.begin() + (size_t)y * KW, keys.begin() + (size_t)(y + 1) * KW);
         });
         std::vector<int32_t> mine;
-        for (uint64_t r = shard_index; r < nt; r += shard_count) mine.push_back(order[r]);
+        if (claim)
+            mine = order;
+        else
+            for (uint64_t r = shard_index; r < nt; r += shard_count) mine.push_back(order[r]);
         // 3. this shard's subtrees, seeded into the parallel engine
         RunOut run;
         if (!mine.empty()) {
             ShardIO seeded;
             seeded.task_dev = io.task_dev;
             seeded.seeds = &mine;
+            seeded.claim = claim;
             run_search(m, c, CUBICS_ENGINE_PARALLEL, record, record ? default_sol_cap(m, c) : 0, run, true, &seeded);
         }
         fill_result(run, out);
@@ -1365,6 +1379,95 @@ extern "C" int cubics_solve_shard(const cubics_model* h, const cubics_search_con
             if (!mine.empty()) deliver(run);
         }
         out->total_ms = now_ms() - t0;
+        return CUBICS_OK;
+    });
+}
+} // namespace
+
+extern "C" int cubics_solve_shard(const cubics_model* h, const cubics_search_config* cfg, int32_t shard_index,
+                                  int32_t shard_count, cubics_keyed_solution_cb cb, void* user, cubics_result* out) {
+    return solve_shard_impl(h, cfg, shard_index, shard_count, nullptr, cb, user, out);
+}
+
+extern "C" int cubics_solve_shard_shared(const cubics_model* h, const cubics_search_config* cfg, int32_t shard_index,
+                                         int32_t shard_count, cubics_task_queue* queue, cubics_keyed_solution_cb cb,
+                                         void* user, cubics_result* out) {
+    if (!queue) return CUBICS_E_INVALID;
+    return solve_shard_impl(h, cfg, shard_index, shard_count, reinterpret_cast<unsigned int*>(queue->counter), cb, user,
+                            out);
+}
+
+// Shared task queue: one u32 claim counter in the owner GPU's HBM, mapped into the other ranks'
+// address spaces with CUDA IPC (peer access over NVLink enabled lazily by the driver).
+extern "C" int cubics_task_queue_create(int32_t device, cubics_task_queue** out, uint8_t* handle) {
+    if (!out) return CUBICS_E_INVALID;
+    *out = nullptr;
+    return guarded([&]() -> int {
+        const int dev = current_device(device);
+        CU(cudaSetDevice(dev));
+        void* p = nullptr;
+        CU(cudaMalloc(&p, 256));
+        CU(cudaMemset(p, 0, 256));
+        if (handle) {
+            cudaIpcMemHandle_t hd;
+            cudaError_t e = cudaIpcGetMemHandle(&hd, p);
+            if (e != cudaSuccess) {
+                cudaFree(p);
+                CU(e);
+            }
+            static_assert(sizeof hd == CUBICS_TASK_QUEUE_HANDLE_BYTES, "IPC handle size");
+            std::memcpy(handle, &hd, sizeof hd);
+        }
+        *out = new cubics_task_queue{p, dev, 1};
+        return CUBICS_OK;
+    });
+}
+
+extern "C" int cubics_task_queue_open(int32_t device, const uint8_t* handle, cubics_task_queue** out) {
+    if (!out || !handle) return CUBICS_E_INVALID;
+    *out = nullptr;
+    return guarded([&]() -> int {
+        const int dev = current_device(device);
+        CU(cudaSetDevice(dev));
+        cudaIpcMemHandle_t hd;
+        std::memcpy(&hd, handle, sizeof hd);
+        void* p = nullptr;
+        CU(cudaIpcOpenMemHandle(&p, hd, cudaIpcMemLazyEnablePeerAccess));
+        *out = new cubics_task_queue{p, dev, 0};
+        return CUBICS_OK;
+    });
+}
+
+extern "C" int cubics_task_queue_reset(cubics_task_queue* q) {
+    if (!q) return CUBICS_E_INVALID;
+    return guarded([&]() -> int {
+        CU(cudaSetDevice(q->device));
+        CU(cudaMemset(q->counter, 0, 256));
+        CU(cudaDeviceSynchronize());
+        return CUBICS_OK;
+    });
+}
+
+extern "C" int cubics_task_queue_claims(cubics_task_queue* q, uint64_t* claims) {
+    if (!q || !claims) return CUBICS_E_INVALID;
+    return guarded([&]() -> int {
+        CU(cudaSetDevice(q->device));
+        uint32_t v = 0;
+        CU(cudaMemcpy(&v, q->counter, sizeof v, cudaMemcpyDeviceToHost));
+        *claims = v;
+        return CUBICS_OK;
+    });
+}
+
+extern "C" int cubics_task_queue_destroy(cubics_task_queue* q) {
+    if (!q) return CUBICS_OK;
+    return guarded([&]() -> int {
+        cudaSetDevice(q->device);
+        if (q->owner)
+            cudaFree(q->counter);
+        else
+            cudaIpcCloseMemHandle(q->counter);
+        delete q;
         return CUBICS_OK;
     });
 }

@@ -14,34 +14,32 @@
 
 namespace cubics {
 
-namespace {
+// internal linkage by `static`, not an anonymous namespace: nvcc names anonymous namespaces after
+// the source file, and every (W, part) object is built from this same file
 // cudaFuncSetAttribute only when a launch needs more dynamic shared memory than already granted
 template <class K>
-cudaError_t grant_smem(K k, size_t smem, size_t& granted) {
+static cudaError_t grant_smem(K k, size_t smem, size_t& granted) {
     if (smem <= granted) return cudaSuccess;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess) granted = smem;
     return e;
 }
-size_t g_search_smem = 48 * 1024, g_prop_smem = 48 * 1024, g_grid_smem = 48 * 1024;
-size_t g_search_smem0 = 48 * 1024, g_search_smem1 = 48 * 1024, g_parity_smem = 48 * 1024;
-size_t g_propgrid_smem = 48 * 1024;
-} // namespace
+static size_t g_search_smem = 48 * 1024, g_prop_smem = 48 * 1024, g_grid_smem = 48 * 1024;
+static size_t g_search_smem0 = 48 * 1024, g_search_smem1 = 48 * 1024, g_parity_smem = 48 * 1024;
+static size_t g_propgrid_smem = 48 * 1024;
 
 #if CUBICS_HAS_PART(0)
 // lean instantiations for narrow domains: {RelBin + small alldiff}, {+ linear}; everything else
 // (tables, large alldifferents, the first-solution bookkeeping, wide domains) runs the full kernel
-namespace {
 using SearchFn = void (*)(const SearchParams);
 
-SearchFn pick_search(int feat) {
+static SearchFn pick_search(int feat) {
     if constexpr (CUBICS_W <= 4) {
         if (feat == 0) return dev::search_kernel<CUBICS_W, 0>;
         if (feat == dev::F_LINEAR) return dev::search_kernel<CUBICS_W, dev::F_LINEAR>;
     }
     return dev::search_kernel<CUBICS_W, dev::F_ALL>;
 }
-} // namespace
 
 template <>
 cudaError_t launch_search<CUBICS_W>(const SearchParams& P, int feat, int grid, int block, size_t smem,

@@ -44,3 +44,9 @@ const char* last_error();
 struct cubics_model {
     cubics::HostModel m;
 };
+
+struct cubics_task_queue {
+    void* counter; // device pointer in this process (owned allocation or IPC mapping)
+    int device;    // device the calling process uses it from
+    int owner;     // 1: cudaMalloc'd here; 0: opened from an IPC handle
+};

@@ -74,6 +74,14 @@ __device__ __forceinline__ void copy4_cg(uint32_t* dst, const uint32_t* src, siz
     for (size_t i = tid; i < nwords / 4; i += T) d[i] = __ldcg(s + i);
 }
 
+// Shared task queue (cubics_solve_shard_shared): claim the next seeded subtree; the counter may
+// live in a peer GPU's HBM (CUDA IPC mapping), hence the system-scope atomic over NVLink.
+// Out of line: it runs once per claimed subtree and must not cost the search loop registers.
+static __device__ __noinline__ int claim_task(unsigned int* counter, int n_seed, int n_ctx) {
+    const unsigned i = atomicAdd_system(counter, 1u);
+    return i < (unsigned)n_seed ? n_ctx + (int)i : -1;
+}
+
 // DFS path key: decision at depth d is bit (31 - d%32) of word d/32, so comparing the words as
 // unsigned integers, most significant first, is the reference's DFS (preorder) order.
 // path_right_word: word i of the key of the right child taken at depth d (prefix [0,d) kept,
@@ -210,30 +218,36 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
 
     // Idle: take a ticket and wait for the task published under it (lock-free ticket queue:
     // each waiter spins on its own ring slot, so there is no shared hot spot to contend on).
+    bool claim_open = P.task_claim != nullptr; // thread 0: shared queue not yet drained
     auto get_work = [&]() -> bool {
         if (tid == 0) {
             const long long t0 = clock64();
-            atomicSub(&ws->outstanding, 1);
-            const uint32_t t = atomicAdd(&ws->hot.pop_ticket, 1u);
-            const unsigned long long* slot = P.ring + (t % P.ring_cap);
-            int got = -1, ns = 32;
-            for (int it = 0;; ++it) {
-                const unsigned long long v = ld_volatile_u64(slot);
-                if ((uint32_t)(v >> 32) == t + 1u) {
-                    got = (int)(v & 0xffffffffu);
-                    break;
-                }
-                if ((it & 7) == 7 && (ld_volatile(&ws->hot.stop) || ld_volatile(&ws->outstanding) == 0)) break;
-                __nanosleep(ns);
-                ns = ns < 1024 ? ns * 2 : ns;
-            }
+            // shared queue first (claiming keeps this context outstanding), then the ring
+            int got = claim_open ? claim_task(P.task_claim, P.n_seed, P.n_ctx) : -1;
             if (got >= 0) {
-                __threadfence();
-                ++steals;
+                s_ll = -1;
+            } else {
+                claim_open = false;
+                atomicSub(&ws->outstanding, 1);
+                const uint32_t t = atomicAdd(&ws->hot.pop_ticket, 1u);
+                const unsigned long long* slot = P.ring + (t % P.ring_cap);
+                int ns = 32;
+                for (int it = 0;; ++it) {
+                    const unsigned long long v = ld_volatile_u64(slot);
+                    if ((uint32_t)(v >> 32) == t + 1u) {
+                        got = (int)(v & 0xffffffffu);
+                        break;
+                    }
+                    if ((it & 7) == 7 && (ld_volatile(&ws->hot.stop) || ld_volatile(&ws->outstanding) == 0)) break;
+                    __nanosleep(ns);
+                    ns = ns < 1024 ? ns * 2 : ns;
+                }
+                if (got >= 0) __threadfence();
+                s_ll = (long long)t + 1; // segment id of the subtree published under ticket t
             }
+            if (got >= 0) ++steals;
             idle_cyc += clock64() - t0;
             s_src = got;
-            s_ll = (long long)t + 1; // segment id of the subtree published under ticket t
         }
         sc.sync();
         const int got = s_src;

@@ -6,6 +6,11 @@ t with t % world == r with the in-GPU parallel engine (dynamic work sharing acro
 contexts). Nodes above the frontier are counted by rank 0 only, so a single all-reduce (sum) of
 (nodes, failures, rounds, solutions) gives exactly the reference's stats. Solutions carry their
 DFS path key; rank 0 merges the ranks' key-sorted streams into the reference's solution order.
+
+With a shared TaskQueue (shared_task_queue) the split is dynamic instead: every rank seeds all
+frontier subtrees and claims them one at a time through one counter in rank 0's HBM, mapped into
+the other ranks with CUDA IPC and incremented with system-scope atomics over NVLink; the stats
+still sum exactly because each subtree is claimed exactly once.
 """
 from __future__ import annotations
 
@@ -14,15 +19,41 @@ import heapq
 from . import solver as S
 
 
-def _collect_shard(model, cfg, rank, world, collect):
+def _collect_shard(model, cfg, rank, world, collect, queue=None):
     sols = []
 
     def cb(key, values):
         sols.append((tuple(key), values))
         return True
 
-    r = S.solve_shard(model, cfg, rank, world, cb if collect else None)
+    r = S.solve_shard(model, cfg, rank, world, cb if collect else None, queue=queue)
     return r, sols
+
+
+def shared_task_queue(rank: int, world: int, device: int = -1):
+    """Collective: rank 0 creates the shared subtree queue on its GPU and broadcasts the IPC
+    handle over the default process group; every other rank maps it. Returns a TaskQueue."""
+    import torch.distributed as dist
+
+    q = S.TaskQueue.create(device) if rank == 0 else None
+    if world == 1:
+        return q
+    box = [q.handle if q is not None else None]
+    dist.broadcast_object_list(box, src=0)
+    err = None
+    if rank != 0:
+        try:
+            q = S.TaskQueue.open(box[0], device)
+        except (S.EngineUnavailable, ValueError) as e:  # e.g. no peer access between these GPUs
+            err = f"rank {rank}: {e}"
+    errs = [None] * world
+    dist.all_gather_object(errs, err)
+    bad = [e for e in errs if e]
+    if bad:  # every rank must agree, or subtrees would be searched twice
+        if q is not None:
+            q.close()
+        raise S.EngineUnavailable("shared task queue unavailable: " + "; ".join(bad))
+    return q
 
 
 def merge_keyed(streams):
@@ -31,18 +62,25 @@ def merge_keyed(streams):
 
 
 def solve_distributed(model, cfg: S.SearchConfig, rank: int, world: int, collect: bool = True,
-                      shard_fn=None, device=None):
+                      shard_fn=None, device=None, queue=None):
     """Run this rank's shard and combine over the default torch.distributed process group.
 
     Returns (stats tuple, solutions in DFS order or None on ranks != 0, max device ms over ranks).
     shard_fn(model, cfg, rank, world, collect) -> (SatisfyResult, [(key, values)]) may replace
     the GPU shard (tests use it to exercise the collective plumbing on CPU/gloo).
+    queue (from shared_task_queue) switches to dynamic subtree claiming; it is reset here.
     """
     import torch
     import torch.distributed as dist
 
-    fn = shard_fn or _collect_shard
-    r, sols = fn(model, cfg, rank, world, collect)
+    if queue is not None:
+        if rank == 0:
+            queue.reset()
+        dist.barrier()
+        r, sols = _collect_shard(model, cfg, rank, world, collect, queue=queue)
+    else:
+        fn = shard_fn or _collect_shard
+        r, sols = fn(model, cfg, rank, world, collect)
     dev = device if device is not None else "cpu"
     t = torch.tensor(list(r.stats.as_tuple()), dtype=torch.int64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)

@@ -564,16 +564,61 @@ def lns_optimize(model: Model, cfg: LnsConfig | None = None) -> LnsResult:
     return res
 
 
-def solve_shard(model: Model, cfg: SearchConfig, shard_index: int, shard_count: int, cb=None):
-    """One rank's share of a multi-GPU search (cubics_solve_shard); cb(key_words, values)."""
+class TaskQueue:
+    """Shared subtree queue for cubics_solve_shard_shared: one claim counter in the owner GPU's
+    HBM. The owner creates it and ships `handle` (64 bytes) to the other ranks, which `open` it
+    (CUDA IPC; NVLink peer access). reset() (owner) + a barrier must precede every search."""
+
+    def __init__(self, ptr, handle: bytes, owner: bool):
+        self.ptr, self.handle, self.owner = ptr, handle, owner
+
+    @classmethod
+    def create(cls, device: int = -1) -> "TaskQueue":
+        ptr = C.c_void_p()
+        buf = C.create_string_buffer(A.TASK_QUEUE_HANDLE_BYTES)
+        _check(lib().cubics_task_queue_create(device, C.byref(ptr), buf), "task_queue_create")
+        return cls(ptr, buf.raw, True)
+
+    @classmethod
+    def open(cls, handle: bytes, device: int = -1) -> "TaskQueue":
+        if len(handle) != A.TASK_QUEUE_HANDLE_BYTES:
+            raise ValueError("task queue handle must be %d bytes" % A.TASK_QUEUE_HANDLE_BYTES)
+        ptr = C.c_void_p()
+        _check(lib().cubics_task_queue_open(device, handle, C.byref(ptr)), "task_queue_open")
+        return cls(ptr, bytes(handle), False)
+
+    def reset(self):
+        _check(lib().cubics_task_queue_reset(self.ptr), "task_queue_reset")
+
+    def claims(self) -> int:
+        v = C.c_uint64()
+        _check(lib().cubics_task_queue_claims(self.ptr, C.byref(v)), "task_queue_claims")
+        return v.value
+
+    def close(self):
+        if self.ptr:
+            lib().cubics_task_queue_destroy(self.ptr)
+            self.ptr = None
+
+
+def solve_shard(model: Model, cfg: SearchConfig, shard_index: int, shard_count: int, cb=None,
+                queue: TaskQueue | None = None):
+    """One rank's share of a multi-GPU search; cb(key_words, values).
+
+    queue=None: cubics_solve_shard (static split of the frontier subtrees). With a TaskQueue:
+    cubics_solve_shard_shared (subtrees claimed dynamically through the shared counter)."""
     def trampoline(_u, key, kw, vals, n):
         return 1 if cb([key[i] for i in range(kw)], [vals[i] for i in range(n)]) else 0
 
     cfun = A.KEYED_SOLUTION_CB(trampoline) if cb else A.KEYED_SOLUTION_CB()
     res = A.Result()
     c = cfg.to_c()
-    _check(lib().cubics_solve_shard(model.handle, C.byref(c), shard_index, shard_count, cfun, None, C.byref(res)),
-           "solve_shard")
+    if queue is None:
+        rc = lib().cubics_solve_shard(model.handle, C.byref(c), shard_index, shard_count, cfun, None, C.byref(res))
+    else:
+        rc = lib().cubics_solve_shard_shared(model.handle, C.byref(c), shard_index, shard_count, queue.ptr, cfun,
+                                             None, C.byref(res))
+    _check(rc, "solve_shard")
     return SatisfyResult(_stats(res), bool(res.complete), res.engine, res.contexts, res.device_ms, res.total_ms,
                          res.h2d_bytes, res.d2h_bytes, res.kernel_launches)
 

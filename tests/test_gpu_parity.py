@@ -390,3 +390,89 @@ def test_grid_context_tables_and_corpus():
     m = S.parse_model(models.random_binary_csp(n, 10, 2 * n, t, 5))
     cfg = S.SearchConfig(max_solutions=1, node_limit=500, engine=A.ENGINE_GRID)
     assert S.solve_satisfy(m, cfg).stats.as_tuple() == O.solve_satisfy(m, cfg).stats.as_tuple()
+
+
+@pytest.mark.parametrize("key", ["nq8|--all", "nq10|--all", "nq12|--all", "magic3|--all", "nq8|--all --fc"])
+@pytest.mark.parametrize("world", [2, 8])
+def test_shared_queue_shards_sum_exactly(key, world):
+    # cubics_solve_shard_shared: every rank seeds all frontier subtrees and claims them through
+    # one counter; run one after another here, so the first rank claims everything and the rest
+    # only count (rank 0) or contribute nothing. Sums and key order are the reference's.
+    from paper_1909_09213_b200 import distributed as D
+
+    inst, flags = G.split_key(key)
+    m = S.parse_model(G.model_text(inst))
+    cfg = G.cfg_from_flags(flags)
+    q = S.TaskQueue.create(0)
+    try:
+        for _ in range(2):  # the queue is reusable after a reset
+            q.reset()
+            assert q.claims() == 0
+            tot = [0, 0, 0, 0]
+            streams = []
+            for r in range(world):
+                keyed = []
+                res = S.solve_shard(m, cfg, r, world, lambda k, v, keyed=keyed: keyed.append((tuple(k), v)) or True,
+                                    queue=q)
+                tot = [a + b for a, b in zip(tot, res.stats.as_tuple())]
+                streams.append(keyed)
+            assert tuple(tot) == G.expected_tuple(G.goldens()[key])
+            assert D.merge_keyed(streams) == [s.values for s in O.enumerate_solutions(m, cfg)]
+            assert q.claims() > 0
+    finally:
+        q.close()
+
+
+def _shared_queue_worker(rank, world, port, key, out):
+    import os
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    from paper_1909_09213_b200 import distributed as D
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        inst, flags = G.split_key(key)
+        m = S.parse_model(G.model_text(inst))
+        cfg = G.cfg_from_flags(flags)
+        q = D.shared_task_queue(rank, world, device=0)
+        res = []
+        for _ in range(2):
+            stats, merged, _ = D.solve_distributed(m, cfg, rank, world, queue=q)
+            res.append((stats, merged))
+        dist.barrier()  # the owner frees the counter only after every mapping is done with it
+        q.close()
+        dist.barrier()
+        out.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_shared_queue_across_processes_ipc():
+    # two processes map one claim counter through CUDA IPC (the NVLink peer-memory path on a
+    # multi-GPU box; here both sit on cuda:0 and never wait on each other's kernels)
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    key, world = "nq12|--all", 2
+    ctx = mp.get_context("spawn")
+    out = ctx.Queue()
+    procs = [ctx.Process(target=_shared_queue_worker, args=(r, world, port, key, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(out.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    inst, flags = G.split_key(key)
+    m = S.parse_model(G.model_text(inst))
+    want = [s.values for s in O.enumerate_solutions(m, G.cfg_from_flags(flags))]
+    for rank in range(world):
+        for stats, merged in got[rank]:
+            assert stats == G.expected_tuple(G.goldens()[key])
+            assert (merged == want) if rank == 0 else merged is None
