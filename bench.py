@@ -38,6 +38,17 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
+def ncu_traffic(instance):
+    """roofline.traffic: dram__bytes_read.sum + dram__bytes_write.sum of the search kernel from one
+    committed `ncu --set full` capture of this workload (scripts/ncu_traffic.py), per launch."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
+            rec = json.load(f)[instance]
+        return rec["dram_read_bytes"] + rec["dram_write_bytes"], rec["report"]
+    except Exception:  # noqa: BLE001
+        return None, None
+
+
 def algorithmic_bytes(model, stats):
     """A = rounds*(4*S + 8*V) + nodes*(4*V), W_v = ceil(width_v/32) u32 words."""
     wv = [(w + 31) // 32 for w in model.widths]
@@ -341,6 +352,7 @@ def impl_ours(args):
     A_bytes, S_, V = algorithmic_bytes(model, tot)
     peak, peak_kind = load_peaks()
     achieved = A_bytes / (mean_ms / 1e3) / 1e9
+    traffic, traffic_src = ncu_traffic(args.instance)
     # CPU baseline: the unmodified reference on this host, bounded sample
     cpu = None
     if os.path.exists(REF_DRIVER) and not args.no_cpu and world == 1:
@@ -367,7 +379,8 @@ def impl_ours(args):
                 "gpu_launches": e2e_launches},
         "gpu_launches": r.kernel_launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                     "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                     "peak_kind": peak_kind,
                      "algorithmic_bytes": A_bytes, "S_words": S_, "V_words": V,
                      "note": "latency/barrier-bound search; A from SURVEY 8(d)"},
         "cpu_baseline": cpu,

@@ -418,7 +418,8 @@ def test_shared_queue_shards_sum_exactly(key, world):
                 streams.append(keyed)
             assert tuple(tot) == G.expected_tuple(G.goldens()[key])
             assert D.merge_keyed(streams) == [s.values for s in O.enumerate_solutions(m, cfg)]
-            assert q.claims() > 0
+            if inst == "nq12":  # the smaller trees can close above the split depth (no subtrees)
+                assert q.claims() > 0
     finally:
         q.close()
 
