@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -1345,9 +1346,26 @@ int solve_shard_impl(const cubics_model* h, const cubics_search_config* cfg, int
                                                 keys.begin() + (size_t)y * KW, keys.begin() + (size_t)(y + 1) * KW);
         });
         std::vector<int32_t> mine;
-        if (claim)
+        uint64_t extra_d2h = 0;
+        if (claim) {
+            // shared queue: claim the (estimated) largest subtrees first, so the last claims are
+            // small and the GPUs finish together (list scheduling, largest first). Estimate =
+            // log2 of the product of the task's domain sizes; every rank computes the same order.
+            std::vector<uint32_t> tdom(nt * P.NWP);
+            if (nt)
+                CU(cudaMemcpy2D(tdom.data(), sizeof(uint32_t) * P.NWP, io.task_dev, sizeof(uint32_t) * OS,
+                                sizeof(uint32_t) * P.NWP, nt, cudaMemcpyDeviceToHost));
+            std::vector<double> est(nt, 0.0);
+            for (uint64_t t = 0; t < nt; ++t)
+                for (int v = 0; v < n; ++v) {
+                    int sz = 0;
+                    for (int w = 0; w < P.W; ++w) sz += __builtin_popcount(tdom[t * P.NWP + (size_t)v * P.W + w]);
+                    if (sz > 1) est[t] += std::log2((double)sz);
+                }
             mine = order;
-        else
+            std::stable_sort(mine.begin(), mine.end(), [&](int32_t x, int32_t y) { return est[x] > est[y]; });
+            extra_d2h = sizeof(uint32_t) * P.NWP * nt;
+        } else
             for (uint64_t r = shard_index; r < nt; r += shard_count) mine.push_back(order[r]);
         // 3. this shard's subtrees, seeded into the parallel engine
         RunOut run;
@@ -1367,7 +1385,7 @@ int solve_shard_impl(const cubics_model* h, const cubics_search_config* cfg, int
         }
         out->device_ms = run.device_ms + ex.device_ms;
         out->h2d_bytes += ex.h2d;
-        out->d2h_bytes += ex.d2h + sizeof(uint32_t) * KW * nt;
+        out->d2h_bytes += ex.d2h + sizeof(uint32_t) * KW * nt + extra_d2h;
         out->kernel_launches += ex.launches;
         out->complete = 1;
         out->has_solution = out->stats.solutions > 0;
