@@ -29,6 +29,13 @@ REF_DRIVER = os.path.join(ROOT, "oracle", "_ref", "fdref_driver")
 MODELS = os.path.join(ROOT, "tests", "golden", "models")
 
 
+def workload_name(instance):
+    """The config.workload string, identical on both arms (this one and --impl reference)."""
+    if instance == "nq14":
+        return "nq14 all solutions (N-Queens n=14, BASELINE configs[1])"
+    return f"{instance} all solutions"
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -153,7 +160,7 @@ def impl_reference(args):
         "metric": METRIC, "impl": "reference", "value": value, "unit": "nodes/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": limit / value * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
-        "data": "synthetic", "config": {"workload": f"{args.instance} all solutions", "sample": f"first {limit} DFS nodes"},
+        "data": "synthetic", "config": {"workload": workload_name(args.instance), "sample": f"first {limit} DFS nodes"},
         "cpu_baseline": {"value": value, "unit": "nodes/s", "cores": threads, "kind": "reference",
                          "sample": f"first {limit} nodes of the {args.instance} all-solutions DFS, threads={threads}",
                          "probe_nodes_per_s": probe},
@@ -365,7 +372,7 @@ def impl_ours(args):
         "metric": METRIC, "value": value, "unit": "nodes/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": mean_ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": {"workload": f"{args.instance} all solutions (N-Queens n=14, BASELINE configs[1])",
+        "config": {"workload": workload_name(args.instance),
                    "engine": "parallel", "contexts": r.contexts, "l2": "flushed (256 MiB write) before every timed step",
                    "balancing": ("in-GPU work-sharing ring" if world == 1 else
                                  "shared subtree queue (claim counter in rank 0 HBM, CUDA IPC over NVLink) + "
