@@ -7,9 +7,12 @@
 // CUBICS_E_CUDA with the CUDA error text in cubics_last_error().
 #include <cuda_runtime.h>
 #include <sys/mman.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <chrono>
+#include <condition_variable>
+#include <functional>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1134,6 +1137,73 @@ extern "C" int cubics_solve_satisfy(const cubics_model* h, const cubics_search_c
     });
 }
 
+// Host workers for the solution-array conversion, started once and kept: spawning 16 threads per
+// cubics_enumerate call cost a visible part of the ~1 ms conversion. run(n, f) calls f(0..n-1),
+// f(0) on the caller; calls are serialised (one job at a time).
+class HostPool {
+public:
+    static HostPool& get() {
+        // never destroyed: workers outlive static teardown. A forked child has none of the
+        // parent's workers, so it starts its own pool.
+        static std::mutex mu;
+        static HostPool* p = nullptr;
+        std::lock_guard<std::mutex> lk(mu);
+        if (!p || p->pid_ != getpid()) p = new HostPool();
+        return *p;
+    }
+    unsigned size() const { return (unsigned)threads_.size() + 1; }
+    void run(unsigned n, const std::function<void(unsigned)>& f) {
+        n = std::min(n, size());
+        if (n <= 1) {
+            if (n) f(0);
+            return;
+        }
+        std::lock_guard<std::mutex> job(job_mu_);
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            fn_ = &f;
+            parts_ = n;
+            pending_ = n - 1;
+            ++gen_;
+        }
+        cv_.notify_all();
+        f(0);
+        std::unique_lock<std::mutex> lk(mu_);
+        done_.wait(lk, [&] { return pending_ == 0; });
+        fn_ = nullptr;
+    }
+
+private:
+    HostPool() {
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        for (unsigned i = 1; i < std::min(16u, hw); ++i) threads_.emplace_back([this, i] { loop(i); });
+        for (auto& t : threads_) t.detach();
+    }
+    void loop(unsigned id) {
+        unsigned long long seen = 0;
+        for (;;) {
+            const std::function<void(unsigned)>* f;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return gen_ != seen; });
+                seen = gen_;
+                if (id >= parts_) continue;
+                f = fn_;
+            }
+            (*f)(id);
+            std::lock_guard<std::mutex> lk(mu_);
+            if (--pending_ == 0) done_.notify_one();
+        }
+    }
+    pid_t pid_ = getpid();
+    std::vector<std::thread> threads_;
+    std::mutex mu_, job_mu_;
+    std::condition_variable cv_, done_;
+    const std::function<void(unsigned)>* fn_ = nullptr;
+    unsigned parts_ = 0, pending_ = 0;
+    unsigned long long gen_ = 0;
+};
+
 // Solution arrays: 2 MiB-aligned and advised as huge pages when large, so filling a 40 MB result
 // costs tens of page faults instead of ten thousand. Freed with free() (cubics_solutions_free).
 int64_t* alloc_values(uint64_t count) {
@@ -1167,19 +1237,16 @@ extern "C" int cubics_enumerate(const cubics_model* h, const cubics_search_confi
         const uint64_t total = r.rec.count * (uint64_t)n;
         S->values = alloc_values(std::max<uint64_t>(total, 1));
         // offset conversion straight into the returned buffer, split over host threads
-        const unsigned nt = total > (1u << 20) ? std::max(1u, std::min(16u, std::thread::hardware_concurrency())) : 1u;
-        auto conv = [&](uint64_t lo, uint64_t hi) {
-            for (uint64_t i = lo; i < hi; ++i) {
-                const uint16_t* row = r.rec.rows() + i * n;
+        const unsigned nt = total > (1u << 20) ? HostPool::get().size() : 1u;
+        const uint64_t count = r.rec.count;
+        const uint16_t* rows = r.rec.rows();
+        HostPool::get().run(nt, [&](unsigned t) {
+            for (uint64_t i = count * t / nt; i < count * (t + 1) / nt; ++i) {
+                const uint16_t* row = rows + i * n;
                 int64_t* dst = S->values + i * n;
                 for (int v = 0; v < n; ++v) dst[v] = m.offset[v] + row[v];
             }
-        };
-        std::vector<std::thread> pool;
-        for (unsigned t = 1; t < nt; ++t)
-            pool.emplace_back(conv, r.rec.count * t / nt, r.rec.count * (t + 1) / nt);
-        conv(0, r.rec.count / nt);
-        for (auto& th : pool) th.join();
+        });
         *sols = S;
         out->total_ms = now_ms() - t0;
         if (std::getenv("CUBICS_DEBUG"))
