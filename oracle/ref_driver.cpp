@@ -7,7 +7,9 @@
 // --impl reference legs and golden-fixture generation run it.
 //
 //   fdref_driver solve <model.fd> [--max N|--all] [--input] [--fc] [--node-limit N]
-//                [--threads T] [--solutions] [--repeat R]
+//                [--threads T] [--solutions] [--repeat R] [--solutions-bin PATH]
+//     --solutions-bin: every solution's values, in callback (DFS) order, as little-endian int64
+//     rows into PATH (the golden sha256 of the full solution stream is taken over this file)
 //   fdref_driver fixpoint <model.fd> [--fc]
 //   fdref_driver gen-nqueens N
 //   fdref_driver gen-random VARS WIDTH CONS SEED
@@ -61,6 +63,7 @@ int cmd_solve(int argc, char** argv) {
     fd::SearchConfig cfg;
     bool print_all = false;
     int repeat = 1;
+    const char* bin_path = nullptr;
     for (int i = 3; i < argc; ++i) {
         std::string a = argv[i];
         if (a == "--max") cfg.max_solutions = std::stoull(argv[++i]);
@@ -71,6 +74,7 @@ int cmd_solve(int argc, char** argv) {
         else if (a == "--threads") cfg.thread_count = std::stoi(argv[++i]);
         else if (a == "--solutions") print_all = true;
         else if (a == "--repeat") repeat = std::stoi(argv[++i]);
+        else if (a == "--solutions-bin") bin_path = argv[++i];
         else { std::fprintf(stderr, "unknown flag %s\n", a.c_str()); return 2; }
     }
     bool optimizing = !std::holds_alternative<fd::Satisfy>(m.goal);
@@ -97,12 +101,16 @@ int cmd_solve(int argc, char** argv) {
                 std::vector<std::vector<std::int64_t>> sols;
                 std::uint64_t count = 0;
                 std::vector<std::int64_t> first;
+                std::FILE* bin = bin_path ? std::fopen(bin_path, "wb") : nullptr;
+                if (bin_path && !bin) { std::fprintf(stderr, "cannot write %s\n", bin_path); std::exit(2); }
                 fd::SatisfyResult res = fd::solve_satisfy(m, cfg, [&](const fd::Solution& s) {
                     if (count == 0) first = s.values;
                     ++count;
                     if (print_all) sols.push_back(s.values);
+                    if (bin) std::fwrite(s.values.data(), sizeof(std::int64_t), s.values.size(), bin);
                     return true;
                 });
+                if (bin) std::fclose(bin);
                 auto t1 = std::chrono::steady_clock::now();
                 best_ms = std::min(best_ms, std::chrono::duration<double, std::milli>(t1 - t0).count());
                 os << "{\"status\":\"" << (count ? "SAT" : (res.complete ? "UNSAT" : "UNKNOWN"))

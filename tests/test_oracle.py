@@ -72,3 +72,36 @@ def test_oracle_random_instances():
         sols = O.enumerate_solutions(m, S.SearchConfig(), st)
         assert [s.values for s in sols] == c[str(seed)]["all"], seed
         assert st.as_tuple() == G.expected_tuple(c[str(seed)]), seed
+
+
+@pytest.mark.parametrize("key", ["nq8|--all", "nq10|--all", "magic3|--all"])
+def test_oracle_solution_stream_hash_matches_reference(key):
+    """The oracle's full callback stream hashes to the reference's (tests/golden/stream_hashes.json,
+    made by make_stream_hashes.py from oracle/_ref/fdref_driver --solutions-bin)."""
+    import hashlib
+    import json
+    import os
+    import struct
+
+    with open(os.path.join(G.GOLDEN, "stream_hashes.json")) as f:
+        h = json.load(f)[key]
+    inst, flags = G.split_key(key)
+    m = S.parse_model(G.model_text(inst))
+    sols = O.enumerate_solutions(m, G.cfg_from_flags(flags))
+    blob = b"".join(struct.pack("<%dq" % len(s.values), *s.values) for s in sols)
+    assert len(sols) == h["rows"]
+    assert hashlib.sha256(blob).hexdigest() == h["sha256"]
+
+
+def test_stream_hash_fixture_consistent_with_goldens():
+    import json
+    import os
+
+    with open(os.path.join(G.GOLDEN, "stream_hashes.json")) as f:
+        hs = json.load(f)
+    gold = G.goldens()
+    assert "nq14|--all" in hs, "regenerate with make_stream_hashes.py --long"
+    for key, h in hs.items():
+        assert tuple(h["stats"]) == G.expected_tuple(gold[key]), key
+        assert h["first"] == gold[key]["first"], key
+        assert h["bytes"] == 8 * h["rows"] * h["n_vars"], key
