@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libcubics.so")
+# CUBICS_LIB: an alternative in-tree build of the engine (A/B probes only)
+LIB_PATH = os.environ.get("CUBICS_LIB") or os.path.join(HERE, "lib", "libcubics.so")
 
 # status codes (enum cubics_status)
 OK, E_INVALID, E_PARSE, E_OVERFLOW, E_NO_OBJECTIVE, E_CUDA, E_CAPACITY, E_UNSUPPORTED = range(8)

@@ -39,6 +39,8 @@ struct DevModel {
     int32_t nr_gen;              // records [0, nr_gen) are not var-form !=
     const int32_t* ne_start;     // [n+1] var-form != incidence: when v becomes a singleton at bit b,
     const int2* ne_edge;         //   each edge (p, s) removes bit b + s from var p
+    const unsigned long long* neq; // [n*n] warp kernel (n <= 32, W = 1): the != edges u -> p folded
+                                 //   into one mask, bit s + 32 per shift s in [-31, 31]; else null
     int32_t nl;
     const int32_t* lin_start; // [nl+1]
     const int32_t* lin_op;    // [nl]
@@ -182,6 +184,7 @@ struct SearchParams {
     uint32_t* seg_key;     // [seg_cap][KW]
     uint64_t* seg_stats;   // [seg_cap][3]
     int32_t* sol_seg;      // [sol_cap]
+    int32_t frames_in_smem; // warp contexts: decision stack in the context's shared memory
 };
 
 struct PropParams {

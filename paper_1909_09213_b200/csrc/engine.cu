@@ -118,6 +118,8 @@ struct Prepared {
     uint64_t depth_bound = 0; // sum(|D| - 1): max binary-tree depth
     Blob blob;
     size_t o_vw = 0;
+    size_t o_neq = 0;
+    bool warp_ok = false;     // search_kernel_warp eligible: n <= 32, W = 1, small alldifferents, no tables
     bool mixed_width = false; // some variable needs <= W/4 words: per-variable word counts pay
     size_t o_off, o_dom, o_rb, o_ls, o_lo, o_lb, o_lv, o_lc, o_as, o_av, o_ash, o_nes, o_nee, o_auw;
     size_t o_tbxy, o_tboff, o_tbsup, o_tns, o_tnv, o_tnn, o_tno, o_tnd;
@@ -140,6 +142,7 @@ struct Prepared {
         M.nr_gen = nr_gen;
         M.ne_start = reinterpret_cast<const int32_t*>(base + o_nes);
         M.ne_edge = reinterpret_cast<const int2*>(base + o_nee);
+        M.neq = warp_ok && nr_gen < nr ? reinterpret_cast<const unsigned long long*>(base + o_neq) : nullptr;
         M.nl = nl;
         M.lin_start = reinterpret_cast<const int32_t*>(base + o_ls);
         M.lin_op = reinterpret_cast<const int32_t*>(base + o_lo);
@@ -400,6 +403,20 @@ void prepare(const HostModel& m, const uint64_t* words, Prepared& P) {
     P.o_tnd = P.blob.add(tn_data.data(), tn_data.size());
     P.o_nes = P.blob.add(nes.data(), nes.size());
     P.o_nee = P.blob.add(nee.data(), nee.size());
+    // warp contexts (warp_ctx.cuh): one lane per variable, one-word domains and alldifferent
+    // universes, <= 32 members per alldifferent, no tables or generic-path alldifferents
+    int max_members = 0;
+    for (int a = 0; a < P.na; ++a) max_members = std::max(max_members, as[a + 1] - as[a]);
+    P.warp_ok = n >= 1 && n <= 32 && W == 1 && P.ntb + P.ntn == 0 && P.big_words == 0 && max_members <= 32;
+    if (P.warp_ok && P.nr_gen < P.nr) {
+        // the != edges u -> p with shift s in [-31, 31] as bit s + 32 of neq[u*n + p] (other shifts
+        // can never hit a one-word domain)
+        std::vector<unsigned long long> neq((size_t)n * n, 0);
+        for (int u = 0; u < n; ++u)
+            for (int e = nes[u]; e < nes[u + 1]; ++e)
+                if (nee[e].y >= -31 && nee[e].y <= 31) neq[(size_t)u * n + nee[e].x] |= 1ull << (nee[e].y + 32);
+        P.o_neq = P.blob.add(neq.data(), neq.size());
+    }
 }
 
 // per-device state created once: capability check, one non-blocking stream, timing events
@@ -616,7 +633,12 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
     if (parallel && KW > 4096) throw StatusError{CUBICS_E_UNSUPPORTED, "search tree too deep for ordered parallel keys"};
     out.KW = KW;
     // launch geometry
+    // small models run warp contexts (warp_ctx.cuh): K contexts per block of 32K threads
+    const bool use_warp = P.warp_ok && !grid && !batch && cfg.block_threads <= 0 &&
+                          (parallel || engine == CUBICS_ENGINE_PARITY) && !std::getenv("CUBICS_NO_WARP");
+    const int warp_k = use_warp && parallel ? std::max(1, std::min(2, std::getenv("CUBICS_WARP_K") ? std::atoi(std::getenv("CUBICS_WARP_K")) : 1)) : 1;
     int block = cfg.block_threads > 0 ? ((cfg.block_threads + 31) / 32) * 32 : 0;
+    if (use_warp) block = 32 * warp_k;
     if (!block && grid) block = 512;
     if (!block) // parallel: one warp per context maximises resident contexts (32 per SM) for small models
         block = parallel ? (P.nr + P.nl + P.ntb + P.ntn > 1024 || P.n > 1024
@@ -624,9 +646,19 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
                                 : (P.W >= 8 || P.nr + P.nl + P.ntb + P.ntn > 256 ? 64 : 32))
                          : parity_block(P);
     block = std::min(std::max(block, 32), batch ? 512 : 1024);
-    const int nw = block / 32;
+    const int nw = use_warp ? 1 : block / 32;
     bool in_smem = !grid; // the grid context keeps its domains in L2/HBM
-    dev::SmemLayout L = dev::smem_layout(P.W, n, P.total_members, nw, KW, in_smem, P.na);
+    int frame_cap = n + 1;
+    if (cfg.node_limit && cfg.node_limit + 1 < (uint64_t)frame_cap) frame_cap = static_cast<int>(cfg.node_limit + 1);
+    frame_cap = std::max(frame_cap, 1);
+    // warp contexts keep their decision stack in shared memory when it is small (n <= 32: at
+    // most 33 frames of 32 words)
+    const bool frames_in_smem = use_warp && !std::getenv("CUBICS_WARP_GFRAMES") &&
+                                (size_t)frame_cap * (P.NWP * 4 + 16) <= 4096;
+    dev::SmemLayout L = dev::smem_layout(P.W, n, P.total_members, nw, KW, in_smem, P.na, frames_in_smem ? frame_cap : 0);
+    // bytes of dynamic shared memory per block (warp contexts: one 16-byte aligned slice each)
+    const size_t smem_block = use_warp ? (size_t)warp_k * ((L.total + 15) & ~size_t(15)) : L.total;
+    if (use_warp && smem_block > kSmemBudget) throw StatusError{CUBICS_E_UNSUPPORTED, "warp context does not fit in shared memory"};
     if (L.total > kSmemBudget) {
         in_smem = false;
         L = dev::smem_layout(P.W, n, P.total_members, nw, KW, false, P.na);
@@ -634,17 +666,23 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
     }
     // propagator features the model needs: the lean kernel instantiations skip the rest
     const int feat = (P.nl ? 1 : 0) | (P.ntb + P.ntn ? 2 : 0) | (P.big_words ? 4 : 0) | (first_mode ? 8 : 0) |
-                     (P.lin_g > 1 ? dev::F_LONG : 0);
+                     (P.lin_g > 1 ? dev::F_LONG : 0) |
+                     (hm.goal == CUBICS_SATISFY && !shard ? dev::F_NOOPT | dev::F_NOSPLIT : 0);
     int n_ctx = batch ? batch->count : 1;
     if (parallel) {
         int per_sm = 0;
+        if (use_warp) {
+            CU(occupancy_search_warp(feat, false, block, smem_block, &per_sm));
+        } else {
 #define OCC(w) occupancy_search<w>(feat, block, L.total, &per_sm)
-        CUBICS_DISPATCH_W(P.W, OCC)
+            CUBICS_DISPATCH_W(P.W, OCC)
 #undef OCC
+        }
         int sms = 0;
         CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        const int cap = std::max(1, per_sm) * sms;
+        const int cap = std::max(1, per_sm) * sms * warp_k;
         n_ctx = cfg.contexts > 0 ? std::min(cfg.contexts, cap) : cap;
+        n_ctx = std::max(warp_k, n_ctx / warp_k * warp_k); // whole blocks of warp contexts
     }
     int grid_blocks = 0;
     if (grid) { // co-resident blocks for the cooperative launch
@@ -659,9 +697,6 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
     }
     out.contexts = n_ctx;
     out.engine = engine;
-    int frame_cap = n + 1;
-    if (cfg.node_limit && cfg.node_limit + 1 < (uint64_t)frame_cap) frame_cap = static_cast<int>(cfg.node_limit + 1);
-    frame_cap = std::max(frame_cap, 1);
     const size_t NWP = P.NWP;
     const size_t OS = NWP + dev::round4((size_t)KW + 2);
     if (!record) sol_cap = 0;
@@ -685,8 +720,8 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
     const size_t a_gctl = take(grid ? 256 : 0);
     const size_t a_gslots = take(grid ? 6 * sizeof(unsigned) : 0);
     const size_t a_gchg = take(grid ? sizeof(uint32_t) * 2 * (((size_t)n + 31) / 32) : 0);
-    const size_t a_frames = take(sizeof(uint32_t) * NWP * frame_cap * n_ctx);
-    const size_t a_meta = take(sizeof(int32_t) * 4 * frame_cap * n_ctx);
+    const size_t a_frames = take(frames_in_smem ? 0 : sizeof(uint32_t) * NWP * frame_cap * n_ctx);
+    const size_t a_meta = take(frames_in_smem ? 0 : sizeof(int32_t) * 4 * frame_cap * n_ctx);
     const size_t a_gdom = take(in_smem ? 0 : sizeof(uint32_t) * 2 * NWP * n_ctx);
     const size_t a_outbox = take(parallel ? sizeof(uint32_t) * OS * (n_ctx + n_seed) : 0);
     const size_t a_seedidx = take(sizeof(int32_t) * n_seed);
@@ -772,6 +807,7 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
         S.KW = KW;
         S.record = record ? 1 : 0;
         S.dom_in_smem = in_smem ? 1 : 0;
+        S.frames_in_smem = frames_in_smem ? 1 : 0;
         S.big_scratch = P.big_words ? reinterpret_cast<uint32_t*>(base + a_big) : nullptr;
         if (grid) {
             const unsigned init[6] = {0, 0, 0, 0xffffffffu, 0xffffffffu, 0xffffffffu};
@@ -823,6 +859,8 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
 #define LG(w) launch_search_grid<w>(S, grid_blocks, block, L.total, st)
             CUBICS_DISPATCH_W(P.W, LG)
 #undef LG
+        } else if (use_warp) {
+            CU(launch_search_warp(S, feat, n_ctx / warp_k, block, smem_block, st));
         } else {
 #define LS(w) launch_search<w>(S, feat, n_ctx, block, L.total, st)
             CUBICS_DISPATCH_W(P.W, LS)
@@ -959,9 +997,9 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
         const WorkState& w = out.ws;
         const double tot = (double)w.busy_cycles + (double)w.idle_cycles;
         std::fprintf(stderr,
-                     "[cubics] engine=%s ctx=%d block=%d W=%d smem=%zu KW=%d ms=%.3f nodes=%llu donations=%llu "
+                     "[cubics] engine=%s%s ctx=%d block=%d W=%d smem=%zu KW=%d ms=%.3f nodes=%llu donations=%llu "
                      "steals=%llu busy=%.3f\n",
-                     parallel ? "parallel" : "parity", n_ctx, block, P.W, L.total, KW, out.device_ms,
+                     parallel ? "parallel" : "parity", use_warp ? "(warp)" : "", n_ctx, block, P.W, smem_block, KW, out.device_ms,
                      (unsigned long long)w.stats[0], (unsigned long long)w.donations, (unsigned long long)w.steals,
                      tot > 0 ? w.busy_cycles / tot : 0.0);
     }

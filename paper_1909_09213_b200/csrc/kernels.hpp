@@ -13,6 +13,9 @@ template <int W>
 cudaError_t launch_search(const SearchParams& P, int feat, int grid, int block, size_t smem, cudaStream_t st);
 template <int W>
 cudaError_t occupancy_search(int feat, int block, size_t smem, int* blocks_per_sm);
+// warp contexts for small models (n <= 32, W = 1): blockDim.x / 32 contexts per block
+cudaError_t launch_search_warp(const SearchParams& P, int feat, int grid, int block, size_t smem, cudaStream_t st);
+cudaError_t occupancy_search_warp(int feat, bool parity, int block, size_t smem, int* blocks_per_sm);
 template <int W>
 cudaError_t launch_search_parity(const SearchParams& P, int grid, int block, size_t smem, cudaStream_t st);
 template <int W>

@@ -21,8 +21,11 @@ namespace dev {
 // F_REGS marks the 128-register parity kernel: register-hungry fast paths are compiled in only
 // there (in the 64-register kernels they cost more in spills than they save).
 // F_LONG: linear sums of more than 4 terms (lane-group form); lean kernels compile it out.
+// F_NOOPT / F_NOSPLIT (lean warp kernels): branch-and-bound, and the frontier expansion and
+// shared-queue claims of sharded runs, are compiled out.
 enum Feature : int {
-    F_LINEAR = 1, F_TABLE = 2, F_BIGAD = 4, F_FIRST = 8, F_LONG = 64, F_ALL = 15 | 64, F_PARITY = 16, F_REGS = 32
+    F_LINEAR = 1, F_TABLE = 2, F_BIGAD = 4, F_FIRST = 8, F_LONG = 64, F_ALL = 15 | 64, F_PARITY = 16, F_REGS = 32,
+    F_NOOPT = 128, F_NOSPLIT = 256
 };
 
 
@@ -39,7 +42,7 @@ CUBICS_HD inline size_t big_scratch_words(int n, int uw) {
 }
 
 struct SmemLayout {
-    size_t dom, rm, mates, scratch, path, bestkey, post, post_ok, chg, total;
+    size_t dom, rm, mates, scratch, path, bestkey, post, post_ok, chg, frames, meta, total;
     int stride;
     bool has_post, has_chg;
 };
@@ -49,8 +52,10 @@ constexpr size_t kPostBudget = 16384;
 // changed-variable trigger bitmaps (two buffers of n bits) are kept up to this size
 constexpr size_t kChgBudget = 65536;
 
+// frame_cap > 0: the decision stack (frame_cap frames of NWP words + 4 meta words each) lives in
+// shared memory too (warp contexts of small models)
 CUBICS_HD inline SmemLayout smem_layout(int W, int n, int total_members, int nw, int KW, bool dom_in_smem,
-                                        int na = 0) {
+                                        int na = 0, int frame_cap = 0) {
     SmemLayout L{};
     const size_t NWP = round4((size_t)n * W);
     size_t p = 0;
@@ -69,13 +74,17 @@ CUBICS_HD inline SmemLayout smem_layout(int W, int n, int total_members, int nw,
     const size_t post_bytes = (size_t)total_members * W * 4;
     L.has_post = na > 0 && post_bytes <= kPostBudget;
     L.post = p;
-    p += L.has_post ? post_bytes : 0;
+    p += L.has_post ? ((post_bytes + 15) & ~size_t(15)) : 0;
     L.post_ok = p;
     p += L.has_post ? (((size_t)na + 15) & ~size_t(15)) : 0;
     const size_t chg_bytes = (((size_t)n + 31) / 32) * 4;
     L.has_chg = 2 * chg_bytes <= kChgBudget;
     L.chg = p;
     p += L.has_chg ? ((2 * chg_bytes + 15) & ~size_t(15)) : 0;
+    L.frames = p;
+    p += (size_t)frame_cap * NWP * 4;
+    L.meta = p;
+    p += (size_t)frame_cap * 16;
     L.total = p;
     return L;
 }

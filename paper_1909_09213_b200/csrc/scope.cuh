@@ -19,6 +19,7 @@ namespace dev {
 
 // control scalars broadcast from thread 0 (shared memory for a block, global for the grid)
 struct Ctl {
+    uint4 hot; // warp contexts: the prefetched HotState (cp.async target)
     int err, min, flag, src;
     long long ll;
     unsigned red[32];
@@ -26,6 +27,7 @@ struct Ctl {
 
 struct BlockScope {
     static constexpr bool kGrid = false;
+    static constexpr bool kWarp = false;
     __device__ __forceinline__ int tid() const { return threadIdx.x; }
     __device__ __forceinline__ int nthreads() const { return blockDim.x; }
     __device__ __forceinline__ int warp() const { return threadIdx.x >> 5; }
@@ -46,8 +48,24 @@ struct BlockScope {
     }
 };
 
+// WarpScope: the context is one warp of a block that may hold several (search_kernel_warp, small
+// models: n <= 32 variables of <= 32 values). Barriers are __syncwarp, votes are warp votes, and
+// the fixpoint keeps each variable's domain in its lane's register (warp_ctx.cuh).
+struct WarpScope {
+    static constexpr bool kGrid = false;
+    static constexpr bool kWarp = true;
+    __device__ __forceinline__ int tid() const { return threadIdx.x & 31; }
+    __device__ __forceinline__ int nthreads() const { return 32; }
+    __device__ __forceinline__ int warp() const { return 0; }
+    __device__ __forceinline__ int nwarps() const { return 1; }
+    __device__ __forceinline__ void sync() { __syncwarp(); }
+    __device__ __forceinline__ int sync_or(int x) { return __any_sync(0xffffffffu, x); }
+    __device__ __forceinline__ unsigned min_u32(unsigned v, unsigned*) { return __reduce_min_sync(0xffffffffu, v); }
+};
+
 struct GridScope {
     static constexpr bool kGrid = true;
+    static constexpr bool kWarp = false;
     unsigned* or_slots;  // [3] rotating vote slots (zero-initialised)
     unsigned* min_slots; // [3] rotating min slots (0xffffffff-initialised)
     unsigned or_seq = 0, min_seq = 0;

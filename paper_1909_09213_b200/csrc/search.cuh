@@ -18,6 +18,7 @@
 #include "layout.hpp"
 #include "propagators.cuh"
 #include "scope.cuh"
+#include "warp_ctx.cuh"
 
 namespace cubics {
 namespace dev {
@@ -112,6 +113,7 @@ __device__ __forceinline__ int select_var(const DevModel& M, const uint32_t* dom
 
 template <int W, int F, class SC>
 __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& C, unsigned* red, uint8_t* smem) {
+    static_assert(!SC::kWarp || W == 1, "warp contexts hold one-word domains");
     int& s_err = C.err;
     int& s_min = C.min;
     int& s_flag = C.flag;
@@ -119,13 +121,19 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
     long long& s_ll = C.ll;
 
     const DevModel& M = P.M;
-    const int ctx = SC::kGrid ? 0 : (int)blockIdx.x, tid = sc.tid(), T = sc.nthreads(), nw = sc.nwarps();
+    // a warp context is warp (threadIdx.x >> 5) of its block; bt/bT index its private shared memory
+    const int ctx = SC::kGrid ? 0
+                    : (SC::kWarp ? (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) : (int)blockIdx.x);
+    const int tid = sc.tid(), T = sc.nthreads(), nw = sc.nwarps();
+    const int bt = SC::kWarp ? (int)(threadIdx.x & 31) : (int)threadIdx.x, bT = SC::kWarp ? 32 : (int)blockDim.x;
     const bool parallel = (F & F_PARITY) == 0 && P.mode == MODE_PARALLEL;
     const int n = M.n;
     const size_t NW = (size_t)n * W, NWP = round4(NW);
     const int KW = P.KW;
     // shared memory is per block: its layout follows the block's warps, not the scope's
-    const SmemLayout L = smem_layout(W, n, M.total_members, (int)(blockDim.x >> 5), KW, P.dom_in_smem, M.na);
+    const SmemLayout L = smem_layout(W, n, M.total_members, SC::kWarp ? 1 : (int)(blockDim.x >> 5), KW, P.dom_in_smem, M.na,
+                                     P.frames_in_smem ? P.frame_cap : 0);
+    if (SC::kWarp) smem += (size_t)(threadIdx.x >> 5) * ((L.total + 15) & ~size_t(15));
     uint32_t* dom = P.dom_in_smem ? reinterpret_cast<uint32_t*>(smem + L.dom) : P.gdom + (size_t)ctx * 2 * NWP;
     uint32_t* rm = P.dom_in_smem ? reinterpret_cast<uint32_t*>(smem + L.rm) : dom + NWP;
     int16_t* mates = reinterpret_cast<int16_t*>(smem + L.mates);
@@ -144,17 +152,17 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
     bool first_all = true; // the root's first round evaluates every propagator
     bool skip_node = false; // first mode: the task just taken lies right of the best solution
     int trig_var = -1;     // var changed by the branch that created the current node
-    uint32_t* frames = P.frames + (size_t)ctx * P.frame_cap * NWP;
-    int32_t* meta = P.frame_meta + (size_t)ctx * P.frame_cap * 4;
+    uint32_t* frames = P.frames_in_smem ? reinterpret_cast<uint32_t*>(smem + L.frames) : P.frames + (size_t)ctx * P.frame_cap * NWP;
+    int32_t* meta = P.frames_in_smem ? reinterpret_cast<int32_t*>(smem + L.meta) : P.frame_meta + (size_t)ctx * P.frame_cap * 4;
     WorkState* ws = P.ws;
     const size_t OS = NWP + round4((size_t)KW + 2); // outbox: domains | path key | depth | branch var
 
     for (size_t i = tid; i < NWP; i += T) rm[i] = 0;
     // block-private shared memory is initialised with block-local indices
-    for (int i = threadIdx.x; i < M.total_members; i += blockDim.x) mates[i] = -1;
+    for (int i = bt; i < M.total_members; i += bT) mates[i] = -1;
     if (L.has_post)
-        for (int i = threadIdx.x; i < M.na; i += blockDim.x) post_ok[i] = 0;
-    for (int i = threadIdx.x; i < KW; i += blockDim.x) {
+        for (int i = bt; i < M.na; i += bT) post_ok[i] = 0;
+    for (int i = bt; i < KW; i += bT) {
         path[i] = 0;
         bestkey[i] = 0xffffffffu;
     }
@@ -163,14 +171,20 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
 
     unsigned long long nodes = 0, failures = 0, rounds = 0, sols = 0;
     int sp = 0, base = 0, depth = 0;
-    const bool batch = (F & F_PARITY) != 0 && P.batch != 0; // parity kernels only
+    const bool batch = (F & F_PARITY) != 0 && !SC::kWarp && P.batch != 0; // parity block kernels only
+    // lean warp kernels compile out branch-and-bound and the frontier expansion / shared claims
+    constexpr bool kOpt = (F & F_NOOPT) == 0, kSplit = (F & F_NOSPLIT) == 0;
     bool has_bound = batch ? P.batch_has_bound[ctx] != 0 : P.has_init_bound != 0;
     long long bound = batch ? P.batch_bound[ctx] : P.init_bound;
     bool has_first = false;
-    const bool optimizing = M.goal != 0, minimizing = M.goal == 1;
+    const bool optimizing = kOpt && M.goal != 0, minimizing = M.goal == 1;
     const int obj = M.goal_var;
     // thread 0's view of the shared coordination state (parallel engine)
-    uint4 hot = make_uint4(0, 0, 0, 0);
+    // warp contexts prefetch it with cp.async into shared memory (no registers held across the
+    // fixpoint); block contexts into registers
+    uint4 hot_reg = make_uint4(0, 0, 0, 0);
+    uint4& hot = SC::kWarp ? C.hot : hot_reg;
+    if (SC::kWarp && tid == 0) hot = hot_reg;
     long long g_bound = P.init_bound;
     int g_has_bound = P.has_init_bound;
     int my_busy = 0;
@@ -218,7 +232,7 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
 
     // Idle: take a ticket and wait for the task published under it (lock-free ticket queue:
     // each waiter spins on its own ring slot, so there is no shared hot spot to contend on).
-    bool claim_open = P.task_claim != nullptr; // thread 0: shared queue not yet drained
+    bool claim_open = kSplit && P.task_claim != nullptr; // thread 0: shared queue not yet drained
     auto get_work = [&]() -> bool {
         if (tid == 0) {
             const long long t0 = clock64();
@@ -302,7 +316,7 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
         if (skip_node) {
             skip_node = false;
             backtrack = true;
-        } else if (P.split_depth >= 0 && depth >= P.split_depth) {
+        } else if (kSplit && P.split_depth >= 0 && depth >= P.split_depth) {
             // ============ frontier expansion: this open node becomes a task (counted by its shard)
             if (tid == 0) s_ll = (long long)atomicAdd((unsigned long long*)&ws->n_tasks, 1ull);
             sc.sync();
@@ -332,7 +346,12 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
             break;
         }
         if (parallel && tid == 0) { // prefetch; consumed after the fixpoint
-            hot = ld_volatile_v4(reinterpret_cast<const uint4*>(&ws->hot));
+            if constexpr (SC::kWarp)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(&C.hot)),
+                             "l"(&ws->hot)
+                             : "memory");
+            else
+                hot = ld_volatile_v4(reinterpret_cast<const uint4*>(&ws->hot));
             if (optimizing) g_bound = ld_volatile_s64(&ws->bound);
             my_busy = ld_volatile(&P.outbox_busy[ctx]);
         }
@@ -368,7 +387,11 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
         }
         if (!backtrack) {
             int r = 0;
-            const int st = block_fixpoint<W, F>(M, R, &s_err, &s_min, 0, &r, nullptr, first_all, sc);
+            int st;
+            if constexpr (SC::kWarp && W == 1)
+                st = warp_fixpoint<F>(M, R, &r, first_all, chg0 ? chg0[0] : 0u, tid);
+            else
+                st = block_fixpoint<W, F>(M, R, &s_err, &s_min, 0, &r, nullptr, first_all, sc);
             first_all = false;
             rounds += (unsigned long long)r;
             if (st == R_ERROR) {
@@ -383,6 +406,8 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
                 backtrack = true;
             }
         }
+        if constexpr (SC::kWarp)
+            if (parallel && tid == 0) asm volatile("cp.async.wait_all;" ::: "memory");
         if (parallel && tid == 0) g_has_bound = (int)hot.w; // the prefetched bound pairs with this flag
         if (!backtrack) {
             const int sel = select_var<W>(M, dom, P.var_heuristic, red, sc);
@@ -495,7 +520,10 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
                     break;
                 }
                 const int bit = dom_first<W>(dom + (size_t)sel * W);
-                copy4(frames + (size_t)sp * NWP, dom, NWP, tid, T);
+                if (SC::kWarp && P.frames_in_smem)
+                    copy4_shared(frames + (size_t)sp * NWP, dom, NWP, tid);
+                else
+                    copy4(frames + (size_t)sp * NWP, dom, NWP, tid, T);
                 if (chg0)
                     for (int i = tid; i < 2 * nbw; i += T) chg0[i] = 0;
                 if (tid == 0) {
@@ -564,7 +592,10 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
             continue;
         }
         --sp;
-        copy4(dom, frames + (size_t)sp * NWP, NWP, tid, T);
+        if (SC::kWarp && P.frames_in_smem)
+            copy4_shared(dom, frames + (size_t)sp * NWP, NWP, tid);
+        else
+            copy4(dom, frames + (size_t)sp * NWP, NWP, tid, T);
         if (chg0)
             for (int i = tid; i < 2 * nbw; i += T) chg0[i] = 0;
         const int var = meta[sp * 4 + 0], bit = meta[sp * 4 + 1], d = meta[sp * 4 + 2];
@@ -618,6 +649,19 @@ __global__ void __launch_bounds__(1024) search_kernel(const SearchParams P) {
     __shared__ unsigned red[32];
     BlockScope sc;
     search_body<W, F>(P, sc, C, red, smem);
+}
+
+// small models (n <= 32, W = 1; warp_ctx.cuh): one search context per warp, blockDim.x / 32
+// contexts per block, each with its own slice of the dynamic shared memory
+#ifndef CUBICS_WARP_MINB
+#define CUBICS_WARP_MINB 16 // 16 x 64 threads per SM: 64 registers
+#endif
+template <int F>
+__global__ void __launch_bounds__(64, CUBICS_WARP_MINB) search_kernel_warp(const SearchParams P) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ Ctl C[2];
+    WarpScope sc;
+    search_body<1, F>(P, sc, C[threadIdx.x >> 5], nullptr, smem);
 }
 
 // one search context spanning the GPU (cooperative launch); see scope.cuh
