@@ -232,17 +232,35 @@ int cubics_solve_shard(const cubics_model* m, const cubics_search_config* cfg,
  * work-sharing ring. Each subtree is searched exactly once across the ranks, so stats sum
  * exactly as for cubics_solve_shard. The counter must be reset (cubics_task_queue_reset on the
  * owner, then a barrier) before every search that uses it. A queue opened in the creating
- * process is not supported by CUDA IPC: pass the creator's queue to every local call instead. */
+ * process is not supported by CUDA IPC: pass the creator's queue to every local call instead;
+ * a call on another device of that process enables peer access to the owner's GPU first
+ * (CUBICS_E_UNSUPPORTED when the two GPUs have none). */
 #define CUBICS_TASK_QUEUE_HANDLE_BYTES 64
 typedef struct cubics_task_queue cubics_task_queue; /* opaque */
 int cubics_task_queue_create(int32_t device, cubics_task_queue** out, uint8_t* handle /* may be NULL */);
 int cubics_task_queue_open(int32_t device, const uint8_t* handle, cubics_task_queue** out);
+/* reset: claim counter 0 and no shared incumbent; call on the owner, then barrier, before each search */
 int cubics_task_queue_reset(cubics_task_queue* q);
 int cubics_task_queue_claims(cubics_task_queue* q, uint64_t* claims); /* claim attempts so far */
 int cubics_task_queue_destroy(cubics_task_queue* q);
 int cubics_solve_shard_shared(const cubics_model* m, const cubics_search_config* cfg,
                               int32_t shard_index, int32_t shard_count, cubics_task_queue* queue,
                               cubics_keyed_solution_cb cb, void* user, cubics_result* out);
+
+/* Multi-GPU branch and bound (fd::solve_optimize, search.hpp:77 / search.cpp:187-201, sharded):
+ * the same deterministic frontier (expanded without the bound, so every rank builds the same
+ * one; solutions above it seed the bound), this rank's subtrees searched by the parallel engine,
+ * and - when queue != NULL - subtrees claimed dynamically AND the incumbent objective shared
+ * through the queue state: a system-scope atomicMin on an order-preserving encoding in the
+ * owner's HBM, merged into every GPU's bound every 16 nodes per search context (the B&B shrink
+ * of search.cpp:87-101 then prunes with the best bound of ALL GPUs). queue == NULL: static split,
+ * bounds not shared. out receives this rank's partial stats (they sum across ranks), and
+ * has_solution / objective / best_values this rank's best incumbent; the caller takes the best
+ * over ranks (distributed.solve_distributed). The optimum is exact; node counts depend on the
+ * schedule (as for the single-GPU parallel engine). */
+int cubics_solve_optimize_shard(const cubics_model* m, const cubics_search_config* cfg,
+                                int32_t shard_index, int32_t shard_count, cubics_task_queue* queue,
+                                int64_t* best_values, cubics_result* out);
 
 /* ---- propagation (kernel-level API) ------------------------------------------------------ */
 typedef struct cubics_fixpoint_result { /* fd::FixpointResult (propagation.hpp:106-110) */

@@ -113,7 +113,7 @@ EXPORTED = [
     "cubics_model_create", "cubics_model_parse", "cubics_model_free", "cubics_model_describe",
     "cubics_model_var_name", "cubics_model_validate", "cubics_search_config_init",
     "cubics_solve_satisfy", "cubics_enumerate", "cubics_solutions_free", "cubics_solve_optimize",
-    "cubics_solve_optimize_batch", "cubics_solve_shard", "cubics_solve_shard_shared",
+    "cubics_solve_optimize_batch", "cubics_solve_shard", "cubics_solve_shard_shared", "cubics_solve_optimize_shard",
     "cubics_task_queue_create", "cubics_task_queue_open", "cubics_task_queue_reset", "cubics_task_queue_claims",
     "cubics_task_queue_destroy", "cubics_propagate",
     "cubics_removals", "cubics_last_error", "cubics_build_info", "cubics_device_count", "cubics_warmup",
@@ -154,6 +154,9 @@ def declare(lib):
     lib.cubics_solve_shard_shared.argtypes = [C.c_void_p, P(SearchConfig), C.c_int32, C.c_int32, C.c_void_p,
                                               KEYED_SOLUTION_CB, C.c_void_p, P(Result)]
     lib.cubics_solve_shard_shared.restype = C.c_int
+    lib.cubics_solve_optimize_shard.argtypes = [C.c_void_p, P(SearchConfig), C.c_int32, C.c_int32, C.c_void_p,
+                                                P(C.c_int64), P(Result)]
+    lib.cubics_solve_optimize_shard.restype = C.c_int
     lib.cubics_task_queue_create.argtypes = [C.c_int32, P(C.c_void_p), C.c_char_p]
     lib.cubics_task_queue_create.restype = C.c_int
     lib.cubics_task_queue_open.argtypes = [C.c_int32, C.c_char_p, P(C.c_void_p)]

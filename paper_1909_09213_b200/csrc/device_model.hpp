@@ -112,6 +112,8 @@ struct WorkState {
     int32_t max_depth;     // deepest solution leaf (parallel): key words that can differ
     int32_t best_lock;     // first mode: guards hot.has_bound, which then holds the best record
     int64_t n_tasks;       // frontier expansion: open nodes emitted at split_depth
+    int32_t inc_found;     // parallel B&B: inc_vals holds an incumbent found by this launch
+    int32_t pad2;
 };
 
 struct SearchParams {
@@ -185,6 +187,10 @@ struct SearchParams {
     uint64_t* seg_stats;   // [seg_cap][3]
     int32_t* sol_seg;      // [sol_cap]
     int32_t frames_in_smem; // warp contexts: decision stack in the context's shared memory
+    // multi-GPU branch-and-bound (cubics_solve_optimize_shard): the shared incumbent objective in
+    // the queue owner's HBM (CUDA IPC, system-scope atomics over NVLink), order-preserving u64
+    // encoding (see bound_enc); all ones = none. Null: single GPU.
+    unsigned long long* g_inc;
 };
 
 struct PropParams {

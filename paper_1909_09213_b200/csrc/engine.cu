@@ -568,6 +568,7 @@ struct ShardIO {
     uint64_t n_tasks = 0;         // out: tasks emitted
     const std::vector<int32_t>* seeds = nullptr; // seeded run: task indices of this shard
     unsigned int* claim = nullptr; // shared queue: seeds are claimed through this counter instead
+    unsigned long long* g_inc = nullptr; // multi-GPU B&B: shared incumbent (queue state, IPC-mapped)
 };
 
 // Batched B&B (cubics_solve_optimize_batch): problem i = block i, reference node order.
@@ -754,7 +755,10 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
         const bool shared_q = shard && shard->claim;
         w0.outstanding = n_ctx + (shared_q ? 0 : n_seed);
         w0.hot.has_bound = first_mode ? -1 : (cfg.has_initial_bound ? 1 : 0);
-        w0.bound = cfg.initial_bound;
+        // no initial bound: the worst value, so merging other GPUs' bounds is a plain atomic min/max
+        w0.bound = cfg.has_initial_bound ? cfg.initial_bound
+                                         : (hm.goal == CUBICS_MAXIMIZE ? std::numeric_limits<int64_t>::min()
+                                                                       : std::numeric_limits<int64_t>::max());
         w0.hot.push_ticket = shared_q ? 0u : (uint32_t)n_seed;
         const size_t stage_bytes = a_ws + sizeof(WorkState);
         uint8_t* stage = pinned_arena(dev, stage_bytes);
@@ -841,6 +845,7 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
         S.tasks = shard ? shard->task_dev : nullptr;
         S.n_seed = n_seed;
         S.task_claim = shard ? shard->claim : nullptr;
+        S.g_inc = shard ? shard->g_inc : nullptr;
         S.first_mode = first_mode ? 1 : 0;
         S.seg_cap = seg_cap;
         S.seg_key = reinterpret_cast<uint32_t*>(base + a_segk);
@@ -1190,8 +1195,9 @@ public:
         return *p;
     }
     unsigned size() const { return (unsigned)threads_.size() + 1; }
+    // f(i) for i < n; n must not exceed size() (callers partition by their own n)
     void run(unsigned n, const std::function<void(unsigned)>& f) {
-        n = std::min(n, size());
+        if (n > size()) throw StatusError{CUBICS_E_INVALID, "host pool: more parts than workers"};
         if (n <= 1) {
             if (n) f(0);
             return;
@@ -1269,11 +1275,12 @@ extern "C" int cubics_enumerate(const cubics_model* h, const cubics_search_confi
         std::lock_guard<std::recursive_mutex> lock(g_dev_mu[current_device(cfg->device)]);
         RunOut r = satisfy_run(m, *cfg, !cfg->count_only, out, true);
         const double t1 = now_ms();
+        const uint64_t total = r.rec.count * (uint64_t)n;
+        int64_t* values = alloc_values(std::max<uint64_t>(total, 1)); // before the struct: no leak on throw
         auto* S = new cubics_solutions{};
         S->n_vars = n;
         S->count = r.rec.count;
-        const uint64_t total = r.rec.count * (uint64_t)n;
-        S->values = alloc_values(std::max<uint64_t>(total, 1));
+        S->values = values;
         // offset conversion straight into the returned buffer, split over host threads
         const unsigned nt = total > (1u << 20) ? HostPool::get().size() : 1u;
         const uint64_t count = r.rec.count;
@@ -1320,7 +1327,7 @@ extern "C" int cubics_solve_optimize(const cubics_model* h, const cubics_search_
         out->complete = !r.ws.limit_hit;
         std::vector<uint16_t> best;
         if (parallel) {
-            if (r.ws.hot.has_bound) best = r.inc_vals;
+            if (r.ws.inc_found) best = r.inc_vals;
         } else if (r.rec.count) {
             best.assign(r.rec.vals.end() - n, r.rec.vals.end());
         }
@@ -1380,22 +1387,55 @@ extern "C" int cubics_solve_optimize_batch(const cubics_model* h, const cubics_s
 }
 
 namespace {
-// claim == nullptr: static split (task t goes to shard t % shard_count); otherwise every shard
-// seeds all tasks in DFS order and claims them dynamically through the shared counter
+// Shared queue state (256 bytes in the owner GPU's HBM, CUDA IPC-mapped by the other ranks):
+//   [0]  u32 claim counter              (next frontier subtree to claim)
+//   [8]  u64 shared incumbent, encoded   (bound_enc in search.cuh; all ones = none)
+struct QueueState {
+    uint32_t claim;
+    uint32_t pad;
+    unsigned long long g_inc;
+};
+
+// The search device must reach the queue owner's memory: peer access inside one process (CUDA
+// IPC mappings from another process enable it themselves, cudaIpcMemLazyEnablePeerAccess).
+void ensure_queue_access(int dev, const cubics_task_queue* q) {
+    if (!q || q->device == dev || !q->owner) return;
+    int ok = 0;
+    CU(cudaDeviceCanAccessPeer(&ok, dev, q->device));
+    if (!ok) throw StatusError{CUBICS_E_UNSUPPORTED, "search device cannot access the task queue's GPU (no peer access)"};
+    CU(cudaSetDevice(dev));
+    const cudaError_t e = cudaDeviceEnablePeerAccess(q->device, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+    } else {
+        CU(e);
+    }
+}
+
+// One rank's share of a multi-GPU search (satisfy: every solution, keyed; optimize: branch and
+// bound with the incumbent shared through the queue state). queue == nullptr: static split
+// (task t goes to shard t % shard_count); otherwise every shard seeds all tasks in DFS order
+// and claims them dynamically through the shared counter.
 int solve_shard_impl(const cubics_model* h, const cubics_search_config* cfg, int32_t shard_index,
-                     int32_t shard_count, unsigned int* claim, cubics_keyed_solution_cb cb, void* user,
-                     cubics_result* out) {
+                     int32_t shard_count, cubics_task_queue* queue, cubics_keyed_solution_cb cb, void* user,
+                     cubics_result* out, bool optimize, int64_t* best_values) {
     if (!h || !cfg || !out || shard_count < 1 || shard_index < 0 || shard_index >= shard_count) return CUBICS_E_INVALID;
     return guarded([&]() -> int {
         const double t0 = now_ms();
         std::memset(out, 0, sizeof *out);
         const HostModel& m = h->m;
-        if (m.goal != CUBICS_SATISFY) throw StatusError{CUBICS_E_UNSUPPORTED, "sharded search enumerates (satisfy goal)"};
+        if (optimize && m.goal == CUBICS_SATISFY)
+            throw StatusError{CUBICS_E_NO_OBJECTIVE, "solve_optimize requires a minimize or maximize goal"};
+        if (!optimize && m.goal != CUBICS_SATISFY)
+            throw StatusError{CUBICS_E_UNSUPPORTED, "sharded enumeration needs a satisfy goal (use cubics_solve_optimize_shard)"};
         cubics_search_config c = *cfg;
         c.engine = CUBICS_ENGINE_PARALLEL;
-        pick_engine(c, false);
-        const bool record = cb && !c.count_only;
+        pick_engine(c, optimize);
+        const bool record = !optimize && cb && !c.count_only;
         const int n = m.n_vars();
+        const int dev = current_device(c.device);
+        ensure_queue_access(dev, queue);
+        QueueState* qs = queue ? reinterpret_cast<QueueState*>(queue->counter) : nullptr;
         std::vector<int64_t> vals(n);
         auto deliver = [&](const RunOut& r) {
             for (uint64_t s = 0; s < r.rec.count; ++s) {
@@ -1404,24 +1444,72 @@ int solve_shard_impl(const cubics_model* h, const cubics_search_config* cfg, int
             }
             return true;
         };
-        if (shard_count == 1) {
-            RunOut r;
-            run_search(m, c, CUBICS_ENGINE_PARALLEL, record, record ? default_sol_cap(m, c) : 0, r, true);
-            fill_result(r, out);
+        // a recorded run that found more solutions than its buffer: rerun with the exact size, or
+        // fail loudly when it cannot be repeated (claims through the shared queue are spent)
+        auto full_records = [&](RunOut& r, auto&& rerun, bool repeatable) {
+            if (!record || r.ws.sol_count <= r.rec.count) return;
+            if (!repeatable)
+                throw StatusError{CUBICS_E_CAPACITY, "shard solution buffer overflow (shared-queue run cannot be repeated)"};
+            const uint64_t want = r.ws.sol_count;
+            r = RunOut{};
+            rerun(want);
+        };
+        // best solution of this rank (optimize): objective and values
+        bool has_best = false;
+        int64_t best_obj = 0;
+        std::vector<int64_t> best(n);
+        auto offer = [&](const uint16_t* row) {
+            const int64_t obj = m.offset[m.goal_var] + row[m.goal_var];
+            if (has_best && (m.goal == CUBICS_MINIMIZE ? obj >= best_obj : obj <= best_obj)) return;
+            has_best = true;
+            best_obj = obj;
+            for (int v = 0; v < n; ++v) best[v] = m.offset[v] + row[v];
+        };
+        auto finish = [&]() {
+            if (optimize) {
+                out->has_solution = has_best;
+                if (has_best) {
+                    out->objective = best_obj;
+                    if (best_values) std::copy(best.begin(), best.end(), best_values);
+                }
+            } else {
+                out->has_solution = out->stats.solutions > 0;
+            }
             out->complete = 1;
-            out->has_solution = r.ws.stats[3] > 0;
-            if (record) deliver(r);
             out->total_ms = now_ms() - t0;
             return CUBICS_OK;
+        };
+        if (shard_count == 1) {
+            RunOut r;
+            ShardIO one;
+            one.g_inc = qs ? &qs->g_inc : nullptr;
+            auto go = [&](uint64_t cap) {
+                run_search(m, c, CUBICS_ENGINE_PARALLEL, record, record ? cap : 0, r, true, qs ? &one : nullptr);
+            };
+            go(record ? default_sol_cap(m, c) : 0);
+            full_records(r, go, true);
+            fill_result(r, out);
+            if (optimize && r.ws.inc_found) offer(r.inc_vals.data());
+            if (record) deliver(r);
+            return finish();
         }
         // 1. deterministic frontier: expand the tree (in parallel; exact node semantics) until
-        //    the open nodes at the split depth are plentiful; they are numbered in DFS order
+        //    the open nodes at the split depth are plentiful; they are numbered in DFS order.
+        //    Branch and bound expands without the bound (goal cleared), so every rank builds the
+        //    same frontier whatever the timing; solutions above the frontier seed the bound.
         Prepared P;
         prepare(m, m.words.data(), P);
         const int KW = static_cast<int>((P.depth_bound + 1 + 31) / 32);
         const size_t OS = P.NWP + dev::round4((size_t)KW + 2);
-        const int dev = current_device(c.device);
         std::lock_guard<std::recursive_mutex> lock(g_dev_mu[dev]); // the task buffer lives across two runs
+        HostModel sat_model;
+        const HostModel* exp_model = &m;
+        if (optimize) {
+            sat_model = m;
+            sat_model.goal = CUBICS_SATISFY;
+            exp_model = &sat_model;
+        }
+        const bool exp_record = record || optimize;
         const uint64_t want = 256ull * (uint64_t)shard_count;
         RunOut ex;
         ShardIO io;
@@ -1432,12 +1520,22 @@ int solve_shard_impl(const cubics_model* h, const cubics_search_config* cfg, int
             for (;;) {
                 io.task_dev = reinterpret_cast<uint32_t*>(device_arena(dev, sizeof(uint32_t) * OS * io.task_cap, 1));
                 ex = RunOut{};
-                run_search(m, c, CUBICS_ENGINE_PARALLEL, record, record ? default_sol_cap(m, c) : 0, ex, true, &io);
+                auto go = [&](uint64_t cap) {
+                    run_search(*exp_model, c, CUBICS_ENGINE_PARALLEL, exp_record, exp_record ? cap : 0, ex, true, &io);
+                };
+                go(exp_record ? default_sol_cap(m, c) : 0);
+                if (exp_record && ex.ws.sol_count > ex.rec.count) {
+                    const uint64_t cap = ex.ws.sol_count;
+                    ex = RunOut{};
+                    go(cap);
+                }
                 if (io.n_tasks <= io.task_cap) break;
                 io.task_cap = io.n_tasks;
             }
             if (io.n_tasks >= want || io.n_tasks == 0 || depth >= 64 || (uint64_t)depth >= P.depth_bound) break;
         }
+        if (optimize)
+            for (uint64_t s = 0; s < ex.rec.count; ++s) offer(ex.rec.vals.data() + s * n);
         // 2. DFS rank of each task = order of its path key
         const uint64_t nt = io.n_tasks;
         std::vector<uint32_t> keys(nt * KW);
@@ -1452,7 +1550,7 @@ int solve_shard_impl(const cubics_model* h, const cubics_search_config* cfg, int
         });
         std::vector<int32_t> mine;
         uint64_t extra_d2h = 0;
-        if (claim) {
+        if (qs) {
             // shared queue: claim the (estimated) largest subtrees first, so the last claims are
             // small and the GPUs finish together (list scheduling, largest first). Estimate =
             // log2 of the product of the task's domain sizes; every rank computes the same order.
@@ -1472,14 +1570,27 @@ int solve_shard_impl(const cubics_model* h, const cubics_search_config* cfg, int
             extra_d2h = sizeof(uint32_t) * P.NWP * nt;
         } else
             for (uint64_t r = shard_index; r < nt; r += shard_count) mine.push_back(order[r]);
-        // 3. this shard's subtrees, seeded into the parallel engine
+        // 3. this shard's subtrees, seeded into the parallel engine (B&B: starting from the best
+        //    solution above the frontier, and sharing incumbents through the queue state)
+        cubics_search_config cs = c;
+        if (optimize && has_best &&
+            (!cs.has_initial_bound || (m.goal == CUBICS_MINIMIZE ? best_obj < cs.initial_bound : best_obj > cs.initial_bound))) {
+            cs.has_initial_bound = 1;
+            cs.initial_bound = best_obj;
+        }
         RunOut run;
         if (!mine.empty()) {
             ShardIO seeded;
             seeded.task_dev = io.task_dev;
             seeded.seeds = &mine;
-            seeded.claim = claim;
-            run_search(m, c, CUBICS_ENGINE_PARALLEL, record, record ? default_sol_cap(m, c) : 0, run, true, &seeded);
+            seeded.claim = qs ? &qs->claim : nullptr;
+            seeded.g_inc = qs && optimize ? &qs->g_inc : nullptr;
+            auto go = [&](uint64_t cap) {
+                run_search(m, cs, CUBICS_ENGINE_PARALLEL, record, record ? cap : 0, run, true, &seeded);
+            };
+            go(record ? default_sol_cap(m, c) : 0);
+            full_records(run, go, qs == nullptr);
+            if (optimize && run.ws.inc_found) offer(run.inc_vals.data());
         }
         fill_result(run, out);
         if (shard_index == 0) { // nodes above the frontier belong to shard 0
@@ -1492,32 +1603,31 @@ int solve_shard_impl(const cubics_model* h, const cubics_search_config* cfg, int
         out->h2d_bytes += ex.h2d;
         out->d2h_bytes += ex.d2h + sizeof(uint32_t) * KW * nt + extra_d2h;
         out->kernel_launches += ex.launches;
-        out->complete = 1;
-        out->has_solution = out->stats.solutions > 0;
         if (record) {
-            if (shard_index == 0 && !deliver(ex)) {
-                out->total_ms = now_ms() - t0;
-                return CUBICS_OK;
-            }
+            if (shard_index == 0 && !deliver(ex)) return finish();
             if (!mine.empty()) deliver(run);
         }
-        out->total_ms = now_ms() - t0;
-        return CUBICS_OK;
+        return finish();
     });
 }
 } // namespace
 
 extern "C" int cubics_solve_shard(const cubics_model* h, const cubics_search_config* cfg, int32_t shard_index,
                                   int32_t shard_count, cubics_keyed_solution_cb cb, void* user, cubics_result* out) {
-    return solve_shard_impl(h, cfg, shard_index, shard_count, nullptr, cb, user, out);
+    return solve_shard_impl(h, cfg, shard_index, shard_count, nullptr, cb, user, out, false, nullptr);
 }
 
 extern "C" int cubics_solve_shard_shared(const cubics_model* h, const cubics_search_config* cfg, int32_t shard_index,
                                          int32_t shard_count, cubics_task_queue* queue, cubics_keyed_solution_cb cb,
                                          void* user, cubics_result* out) {
     if (!queue) return CUBICS_E_INVALID;
-    return solve_shard_impl(h, cfg, shard_index, shard_count, reinterpret_cast<unsigned int*>(queue->counter), cb, user,
-                            out);
+    return solve_shard_impl(h, cfg, shard_index, shard_count, queue, cb, user, out, false, nullptr);
+}
+
+extern "C" int cubics_solve_optimize_shard(const cubics_model* h, const cubics_search_config* cfg, int32_t shard_index,
+                                           int32_t shard_count, cubics_task_queue* queue, int64_t* best_values,
+                                           cubics_result* out) {
+    return solve_shard_impl(h, cfg, shard_index, shard_count, queue, nullptr, nullptr, out, true, best_values);
 }
 
 // Shared task queue: one u32 claim counter in the owner GPU's HBM, mapped into the other ranks'
@@ -1531,6 +1641,9 @@ extern "C" int cubics_task_queue_create(int32_t device, cubics_task_queue** out,
         void* p = nullptr;
         CU(cudaMalloc(&p, 256));
         CU(cudaMemset(p, 0, 256));
+        QueueState init{};
+        init.g_inc = ~0ull; // no incumbent
+        CU(cudaMemcpy(p, &init, sizeof init, cudaMemcpyHostToDevice));
         if (handle) {
             cudaIpcMemHandle_t hd;
             cudaError_t e = cudaIpcGetMemHandle(&hd, p);
@@ -1565,7 +1678,10 @@ extern "C" int cubics_task_queue_reset(cubics_task_queue* q) {
     if (!q) return CUBICS_E_INVALID;
     return guarded([&]() -> int {
         CU(cudaSetDevice(q->device));
+        QueueState init{};
+        init.g_inc = ~0ull; // no incumbent
         CU(cudaMemset(q->counter, 0, 256));
+        CU(cudaMemcpy(q->counter, &init, sizeof init, cudaMemcpyHostToDevice));
         CU(cudaDeviceSynchronize());
         return CUBICS_OK;
     });

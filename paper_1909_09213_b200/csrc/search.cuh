@@ -83,6 +83,33 @@ static __device__ __noinline__ int claim_task(unsigned int* counter, int n_seed,
     return i < (unsigned)n_seed ? n_ctx + (int)i : -1;
 }
 
+// Shared incumbent across GPUs: objectives as u64 whose unsigned order is "better first", so one
+// system-scope atomicMin keeps the best (minimise: v ^ 2^63; maximise: ~(v ^ 2^63)).
+__device__ __forceinline__ unsigned long long bound_enc(long long v, bool minimizing) {
+    const unsigned long long u = (unsigned long long)v ^ 0x8000000000000000ull;
+    return minimizing ? u : ~u;
+}
+__device__ __forceinline__ long long bound_dec(unsigned long long e, bool minimizing) {
+    return (long long)((minimizing ? e : ~e) ^ 0x8000000000000000ull);
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_sys_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+// out of line: runs every 16 nodes per context and must not cost the search loop registers
+static __device__ __noinline__ void pull_global_bound(WorkState* ws, const unsigned long long* g_inc, bool minimizing) {
+    const unsigned long long e = ld_relaxed_sys_u64(g_inc);
+    if (e == ~0ull) return;
+    const long long v = bound_dec(e, minimizing);
+    if (minimizing)
+        atomicMin(reinterpret_cast<long long*>(&ws->bound), v);
+    else
+        atomicMax(reinterpret_cast<long long*>(&ws->bound), v);
+    __threadfence();
+    if (!*reinterpret_cast<volatile int32_t*>(&ws->hot.has_bound)) atomicExch(&ws->hot.has_bound, 1);
+}
+
 // DFS path key: decision at depth d is bit (31 - d%32) of word d/32, so comparing the words as
 // unsigned integers, most significant first, is the reference's DFS (preorder) order.
 // path_right_word: word i of the key of the right child taken at depth d (prefix [0,d) kept,
@@ -352,7 +379,11 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
                              : "memory");
             else
                 hot = ld_volatile_v4(reinterpret_cast<const uint4*>(&ws->hot));
-            if (optimizing) g_bound = ld_volatile_s64(&ws->bound);
+            if (optimizing) {
+                // other GPUs' incumbents: merged into this launch's bound every 16 nodes
+                if (kSplit && P.g_inc && (nodes & 15) == 1) pull_global_bound(ws, P.g_inc, minimizing);
+                g_bound = ld_volatile_s64(&ws->bound);
+            }
             my_busy = ld_volatile(&P.outbox_busy[ctx]);
         }
         if (optimizing) { // branch-and-bound shrink (:87-101), done by thread 0
@@ -492,9 +523,15 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
                         volatile int32_t* ghb = &ws->hot.has_bound;
                         if (!*ghb || (minimizing ? val < *gb : val > *gb)) {
                             for (int v = 0; v < n; ++v) P.inc_vals[v] = (uint16_t)dom_first<W>(dom + (size_t)v * W);
-                            *gb = val;
+                            ws->inc_found = 1;
+                            // atomic: a concurrent pull of another GPU's better bound must win
+                            if (minimizing)
+                                atomicMin(reinterpret_cast<long long*>(&ws->bound), val);
+                            else
+                                atomicMax(reinterpret_cast<long long*>(&ws->bound), val);
                             __threadfence();
                             *ghb = 1;
+                            if (kSplit && P.g_inc) atomicMin_system(P.g_inc, bound_enc(val, minimizing));
                         }
                         spin_unlock(&ws->inc_lock);
                         g_bound = *gb; // our own incumbent is visible to us at once

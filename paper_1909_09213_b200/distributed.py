@@ -61,35 +61,73 @@ def merge_keyed(streams):
     return [v for _, v in heapq.merge(*[sorted(s) for s in streams], key=lambda kv: kv[0])]
 
 
+def _optimize_shard(model, cfg, rank, world, queue=None):
+    return S.solve_optimize_shard(model, cfg, rank, world, queue=queue)
+
+
 def solve_distributed(model, cfg: S.SearchConfig, rank: int, world: int, collect: bool = True,
                       shard_fn=None, device=None, queue=None):
     """Run this rank's shard and combine over the default torch.distributed process group.
 
-    Returns (stats tuple, solutions in DFS order or None on ranks != 0, max device ms over ranks).
-    shard_fn(model, cfg, rank, world, collect) -> (SatisfyResult, [(key, values)]) may replace
-    the GPU shard (tests use it to exercise the collective plumbing on CPU/gloo).
+    Satisfy goals: returns (stats tuple, solutions in DFS order or None on ranks != 0, max device
+    ms over ranks). Minimize / maximize goals (branch and bound, cubics_solve_optimize_shard):
+    returns (stats tuple, best Solution over all ranks or None, max device ms); with a queue the
+    GPUs share the incumbent while they search.
+    shard_fn(model, cfg, rank, world, collect) -> (SatisfyResult, [(key, values)]) (satisfy) or
+    shard_fn(model, cfg, rank, world) -> OptimizeResult (optimize) may replace the GPU shard (tests
+    use it to exercise the collective plumbing on CPU/gloo).
     queue (from shared_task_queue) switches to dynamic subtree claiming; it is reset here.
+    A rank whose shard raises still joins every collective: the error flag travels with the stats
+    all-reduce and every rank raises, instead of the others blocking forever.
     """
     import torch
     import torch.distributed as dist
 
+    optimize = model.goal != 0
+    r, sols, err = None, [], None
     if queue is not None:
-        if rank == 0:
-            queue.reset()
+        try:
+            if rank == 0:
+                queue.reset()
+        except Exception as e:  # noqa: BLE001 - re-raised after the collectives
+            err = e
         dist.barrier()
-        r, sols = _collect_shard(model, cfg, rank, world, collect, queue=queue)
-    else:
-        fn = shard_fn or _collect_shard
-        r, sols = fn(model, cfg, rank, world, collect)
+    if err is None:
+        try:
+            if optimize:
+                r = shard_fn(model, cfg, rank, world) if shard_fn else _optimize_shard(model, cfg, rank, world, queue)
+            elif queue is not None:
+                r, sols = _collect_shard(model, cfg, rank, world, collect, queue=queue)
+            else:
+                r, sols = (shard_fn or _collect_shard)(model, cfg, rank, world, collect)
+        except Exception as e:  # noqa: BLE001 - re-raised after the collectives
+            err = e
     dev = device if device is not None else "cpu"
-    t = torch.tensor(list(r.stats.as_tuple()), dtype=torch.int64, device=dev)
+    stats = list(r.stats.as_tuple()) if r is not None else [0, 0, 0, 0]
+    t = torch.tensor(stats + [1 if err is not None else 0], dtype=torch.int64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
-    ms = torch.tensor([r.device_ms], dtype=torch.float64, device=dev)
+    ms = torch.tensor([r.device_ms if r is not None else 0.0], dtype=torch.float64, device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    if int(t[4].item()):
+        if err is not None:
+            raise err
+        raise RuntimeError("solve_distributed: another rank's shard failed")
+    total = tuple(int(x) for x in t[:4].tolist())
+    if optimize:
+        mine = (r.best.objective, r.best.values) if r is not None and r.best is not None else None
+        allb = [None] * world
+        dist.all_gather_object(allb, mine)
+        best = None
+        for cand in allb:  # best objective; ties to the lowest rank (deterministic)
+            if cand is None:
+                continue
+            if best is None or (cand[0] < best[0] if model.goal == 1 else cand[0] > best[0]):
+                best = cand
+        return total, (S.Solution(best[1], best[0]) if best else None), float(ms.item())
     merged = None
     if collect:
         gathered = [None] * world if rank == 0 else None
         dist.gather_object(sols, gathered, dst=0)
         if rank == 0:
             merged = merge_keyed(gathered)
-    return tuple(int(x) for x in t.tolist()), merged, float(ms.item())
+    return total, merged, float(ms.item())

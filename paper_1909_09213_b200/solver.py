@@ -623,6 +623,22 @@ def solve_shard(model: Model, cfg: SearchConfig, shard_index: int, shard_count: 
                          res.h2d_bytes, res.d2h_bytes, res.kernel_launches)
 
 
+def solve_optimize_shard(model: Model, cfg: SearchConfig, shard_index: int, shard_count: int,
+                         queue: TaskQueue | None = None) -> OptimizeResult:
+    """One rank's share of a multi-GPU branch and bound (cubics_solve_optimize_shard): partial
+    stats (summed across ranks) and this rank's best incumbent (the best over ranks is the
+    optimum). With a TaskQueue the subtrees are claimed dynamically and the incumbent objective is
+    shared between the GPUs through the queue state (reset it before every search)."""
+    res = A.Result()
+    best = (C.c_int64 * max(1, model.n_vars))()
+    c = cfg.to_c()
+    _check(lib().cubics_solve_optimize_shard(model.handle, C.byref(c), shard_index, shard_count,
+                                             queue.ptr if queue is not None else None, best, C.byref(res)),
+           "solve_optimize_shard")
+    sol = Solution([best[i] for i in range(model.n_vars)], res.objective) if res.has_solution else None
+    return OptimizeResult(sol, bool(res.complete), _stats(res), res.engine, res.contexts, res.device_ms, res.total_ms)
+
+
 # ------------------------------------------------------------------ propagation
 def propagate_fixpoint(model: Model, domains=None, alldiff=A.ARC_CONSISTENT, max_rounds=0):
     """fd::propagate_fixpoint over `domains` (default: the model's); returns (domains, FixpointResult)."""

@@ -68,3 +68,72 @@ def test_two_rank_gloo_allreduce_and_merge():
     merged = out[0][1]
     assert len(merged) == 92 and merged[0] == g["first"]
     assert out[1][1] is None
+
+
+def _worker_opt(rank, world, port, q, fail_rank):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    import oracle_binding as O
+    from paper_1909_09213_b200 import distributed as D
+    from paper_1909_09213_b200 import solver as S
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        m = S.parse_model(G.model_text("golomb6"))
+        opt = O.solve_optimize(m)
+
+        def fake_shard(model, cfg, r, w):
+            if r == fail_rank:
+                raise S.CapacityError("shard buffer overflow on rank %d" % r)
+            # the optimum sits on the last rank; the others hold worse incumbents (or none)
+            part = [x // w + (x % w if r == 0 else 0) for x in opt.stats.as_tuple()]
+            if r == w - 1:
+                best = opt.best
+            elif r == 0:
+                best = S.Solution(list(opt.best.values), opt.best.objective + 5)
+            else:
+                best = None
+            return S.OptimizeResult(best, True, S.SearchStats(*part), device_ms=float(r))
+
+        try:
+            stats, best, ms = D.solve_distributed(m, S.SearchConfig(), rank, world, shard_fn=fake_shard)
+            q.put((rank, "ok", stats, (best.objective, best.values) if best else None, ms, opt.stats.as_tuple(),
+                   opt.best.objective))
+        except Exception as e:  # noqa: BLE001
+            q.put((rank, "raised", type(e).__name__, str(e), None, None, None))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run_opt(world, fail_rank):
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker_opt, args=(r, world, port, q, fail_rank)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = {}
+    for _ in range(world):
+        rec = q.get(timeout=120)
+        out[rec[0]] = rec[1:]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return out
+
+
+def test_two_rank_gloo_branch_and_bound_best_over_ranks():
+    out = _run_opt(2, fail_rank=-1)
+    for rank in range(2):
+        status, stats, best, ms, exp_stats, exp_obj = out[rank]
+        assert status == "ok"
+        assert stats == exp_stats  # partial stats sum exactly
+        assert best[0] == exp_obj == 17  # golomb6 optimum, from the rank that holds it
+        assert ms == 1.0
+
+
+def test_failing_rank_raises_on_every_rank_instead_of_hanging():
+    out = _run_opt(2, fail_rank=1)
+    assert out[1][0] == "raised" and out[1][1] == "CapacityError"
+    assert out[0][0] == "raised" and "another rank" in out[0][2]

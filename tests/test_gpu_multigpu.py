@@ -1,0 +1,115 @@
+"""Multi-GPU search paths on one B200: the ranks' shard calls run one after another on cuda:0
+(or as two processes mapping one queue through CUDA IPC), which exercises every line of the
+N-GPU code without ranks that wait on each other's kernels.
+
+* Branch and bound across shards (cubics_solve_optimize_shard): Golomb m=10 must reach the
+  reference's optimum 55 and its ruler 0 1 6 10 23 26 34 41 53 55 (the optimal ruler is unique
+  once d1_2 < d9_10 breaks the mirror symmetry, so every complete B&B returns the reference's
+  solution) for world 2, 3 and 8, static split and shared queue (shared incumbent).
+* The same through distributed.solve_distributed in two processes (gloo plumbing, IPC queue).
+"""
+import socket
+
+import pytest
+
+import golden_cases as G
+from paper_1909_09213_b200 import solver as S
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def engine_present():
+    assert S.device_count() >= 1, "no CUDA device visible to libcubics"
+
+
+def _best_over(results, minimize=True):
+    best = None
+    for r in results:
+        if r.best is None:
+            continue
+        if best is None or (r.best.objective < best.objective if minimize else r.best.objective > best.objective):
+            best = r.best
+    return best
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+@pytest.mark.parametrize("shared", [False, True])
+@pytest.mark.parametrize("inst", ["golomb8", "golomb10"])
+def test_branch_and_bound_across_shards(inst, world, shared):
+    g = G.goldens()[inst]
+    m = S.parse_model(G.model_text(inst))
+    q = S.TaskQueue.create(0) if shared else None
+    try:
+        if q is not None:
+            q.reset()
+        res = [S.solve_optimize_shard(m, S.SearchConfig(device=0), r, world, queue=q) for r in range(world)]
+    finally:
+        if q is not None:
+            q.close()
+    best = _best_over(res)
+    assert best is not None and best.objective == g["objective"]
+    assert best.values == g["best"]
+    assert all(r.complete for r in res)
+    # every rank searched something or found the frontier closed; rank 0 counts the expansion
+    assert sum(r.stats.nodes for r in res) > 0
+
+
+def test_optimize_shard_single_rank_matches_reference_optimum():
+    g = G.goldens()["golomb9"]
+    m = S.parse_model(G.model_text("golomb9"))
+    r = S.solve_optimize_shard(m, S.SearchConfig(device=0), 0, 1)
+    assert r.best.objective == g["objective"] and r.best.values == g["best"]
+
+
+def test_optimize_shard_rejects_satisfy_model():
+    m = S.parse_model(G.model_text("nq8"))
+    with pytest.raises(S.LogicError):
+        S.solve_optimize_shard(m, S.SearchConfig(device=0), 0, 2)
+
+
+def _bnb_worker(rank, world, port, inst, out):
+    import os
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    from paper_1909_09213_b200 import distributed as D
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        m = S.parse_model(G.model_text(inst))
+        q = D.shared_task_queue(rank, world, device=0)
+        res = []
+        for _ in range(2):
+            stats, best, _ = D.solve_distributed(m, S.SearchConfig(device=0), rank, world, queue=q)
+            res.append((stats, best.objective if best else None, best.values if best else None))
+        dist.barrier()
+        q.close()
+        dist.barrier()
+        out.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_distributed_branch_and_bound_two_processes_ipc():
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    inst, world = "golomb9", 2
+    ctx = mp.get_context("spawn")
+    out = ctx.Queue()
+    procs = [ctx.Process(target=_bnb_worker, args=(r, world, port, inst, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(out.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    g = G.goldens()[inst]
+    for rank in range(world):
+        for stats, obj, vals in got[rank]:
+            assert obj == g["objective"] and vals == g["best"]
+            assert stats[0] > 0
