@@ -49,7 +49,7 @@ def ncu_traffic(instance):
     """roofline.traffic: dram__bytes_read.sum + dram__bytes_write.sum of the search kernel from one
     committed `ncu --set full` capture of this workload (scripts/ncu_traffic.py), per launch."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r02_ncu_traffic.json")) as f:
             rec = json.load(f)[instance]
         return rec["dram_read_bytes"] + rec["dram_write_bytes"], rec["report"]
     except Exception:  # noqa: BLE001
