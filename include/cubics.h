@@ -177,7 +177,11 @@ typedef struct cubics_result {
 } cubics_result;
 
 /* Receives each solution (values indexed by var id, as fd::Solution::values) in the
- * reference's DFS order, on the calling thread. Return 0 to stop the stream. */
+ * reference's DFS order, on the calling thread, WHILE the device search runs (search.cpp:134-156):
+ * the kernel streams solutions through a ring in host-mapped pinned memory; the parallel engine's
+ * subtree segments put them back into DFS order. Return 0 to stop the stream: the device search
+ * stops at once and the result carries the reference's stats at that solution (search.cpp:147-149).
+ * The callback must not start another search on the same device (CUBICS_E_INVALID). */
 typedef int32_t (*cubics_solution_cb)(void* user, const int64_t* values, int32_t n_vars);
 
 int cubics_solve_satisfy(const cubics_model* m, const cubics_search_config* cfg,

@@ -114,6 +114,8 @@ struct WorkState {
     int64_t n_tasks;       // frontier expansion: open nodes emitted at split_depth
     int32_t inc_found;     // parallel B&B: inc_vals holds an incumbent found by this launch
     int32_t pad2;
+    uint64_t ev_head;      // streaming: event slots reserved
+    uint64_t ev_tail;      // streaming: the host's consumed count as last read over PCIe
 };
 
 struct SearchParams {
@@ -191,7 +193,21 @@ struct SearchParams {
     // the queue owner's HBM (CUDA IPC, system-scope atomics over NVLink), order-preserving u64
     // encoding (see bound_enc); all ones = none. Null: single GPU.
     unsigned long long* g_inc;
+    // streaming delivery (cubics_solve_satisfy with a callback): solutions, and in the parallel
+    // engine the segment events that put them back into DFS order, go into a ring in host-mapped
+    // pinned memory that the calling thread drains while the kernel runs (see search.cuh EvKind).
+    // The host stops the search by setting ws->hot.stop from a second stream.
+    int32_t stream;
+    uint32_t ev_cap;                         // slots
+    uint32_t ev_slot;                        // bytes per slot
+    uint32_t ev_epoch;                       // per-call tag in the slots' sequence words
+    uint8_t* ev_ring;                        // host-mapped [ev_cap][ev_slot]
+    const unsigned long long* ev_tail_host;  // host-mapped: events the host has consumed
 };
+
+// streaming event kinds and slot header bytes (search.cuh ev_commit, engine.cu drain_stream)
+enum EvKind : uint32_t { EV_SOL = 1, EV_NEW = 2, EV_END = 3 };
+constexpr int kEvHeader = 40;
 
 struct PropParams {
     DevModel M;

@@ -10,6 +10,10 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
+#include <map>
+#include <memory>
+#include <unordered_map>
 #include <chrono>
 #include <condition_variable>
 #include <functional>
@@ -93,6 +97,20 @@ uint8_t* pinned_arena(int dev, size_t bytes, int slot = 0) {
         size_t want = std::max(bytes, a.cap * 3 / 2);
         CU(cudaMallocHost(&a.ptr, want));
         a.cap = want;
+    }
+    return static_cast<uint8_t*>(a.ptr);
+}
+
+// host-mapped pinned memory (streaming event ring), grow-only per device
+Arena g_mapped[64];
+uint8_t* mapped_arena(int dev, size_t bytes) {
+    Arena& a = g_mapped[dev];
+    if (a.cap < bytes) {
+        if (a.ptr) cudaFreeHost(a.ptr);
+        a.ptr = nullptr;
+        a.cap = 0;
+        CU(cudaHostAlloc(&a.ptr, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+        a.cap = bytes;
     }
     return static_cast<uint8_t*>(a.ptr);
 }
@@ -424,7 +442,9 @@ struct DevState {
     bool checked = false;
     bool ok = false;
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr; // streaming: the stop flag is written on this stream mid-kernel
     cudaEvent_t e0 = nullptr, e1 = nullptr;
+    bool streaming = false;      // a callback of a streaming search is running on this device
 };
 DevState g_dev[64];
 int g_count = -1;
@@ -448,6 +468,7 @@ int current_device(int want) {
         s.checked = true;
         if (s.ok) {
             CU(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+            CU(cudaStreamCreateWithFlags(&s.side, cudaStreamNonBlocking));
             CU(cudaEventCreate(&s.e0));
             CU(cudaEventCreate(&s.e1));
         }
@@ -585,6 +606,167 @@ struct BatchIO {
     std::vector<uint16_t> inc;      // [count][n]
 };
 
+// Streaming delivery (cubics_solve_satisfy with a callback; search.cpp:134-156): the kernel
+// writes solution / segment events into a host-mapped ring (search.cuh EvKind) and the calling
+// thread runs the callback while the search goes on. visit(row, stats) gets each solution's bit
+// indices and the reference's (nodes, failures, rounds) at its emission; false stops the search.
+struct StreamIO {
+    std::function<bool(const uint16_t* row, const uint64_t* stats)> visit;
+    // out
+    bool stopped = false;
+    uint64_t delivered = 0;
+    uint64_t stop_stats[3] = {0, 0, 0};
+};
+
+// Puts the parallel engine's events back into DFS order. Segments (the root = 0, each handed-out
+// subtree = ring ticket + 1) are contiguous DFS intervals ordered by root key; the cursor is the
+// leftmost unfinished one. Its solutions go out as they arrive, the others' wait in host memory;
+// when the cursor finishes, every segment left of the next one has been announced (a donor's
+// EV_NEW precedes its EV_END), so the next key in the map is the next interval.
+class SegmentOrder {
+public:
+    SegmentOrder(int KW, int n, StreamIO& io) : KW_(KW), n_(n), io_(io) {
+        Seg& root = segs_[0];
+        root.key.assign(KW, 0u);
+        order_.emplace(root.key, 0u);
+    }
+    void on_new(uint32_t id, const uint32_t* key) {
+        std::vector<uint32_t> k(key, key + KW_);
+        if (!done_ && !(segs_.at(cursor_).key < k))
+            throw StatusError{CUBICS_E_INVALID, "stream: segment announced left of the delivery cursor"};
+        Seg& s = segs_[id];
+        s.key = k;
+        order_.emplace(std::move(k), id);
+    }
+    void on_sol(uint32_t id, const uint16_t* row, const uint64_t* snap) {
+        if (io_.stopped) return;
+        auto it = segs_.find(id);
+        if (it == segs_.end()) throw StatusError{CUBICS_E_INVALID, "stream: solution of an unknown segment"};
+        if (id == cursor_ && !done_) {
+            deliver(row, snap);
+            return;
+        }
+        Seg& s = it->second;
+        s.rows.insert(s.rows.end(), row, row + n_);
+        s.snaps.insert(s.snaps.end(), snap, snap + 3);
+    }
+    void on_end(uint32_t id, const uint64_t* st) {
+        auto it = segs_.find(id);
+        if (it == segs_.end()) return;
+        it->second.done = true;
+        std::copy_n(st, 3, it->second.st);
+        while (!io_.stopped && !done_ && segs_.at(cursor_).done) {
+            Seg& c = segs_.at(cursor_);
+            for (int i = 0; i < 3; ++i) prefix_[i] += c.st[i];
+            order_.erase(order_.begin());
+            segs_.erase(cursor_);
+            if (order_.empty()) {
+                done_ = true;
+                break;
+            }
+            cursor_ = order_.begin()->second;
+            Seg& nx = segs_.at(cursor_);
+            for (size_t r = 0; r * 3 < nx.snaps.size() && !io_.stopped; ++r)
+                deliver(nx.rows.data() + r * n_, nx.snaps.data() + r * 3);
+            nx.rows.clear();
+            nx.rows.shrink_to_fit();
+            nx.snaps.clear();
+            nx.snaps.shrink_to_fit();
+        }
+    }
+
+private:
+    struct Seg {
+        std::vector<uint32_t> key;
+        bool done = false;
+        uint64_t st[3] = {0, 0, 0};
+        std::vector<uint16_t> rows;
+        std::vector<uint64_t> snaps;
+    };
+    void deliver(const uint16_t* row, const uint64_t* snap) {
+        uint64_t st[3];
+        for (int i = 0; i < 3; ++i) st[i] = prefix_[i] + snap[i];
+        ++io_.delivered;
+        if (!io_.visit(row, st)) {
+            io_.stopped = true;
+            std::copy_n(st, 3, io_.stop_stats);
+        }
+    }
+    int KW_, n_;
+    StreamIO& io_;
+    std::unordered_map<uint32_t, Seg> segs_;
+    std::map<std::vector<uint32_t>, uint32_t> order_;
+    uint32_t cursor_ = 0;
+    bool done_ = false;
+    uint64_t prefix_[3] = {0, 0, 0};
+};
+
+// The calling thread's side of the stream: consume slots in ticket order until the kernel has
+// finished and every reserved slot is drained, or until the callback stops the search (then the
+// stop flag goes to the device on the side stream and the rest of the ring is ignored).
+void drain_stream(uint8_t* ring, uint32_t cap, uint32_t slot_bytes, volatile unsigned long long* tail_host,
+                  unsigned long long epoch, int KW, int n, bool parallel, cudaEvent_t done_ev, int32_t* dev_stop, const int32_t* host_one,
+                  cudaStream_t side, StreamIO& io) {
+    std::unique_ptr<SegmentOrder> order;
+    if (parallel) order.reset(new SegmentOrder(KW, n, io));
+    uint64_t tail = 0;
+    bool kernel_done = false;
+    int idle = 0;
+    for (;;) {
+        uint8_t* s = ring + (size_t)(tail % cap) * slot_bytes;
+        const unsigned long long seq = *reinterpret_cast<volatile unsigned long long*>(s);
+        if (seq == ((epoch << 40) | (tail + 1))) {
+            std::atomic_thread_fence(std::memory_order_acquire);
+            const uint32_t kind = *reinterpret_cast<volatile uint32_t*>(s + 8);
+            const uint32_t seg = *reinterpret_cast<volatile uint32_t*>(s + 12);
+            uint64_t st[3];
+            std::memcpy(st, s + 16, sizeof st);
+            const uint32_t* key = reinterpret_cast<const uint32_t*>(s + kEvHeader);
+            const uint16_t* row = reinterpret_cast<const uint16_t*>(s + kEvHeader + 4 * KW);
+            if (kind == EV_SOL) {
+                if (order) {
+                    order->on_sol(seg, row, st);
+                } else if (!io.stopped) {
+                    ++io.delivered;
+                    if (!io.visit(row, st)) {
+                        io.stopped = true;
+                        std::copy_n(st, 3, io.stop_stats);
+                    }
+                }
+            } else if (kind == EV_NEW && order) {
+                order->on_new(seg, key);
+            } else if (kind == EV_END && order) {
+                order->on_end(seg, st);
+            }
+            ++tail;
+            if ((tail & 255) == 0) *tail_host = tail;
+            idle = 0;
+            if (io.stopped) {
+                CU(cudaMemcpyAsync(dev_stop, host_one, sizeof(int32_t), cudaMemcpyHostToDevice, side));
+                CU(cudaStreamSynchronize(side));
+                return;
+            }
+            continue;
+        }
+        *tail_host = tail;
+        if (kernel_done) { // finished and nothing left: every reserved slot was written
+            if (std::getenv("CUBICS_DEBUG"))
+                std::fprintf(stderr, "[cubics] stream: %llu events, %llu delivered, next seq %llx want %llx\n",
+                             (unsigned long long)tail, (unsigned long long)io.delivered, seq,
+                             (epoch << 40) | (tail + 1));
+            return;
+        }
+        const cudaError_t q = cudaEventQuery(done_ev);
+        if (q == cudaSuccess) {
+            kernel_done = true; // one more pass over what the last contexts wrote
+            continue;
+        }
+        if (q != cudaErrorNotReady) CU(q);
+        if (++idle > 64) std::this_thread::sleep_for(std::chrono::microseconds(20));
+        else std::this_thread::yield();
+    }
+}
+
 __global__ void gather_tasks(const uint32_t* src, const int32_t* idx, int n, size_t os, uint32_t* dst) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < (size_t)n * os; i += (size_t)gridDim.x * blockDim.x)
         dst[i] = src[(size_t)idx[i / os] * os + i % os];
@@ -592,9 +774,17 @@ __global__ void gather_tasks(const uint32_t* src, const int32_t* idx, int n, siz
 
 // One device search: upload, launch, download.
 void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine, bool record, uint64_t sol_cap,
-                RunOut& out, bool want_keys = false, ShardIO* shard = nullptr, BatchIO* batch = nullptr) {
+                RunOut& out, bool want_keys = false, ShardIO* shard = nullptr, BatchIO* batch = nullptr,
+                StreamIO* sio = nullptr) {
     const int dev = current_device(cfg.device);
     std::lock_guard<std::recursive_mutex> lock(g_dev_mu[dev]);
+    // a solution callback runs while its search still owns this device's arenas and stream
+    if (g_dev[dev].streaming)
+        throw StatusError{CUBICS_E_INVALID, "a solution callback cannot start another search on the same device"};
+    if (sio) {
+        record = false;
+        sol_cap = 0;
+    }
     Prepared P;
     prepare(hm, hm.words.data(), P);
     const int n = P.n;
@@ -623,8 +813,10 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
     const bool parallel = engine == CUBICS_ENGINE_PARALLEL;
     const bool keyed = parallel || (shard && shard->split_depth > 0);
     // exact parallel first solution: complete otherwise-equal search, max_solutions == 1
-    const bool first_mode = parallel && !shard && hm.goal == CUBICS_SATISFY && cfg.max_solutions == 1 &&
+    const bool first_mode = parallel && !shard && !sio && hm.goal == CUBICS_SATISFY && cfg.max_solutions == 1 &&
                             cfg.node_limit == 0;
+    if (sio && (shard || batch || (parallel && hm.goal != CUBICS_SATISFY)))
+        throw StatusError{CUBICS_E_INVALID, "streaming: reference-order engines, or the parallel engine on satisfy goals"};
     if (first_mode) {
         record = true;
         sol_cap = 65536;
@@ -666,7 +858,10 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
         if (L.total > kSmemBudget) throw StatusError{CUBICS_E_UNSUPPORTED, "search context does not fit in shared memory"};
     }
     // propagator features the model needs: the lean kernel instantiations skip the rest
-    const int feat = (P.nl ? 1 : 0) | (P.ntb + P.ntn ? 2 : 0) | (P.big_words ? 4 : 0) | (first_mode ? 8 : 0) |
+    // F_FIRST (8): segment bookkeeping, also what streaming needs (a reference-order search
+    // wider than 512 threads runs the generic kernel, whose lean instantiations do not stream)
+    const int feat = (P.nl ? 1 : 0) | (P.ntb + P.ntn ? 2 : 0) | (P.big_words ? 4 : 0) |
+                     (first_mode || sio ? 8 : 0) |
                      (P.lin_g > 1 ? dev::F_LONG : 0) |
                      (hm.goal == CUBICS_SATISFY && !shard ? dev::F_NOOPT | dev::F_NOSPLIT : 0);
     int n_ctx = batch ? batch->count : 1;
@@ -858,6 +1053,26 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
         S.batch_stats = reinterpret_cast<uint64_t*>(base + a_bstats);
         S.batch_flags = reinterpret_cast<int32_t*>(base + a_bflags);
         S.batch_inc = reinterpret_cast<uint16_t*>(base + a_binc);
+        // streaming: [host tail u64 | stop source i32 | pad to 64] [ring of cap slots]
+        uint8_t* ev_host = nullptr;
+        uint32_t ev_cap = 0, ev_slot = 0;
+        static uint32_t epochs[64];
+        if (sio) {
+            ev_slot = (uint32_t)(((size_t)kEvHeader + 4 * (size_t)KW + 2 * (size_t)n + 15) & ~size_t(15));
+            ev_cap = (uint32_t)std::max<size_t>(256, std::min<size_t>((size_t)1 << 20, ((size_t)64 << 20) / ev_slot));
+            ev_host = mapped_arena(dev, 64 + (size_t)ev_cap * ev_slot);
+            *reinterpret_cast<volatile unsigned long long*>(ev_host) = 0;
+            *reinterpret_cast<volatile int32_t*>(ev_host + 8) = 1;
+            void* dptr = nullptr;
+            CU(cudaHostGetDevicePointer(&dptr, ev_host, 0));
+            epochs[dev] = (epochs[dev] + 1) & 0xffffffu;
+            S.stream = 1;
+            S.ev_cap = ev_cap;
+            S.ev_slot = ev_slot;
+            S.ev_epoch = epochs[dev];
+            S.ev_ring = static_cast<uint8_t*>(dptr) + 64;
+            S.ev_tail_host = static_cast<const unsigned long long*>(dptr);
+        }
 
         CU(cudaEventRecord(e0, st));
         if (grid) {
@@ -873,6 +1088,24 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
         }
         CU(cudaEventRecord(e1, st));
         out.launches += 1;
+        if (sio) { // the calling thread runs the callback while the kernel searches on
+            struct Flag {
+                bool& f;
+                explicit Flag(bool& x) : f(x) { f = true; }
+                ~Flag() { f = false; }
+            } busy(g_dev[dev].streaming);
+            int32_t* dev_stop = &reinterpret_cast<WorkState*>(base + a_ws)->hot.stop;
+            try {
+                drain_stream(ev_host + 64, ev_cap, ev_slot, reinterpret_cast<volatile unsigned long long*>(ev_host),
+                             S.ev_epoch, KW, n, parallel, e1, dev_stop, reinterpret_cast<const int32_t*>(ev_host + 8),
+                             g_dev[dev].side, *sio);
+            } catch (...) { // stop the device before unwinding (the callback or the ordering threw)
+                cudaMemcpyAsync(dev_stop, ev_host + 8, sizeof(int32_t), cudaMemcpyHostToDevice, g_dev[dev].side);
+                cudaStreamSynchronize(g_dev[dev].side);
+                cudaStreamSynchronize(st);
+                throw;
+            }
+        }
         CU(cudaMemcpyAsync(&out.ws, base + a_ws, sizeof(WorkState), cudaMemcpyDeviceToHost, st));
         CU(cudaStreamSynchronize(st));
         out.d2h += sizeof(WorkState);
@@ -997,6 +1230,11 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
             out.d2h += sizeof(uint16_t) * n;
         }
         CU(cudaStreamSynchronize(st));
+    }
+    if (sio && sio->stopped) { // the reference's stats where its callback stopped (search.cpp:147-149)
+        for (int i = 0; i < 3; ++i) out.ws.stats[i] = sio->stop_stats[i];
+        out.ws.stats[3] = sio->delivered;
+        out.ws.user_stop = 1;
     }
     if (std::getenv("CUBICS_DEBUG")) {
         const WorkState& w = out.ws;
@@ -1173,7 +1411,31 @@ extern "C" int cubics_solve_satisfy(const cubics_model* h, const cubics_search_c
         const HostModel& m = h->m;
         const int n = m.n_vars();
         std::vector<int64_t> vals(n);
-        return satisfy_records(m, *cfg, cb && !cfg->count_only, out, [&](uint64_t, const uint16_t* row) {
+        const bool want = cb && !cfg->count_only;
+        const int engine = want ? pick_engine(*cfg, m.goal != CUBICS_SATISFY) : CUBICS_ENGINE_PARITY;
+        // streamed unless it is the exact parallel first solution (one row) or a parallel
+        // branch-and-bound stream (reference-order incumbents need the parity engine)
+        const bool par = engine == CUBICS_ENGINE_PARALLEL;
+        if (want && !(par && (cfg->max_solutions == 1 || m.goal != CUBICS_SATISFY))) {
+            const double t0 = now_ms();
+            std::memset(out, 0, sizeof *out);
+            int64_t last_obj = 0;
+            StreamIO io;
+            io.visit = [&](const uint16_t* row, const uint64_t*) {
+                for (int v = 0; v < n; ++v) vals[v] = m.offset[v] + row[v];
+                if (m.goal != CUBICS_SATISFY) last_obj = vals[m.goal_var];
+                return cb(user, vals.data(), n) != 0;
+            };
+            RunOut r;
+            run_search(m, *cfg, engine, false, 0, r, false, nullptr, nullptr, &io);
+            fill_result(r, out);
+            out->complete = !r.ws.limit_hit && !r.ws.user_stop;
+            out->has_solution = r.ws.stats[3] > 0;
+            if (m.goal != CUBICS_SATISFY && io.delivered) out->objective = last_obj;
+            out->total_ms = now_ms() - t0;
+            return (int)CUBICS_OK;
+        }
+        return satisfy_records(m, *cfg, want, out, [&](uint64_t, const uint16_t* row) {
             for (int v = 0; v < n; ++v) vals[v] = m.offset[v] + row[v];
             return cb(user, vals.data(), n) != 0;
         });

@@ -110,6 +110,75 @@ static __device__ __noinline__ void pull_global_bound(WorkState* ws, const unsig
     if (!*reinterpret_cast<volatile int32_t*>(&ws->hot.has_bound)) atomicExch(&ws->hot.has_bound, 1);
 }
 
+// Streaming delivery (cubics_solve_satisfy with a callback; emit_solution, search.cpp:134-156):
+// the kernel writes events into a ring in host-mapped pinned memory while the calling thread
+// drains it and runs the callback. Slot t: u64 seq = epoch<<40 | t+1 (written last, after a
+// system fence; the per-call epoch keeps a reused ring's old slots from reading as new) |
+// u32 kind | u32 segment | u64 stats[3] | u32 key[KW] | u16 vals[n].
+//   EV_SOL  a solution: its segment and the segment-local nodes/failures/rounds at emission
+//           (parity engine: segment 0 = the whole search, so the stats are the reference's)
+//   EV_NEW  a subtree handed out (parallel): its segment id and root path key, published by the
+//           donor BEFORE the subtree enters the ticket ring, so the host knows every segment left
+//           of a finished one before that one's EV_END
+//   EV_END  a segment finished: its totals
+// Segments are contiguous intervals of the DFS order (a donor only hands out branches right of
+// everything it still visits), so the host releases solutions in DFS order segment by segment
+// and the reference's stats at any solution are the finished segments left of it plus its
+// snapshot: a callback that stops gets exactly the stats of search.cpp:147-149.
+__device__ __forceinline__ uint8_t* ev_slot_ptr(const SearchParams& P, long long t) {
+    return P.ev_ring + (size_t)((unsigned long long)t % P.ev_cap) * P.ev_slot;
+}
+
+// thread 0: reserve the next slot, waiting while the ring is full; -1 once the search is stopped
+// (the host no longer drains then). The host's consumed count is read over PCIe only when the
+// cached copy says the ring is full.
+static __device__ __noinline__ long long ev_reserve(const SearchParams& P) {
+    WorkState* ws = P.ws;
+    const unsigned long long t = atomicAdd((unsigned long long*)&ws->ev_head, 1ull);
+    int ns = 64;
+    for (;;) {
+        unsigned long long tail = ld_volatile_u64((const unsigned long long*)&ws->ev_tail);
+        if (t - tail < P.ev_cap) return (long long)t;
+        tail = *reinterpret_cast<const volatile unsigned long long*>(P.ev_tail_host);
+        atomicMax((unsigned long long*)&ws->ev_tail, tail);
+        if (t - tail < P.ev_cap) return (long long)t;
+        if (ld_volatile(&ws->hot.stop)) return -1;
+        __nanosleep(ns);
+        ns = ns < 8192 ? ns * 2 : ns;
+    }
+}
+
+// thread 0: header, stats, system fence, then the sequence word that hands the slot to the host
+// (the writers of the key / values fenced before the barrier that precedes this call)
+static __device__ __noinline__ void ev_commit(const SearchParams& P, long long t, uint32_t kind, uint32_t seg,
+                                              unsigned long long a, unsigned long long b, unsigned long long c) {
+    uint8_t* s = ev_slot_ptr(P, t);
+    volatile uint32_t* h = reinterpret_cast<volatile uint32_t*>(s + 8);
+    h[0] = kind;
+    h[1] = seg;
+    volatile unsigned long long* st = reinterpret_cast<volatile unsigned long long*>(s + 16);
+    st[0] = a;
+    st[1] = b;
+    st[2] = c;
+    __threadfence_system();
+    *reinterpret_cast<volatile unsigned long long*>(s) = ((unsigned long long)P.ev_epoch << 40) | ((unsigned long long)t + 1ull);
+}
+
+// thread 0 of a donor: EV_NEW for the subtree about to be published (key from its outbox)
+static __device__ __noinline__ void ev_new_segment(const SearchParams& P, uint32_t seg, const uint32_t* key) {
+    const long long t = ev_reserve(P);
+    if (t < 0) return;
+    uint32_t* k = reinterpret_cast<uint32_t*>(ev_slot_ptr(P, t) + kEvHeader);
+    for (int i = 0; i < P.KW; ++i) k[i] = key[i];
+    ev_commit(P, t, EV_NEW, seg, 0, 0, 0);
+}
+
+static __device__ __noinline__ void ev_end_segment(const SearchParams& P, uint32_t seg, unsigned long long a,
+                                                   unsigned long long b, unsigned long long c) {
+    const long long t = ev_reserve(P);
+    if (t >= 0) ev_commit(P, t, EV_END, seg, a, b, c);
+}
+
 // DFS path key: decision at depth d is bit (31 - d%32) of word d/32, so comparing the words as
 // unsigned integers, most significant first, is the reference's DFS (preorder) order.
 // path_right_word: word i of the key of the right child taken at depth d (prefix [0,d) kept,
@@ -220,6 +289,9 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
     const long long t_start = clock64();
     // first mode: current segment and the counters at its start; thread 0 caches the best key
     const bool first_mode = (F & F_FIRST) != 0 && (F & F_PARITY) == 0 && P.first_mode != 0; // compile-time off in lean kernels
+    // streaming delivery: compiled into the reference-order kernels and the parallel kernels
+    // with segment bookkeeping (F_FIRST); the lean parallel kernels never stream
+    const bool stream = (F & (F_FIRST | F_PARITY)) != 0 && P.stream != 0;
     long long seg = (!parallel || ctx == 0) && !P.n_seed ? 0 : -1;
     unsigned long long seg_n0 = 0, seg_f0 = 0, seg_r0 = 0;
     int gbest_idx = -1;
@@ -228,6 +300,10 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
             P.seg_stats[seg * 3 + 0] = nodes - seg_n0;
             P.seg_stats[seg * 3 + 1] = failures - seg_f0;
             P.seg_stats[seg * 3 + 2] = rounds - seg_r0;
+        }
+        if (stream && tid == 0 && seg >= 0) {
+            ev_end_segment(P, (uint32_t)seg, nodes - seg_n0, failures - seg_f0, rounds - seg_r0);
+            seg = -1; // once per segment (thread 0 is the only reader of seg in stream mode)
         }
     };
     // first mode: is the current path key right of the best solution key (thread 0 only)?
@@ -372,6 +448,16 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
             }
             break;
         }
+        if (stream && !parallel && (nodes & 1023) == 0) { // has a callback stopped the stream?
+            if (tid == 0) s_flag = ld_volatile(&ws->hot.stop);
+            sc.sync();
+            const int stp = s_flag;
+            sc.sync();
+            if (stp) {
+                if (tid == 0) ws->user_stop = 1;
+                break;
+            }
+        }
         if (parallel && tid == 0) { // prefetch; consumed after the fixpoint
             if constexpr (SC::kWarp)
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(&C.hot)),
@@ -445,7 +531,9 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
             if (sel < 0) {
                 // ============ solution leaf (emit_solution, search.cpp:134-156)
                 if (tid == 0) {
-                    if (first_mode) // only a solution left of the best known one can matter
+                    if (stream) // an event slot in the host-mapped ring
+                        s_ll = ev_reserve(P);
+                    else if (first_mode) // only a solution left of the best known one can matter
                         s_ll = right_of_best() ? -1 : (long long)atomicAdd((unsigned long long*)&ws->sol_count, 1ull);
                     else
                         s_ll = parallel ? (long long)atomicAdd((unsigned long long*)&ws->sol_count, 1ull) : (long long)sols;
@@ -455,7 +543,18 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
                 const long long sidx = s_ll;
                 const unsigned long long idx = (unsigned long long)sidx;
                 ++sols;
-                if (P.record && sidx >= 0 && idx < P.sol_cap) {
+                if (stream && sidx >= 0) {
+                    uint8_t* es = ev_slot_ptr(P, sidx);
+                    uint32_t* ek = reinterpret_cast<uint32_t*>(es + kEvHeader);
+                    uint16_t* ev = reinterpret_cast<uint16_t*>(es + kEvHeader + 4 * KW);
+                    for (int v = tid; v < n; v += T) ev[v] = (uint16_t)dom_first<W>(dom + (size_t)v * W);
+                    for (int i = tid; i < KW; i += T) ek[i] = path[i];
+                    __threadfence_system();
+                    sc.sync();
+                    if (tid == 0)
+                        ev_commit(P, sidx, EV_SOL, (uint32_t)(seg < 0 ? 0 : seg), nodes - seg_n0, failures - seg_f0,
+                                  rounds - seg_r0);
+                } else if (P.record && sidx >= 0 && idx < P.sol_cap) {
                     for (int v = tid; v < n; v += T) P.sol_vals[idx * n + v] = (uint16_t)dom_first<W>(dom + (size_t)v * W);
                     for (int i = tid; i < KW; i += T) P.sol_keys[idx * KW + i] = path[i];
                     if (tid == 0 && (!parallel || first_mode)) { // parity: global; first mode: segment-local
@@ -538,8 +637,9 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
                         g_has_bound = 1;
                     }
                 }
+                if (stream && !parallel && tid == 0) s_flag = ld_volatile(&ws->hot.stop);
                 sc.sync();
-                if (!parallel && sols >= P.max_solutions) {
+                if (!parallel && (sols >= P.max_solutions || (stream && s_flag))) {
                     if (tid == 0) {
                         ws->user_stop = 1;
                         ws->hot.stop = 1;
@@ -605,6 +705,7 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
                         P.outbox_busy[ctx] = 1;
                         atomicAdd(&ws->outstanding, 1);
                         const uint32_t s = atomicAdd(&ws->hot.push_ticket, 1u);
+                        if (stream) ev_new_segment(P, s + 1u, ob + NWP); // known to the host first
                         __threadfence();
                         st_volatile_u64(P.ring + (s % P.ring_cap), ((unsigned long long)(s + 1u) << 32) | (unsigned)ctx);
                         ++donations;

@@ -2,7 +2,7 @@
 
 usage: python scripts/ncu_traffic.py REPORT.ncu-rep INSTANCE [OUT.json]
 Writes {INSTANCE: {"dram_read_bytes", "dram_write_bytes", "kernel", "report"}} into
-profiles/r01_ncu_traffic.json (bench.py reads it for roofline.traffic).
+profiles/r02_ncu_traffic.json (bench.py reads it for roofline.traffic).
 """
 import csv
 import io
@@ -17,7 +17,7 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1
 def main():
     rep, inst = sys.argv[1], sys.argv[2]
     out = sys.argv[3] if len(sys.argv) > 3 else os.path.join(os.path.dirname(__file__), "..", "profiles",
-                                                              "r01_ncu_traffic.json")
+                                                              "r02_ncu_traffic.json")
     txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics",
                           "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum"],
                          capture_output=True, text=True).stdout
