@@ -266,6 +266,28 @@ int cubics_solve_optimize_shard(const cubics_model* m, const cubics_search_confi
                                 int32_t shard_index, int32_t shard_count, cubics_task_queue* queue,
                                 int64_t* best_values, cubics_result* out);
 
+/* Multi-GPU exact first solution (fd::solve_satisfy with max_solutions == 1, search.cpp:174-186,
+ * sharded). Each rank runs cubics_solve_first_shard: the same deterministic frontier (with its
+ * DFS segments recorded), then its subtrees (t % shard_count == shard_index, or claimed through
+ * queue when non-NULL) by the parallel engine's exact-first search. Then:
+ *   1. cubics_first_shard_best: this rank's DFS-first solution key (key_words u32 words,
+ *      lexicographic = reference DFS order) and values; the caller takes the minimum key K* over
+ *      ranks (distributed.solve_distributed: one all-gather);
+ *   2. cubics_first_shard_prefix(K*): this rank's share of the reference's stats up to K*; the
+ *      shares sum (one all-reduce) to exactly the reference's nodes / failures / rounds, and
+ *      solutions == 1. key == NULL (no rank found one): the complete search's share.
+ * out receives this rank's raw work. */
+typedef struct cubics_first_shard cubics_first_shard; /* opaque */
+int cubics_solve_first_shard(const cubics_model* m, const cubics_search_config* cfg,
+                             int32_t shard_index, int32_t shard_count, cubics_task_queue* queue,
+                             cubics_first_shard** out_shard, cubics_result* out);
+/* *key_words: in = capacity of key (words), out = the key's length; *has = 0 when none */
+int cubics_first_shard_best(const cubics_first_shard* s, uint32_t* key, int32_t* key_words,
+                            int64_t* values, int32_t* has);
+int cubics_first_shard_prefix(const cubics_first_shard* s, const uint32_t* key, int32_t key_words,
+                              cubics_stats* out);
+void cubics_first_shard_free(cubics_first_shard* s);
+
 /* ---- propagation (kernel-level API) ------------------------------------------------------ */
 typedef struct cubics_fixpoint_result { /* fd::FixpointResult (propagation.hpp:106-110) */
     int32_t failed;

@@ -115,7 +115,8 @@ EXPORTED = [
     "cubics_solve_satisfy", "cubics_enumerate", "cubics_solutions_free", "cubics_solve_optimize",
     "cubics_solve_optimize_batch", "cubics_solve_shard", "cubics_solve_shard_shared", "cubics_solve_optimize_shard",
     "cubics_task_queue_create", "cubics_task_queue_open", "cubics_task_queue_reset", "cubics_task_queue_claims",
-    "cubics_task_queue_destroy", "cubics_propagate",
+    "cubics_task_queue_destroy", "cubics_solve_first_shard", "cubics_first_shard_best", "cubics_first_shard_prefix",
+    "cubics_first_shard_free", "cubics_propagate",
     "cubics_removals", "cubics_last_error", "cubics_build_info", "cubics_device_count", "cubics_warmup",
 ]
 
@@ -167,6 +168,15 @@ def declare(lib):
     lib.cubics_task_queue_claims.restype = C.c_int
     lib.cubics_task_queue_destroy.argtypes = [C.c_void_p]
     lib.cubics_task_queue_destroy.restype = C.c_int
+    lib.cubics_solve_first_shard.argtypes = [C.c_void_p, P(SearchConfig), C.c_int32, C.c_int32, C.c_void_p,
+                                             P(C.c_void_p), P(Result)]
+    lib.cubics_solve_first_shard.restype = C.c_int
+    lib.cubics_first_shard_best.argtypes = [C.c_void_p, P(C.c_uint32), P(C.c_int32), P(C.c_int64), P(C.c_int32)]
+    lib.cubics_first_shard_best.restype = C.c_int
+    lib.cubics_first_shard_prefix.argtypes = [C.c_void_p, P(C.c_uint32), C.c_int32, P(Stats)]
+    lib.cubics_first_shard_prefix.restype = C.c_int
+    lib.cubics_first_shard_free.argtypes = [C.c_void_p]
+    lib.cubics_first_shard_free.restype = None
     lib.cubics_propagate.argtypes = [C.c_void_p, P(C.c_uint64), C.c_int32, C.c_int32, P(FixpointResult)]
     lib.cubics_propagate.restype = C.c_int
     lib.cubics_removals.argtypes = [C.c_void_p, P(C.c_uint64), C.c_int32, P(C.c_int32), C.c_int32, P(C.c_uint64)]

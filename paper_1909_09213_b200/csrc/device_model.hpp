@@ -183,7 +183,9 @@ struct SearchParams {
     uint64_t* batch_stats;     // [batch][4] nodes, failures, rounds, solutions
     int32_t* batch_flags;      // [batch] bit0 limit hit, bit1 has incumbent
     uint16_t* batch_inc;       // [batch][n] last incumbent (bit indices)
-    int32_t first_mode;
+    int32_t first_mode;    // 1: exact first solution (segments + abandoning); 2: segments only
+    int32_t seg_base;      // segment id of ring ticket t = t + 1 + seg_base (claimed seed i: 1 + i)
+    uint64_t* task_snap;   // frontier expansion with segments: [task_cap][4] segment, nodes, failures, rounds
     int64_t seg_cap;
     uint32_t* seg_key;     // [seg_cap][KW]
     uint64_t* seg_stats;   // [seg_cap][3]
@@ -193,6 +195,10 @@ struct SearchParams {
     // the queue owner's HBM (CUDA IPC, system-scope atomics over NVLink), order-preserving u64
     // encoding (see bound_enc); all ones = none. Null: single GPU.
     unsigned long long* g_inc;
+    // sharded exact first solution (cubics_solve_first_shard with a queue): the first 64 path-key
+    // bits of the best solution any rank found, system-scope atomicMin; a subtree whose key prefix
+    // is above it lies right of that solution and is abandoned on every GPU. Null: not shared.
+    unsigned long long* g_first;
     // streaming delivery (cubics_solve_satisfy with a callback): solutions, and in the parallel
     // engine the segment events that put them back into DFS order, go into a ring in host-mapped
     // pinned memory that the calling thread drains while the kernel runs (see search.cuh EvKind).

@@ -564,6 +564,7 @@ struct Records { // solutions copied back from the device
     }
     std::vector<uint32_t> keys;
     std::vector<uint64_t> stats;
+    std::vector<int32_t> seg; // segment bookkeeping: each solution's segment (stats: segment-local)
 };
 
 struct RunOut {
@@ -590,6 +591,16 @@ struct ShardIO {
     const std::vector<int32_t>* seeds = nullptr; // seeded run: task indices of this shard
     unsigned int* claim = nullptr; // shared queue: seeds are claimed through this counter instead
     unsigned long long* g_inc = nullptr; // multi-GPU B&B: shared incumbent (queue state, IPC-mapped)
+    unsigned long long* g_first = nullptr; // sharded first solution: best key prefix of all ranks
+    // sharded first solution: 1 = seeded run with the exact-first bookkeeping (segments,
+    // abandoning right of this rank's best); 2 = frontier expansion with segments only
+    int first = 0;
+    // out (first != 0): segments [n_seg] (root keys, stats), solutions' segments / snapshots in
+    // RunOut::rec, frontier tasks' [n_tasks][4] (segment, nodes, failures, rounds) in emission order
+    uint64_t n_seg = 0;
+    std::vector<uint32_t> seg_key;
+    std::vector<uint64_t> seg_st;
+    std::vector<uint64_t> task_snap;
 };
 
 // Batched B&B (cubics_solve_optimize_batch): problem i = block i, reference node order.
@@ -821,13 +832,16 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
         record = true;
         sol_cap = 65536;
     }
+    const int seg_mode = first_mode ? 1 : (shard ? shard->first : 0);
     const int KW = keyed ? static_cast<int>((P.depth_bound + 1 + 31) / 32) : 0;
     const int n_seed = (shard && shard->seeds) ? static_cast<int>(shard->seeds->size()) : 0;
     if (parallel && KW > 4096) throw StatusError{CUBICS_E_UNSUPPORTED, "search tree too deep for ordered parallel keys"};
     out.KW = KW;
     // launch geometry
     // small models run warp contexts (warp_ctx.cuh): K contexts per block of 32K threads
-    const bool use_warp = P.warp_ok && !grid && !batch && cfg.block_threads <= 0 &&
+    // (sharded first-solution runs need the frontier split with segment bookkeeping, which the
+    // lean warp kernels compile out: they run block contexts)
+    const bool use_warp = P.warp_ok && !grid && !batch && cfg.block_threads <= 0 && !(shard && shard->first) &&
                           (parallel || engine == CUBICS_ENGINE_PARITY) && !std::getenv("CUBICS_NO_WARP");
     const int warp_k = use_warp && parallel ? std::max(1, std::min(2, std::getenv("CUBICS_WARP_K") ? std::atoi(std::getenv("CUBICS_WARP_K")) : 1)) : 1;
     int block = cfg.block_threads > 0 ? ((cfg.block_threads + 31) / 32) * 32 : 0;
@@ -861,7 +875,7 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
     // F_FIRST (8): segment bookkeeping, also what streaming needs (a reference-order search
     // wider than 512 threads runs the generic kernel, whose lean instantiations do not stream)
     const int feat = (P.nl ? 1 : 0) | (P.ntb + P.ntn ? 2 : 0) | (P.big_words ? 4 : 0) |
-                     (first_mode || sio ? 8 : 0) |
+                     (seg_mode || sio ? 8 : 0) |
                      (P.lin_g > 1 ? dev::F_LONG : 0) |
                      (hm.goal == CUBICS_SATISFY && !shard ? dev::F_NOOPT | dev::F_NOSPLIT : 0);
     int n_ctx = batch ? batch->count : 1;
@@ -923,15 +937,18 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
     const size_t a_seedidx = take(sizeof(int32_t) * n_seed);
     const size_t a_svals = take(sizeof(uint16_t) * n * sol_cap);
     const size_t a_skeys = take(sizeof(uint32_t) * KW * sol_cap);
-    const size_t a_sstats = take(parallel && !first_mode ? 0 : sizeof(uint64_t) * 3 * sol_cap);
+    const size_t a_sstats = take(parallel && !seg_mode ? 0 : sizeof(uint64_t) * 3 * sol_cap);
     const size_t a_fkey = take(sizeof(uint32_t) * KW * n_ctx);
     const size_t a_fval = take(parallel ? sizeof(uint16_t) * n * n_ctx : 0);
     const size_t a_inc = take(sizeof(uint16_t) * std::max(n, 1));
     // one segment per handed-out subtree; sized by memory (<= 1 GiB), parity fallback beyond
-    const int64_t seg_cap = first_mode ? std::min<int64_t>((int64_t)1 << 21, ((int64_t)1 << 30) / (4 * KW + 24)) : 0;
+    const int64_t seg_cap = seg_mode ? std::max<int64_t>(n_seed + 1 + 2 * (int64_t)n_ctx,
+                                                         std::min<int64_t>((int64_t)1 << 21, ((int64_t)1 << 30) / (4 * KW + 24)))
+                                     : 0;
+    const size_t a_tsnap = take(seg_mode && shard && shard->split_depth > 0 ? sizeof(uint64_t) * 4 * shard->task_cap : 0);
     const size_t a_segk = take(sizeof(uint32_t) * KW * seg_cap);
     const size_t a_segs = take(sizeof(uint64_t) * 3 * seg_cap);
-    const size_t a_sseg = take(first_mode ? sizeof(int32_t) * sol_cap : 0);
+    const size_t a_sseg = take(seg_mode ? sizeof(int32_t) * sol_cap : 0);
     const int nb = batch ? batch->count : 0;
     const size_t a_bdom = take(sizeof(uint32_t) * NWP * nb);
     const size_t a_bbound = take(sizeof(int64_t) * nb);
@@ -949,7 +966,7 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
         WorkState w0{};
         const bool shared_q = shard && shard->claim;
         w0.outstanding = n_ctx + (shared_q ? 0 : n_seed);
-        w0.hot.has_bound = first_mode ? -1 : (cfg.has_initial_bound ? 1 : 0);
+        w0.hot.has_bound = seg_mode == 1 ? -1 : (cfg.has_initial_bound ? 1 : 0);
         // no initial bound: the worst value, so merging other GPUs' bounds is a plain atomic min/max
         w0.bound = cfg.has_initial_bound ? cfg.initial_bound
                                          : (hm.goal == CUBICS_MAXIMIZE ? std::numeric_limits<int64_t>::min()
@@ -963,7 +980,7 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
         CU(cudaMemcpyAsync(base, stage, stage_bytes, cudaMemcpyHostToDevice, st));
         out.h2d += stage_bytes;
         CU(cudaMemsetAsync(base + a_queue, 0, zero_end - a_queue, st));
-        if (first_mode) {
+        if (seg_mode) {
             CU(cudaMemsetAsync(base + a_segk, 0, sizeof(uint32_t) * KW * seg_cap, st));
             CU(cudaMemsetAsync(base + a_segs, 0, sizeof(uint64_t) * 3 * seg_cap, st));
         }
@@ -1041,7 +1058,10 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
         S.n_seed = n_seed;
         S.task_claim = shard ? shard->claim : nullptr;
         S.g_inc = shard ? shard->g_inc : nullptr;
-        S.first_mode = first_mode ? 1 : 0;
+        S.g_first = shard ? shard->g_first : nullptr;
+        S.first_mode = seg_mode;
+        S.seg_base = shard && shard->claim ? n_seed : 0;
+        S.task_snap = reinterpret_cast<uint64_t*>(base + a_tsnap);
         S.seg_cap = seg_cap;
         S.seg_key = reinterpret_cast<uint32_t*>(base + a_segk);
         S.seg_stats = reinterpret_cast<uint64_t*>(base + a_segs);
@@ -1182,7 +1202,12 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
                                    cudaMemcpyDeviceToHost, st));
                 out.d2h += sizeof(uint32_t) * KW * recorded;
             }
-            if (!parallel) {
+            if (seg_mode) {
+                out.rec.seg.resize(recorded);
+                CU(cudaMemcpyAsync(out.rec.seg.data(), base + a_sseg, sizeof(int32_t) * recorded, cudaMemcpyDeviceToHost, st));
+                out.d2h += sizeof(int32_t) * recorded;
+            }
+            if (!parallel || seg_mode) {
                 out.rec.stats.resize(recorded * 3);
                 CU(cudaMemcpyAsync(out.rec.stats.data(), base + a_sstats, sizeof(uint64_t) * 3 * recorded,
                                    cudaMemcpyDeviceToHost, st));
@@ -1224,6 +1249,22 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
             out.d2h += (sizeof(uint64_t) * 4 + sizeof(int32_t) + sizeof(uint16_t) * n) * nb;
         }
         if (shard) shard->n_tasks = (uint64_t)out.ws.n_tasks;
+        if (shard && seg_mode) { // segments and the frontier tasks' positions, for the host's prefix sums
+            const uint64_t nseg = (uint64_t)out.ws.hot.push_ticket + 1 + (uint64_t)S.seg_base;
+            if (nseg > (uint64_t)seg_cap) throw StatusError{CUBICS_E_CAPACITY, "segment bookkeeping capacity"};
+            shard->n_seg = nseg;
+            shard->seg_key.resize(nseg * KW);
+            shard->seg_st.resize(nseg * 3);
+            CU(cudaMemcpyAsync(shard->seg_key.data(), base + a_segk, sizeof(uint32_t) * KW * nseg, cudaMemcpyDeviceToHost, st));
+            CU(cudaMemcpyAsync(shard->seg_st.data(), base + a_segs, sizeof(uint64_t) * 3 * nseg, cudaMemcpyDeviceToHost, st));
+            out.d2h += (sizeof(uint32_t) * KW + sizeof(uint64_t) * 3) * nseg;
+            if (shard->split_depth > 0) {
+                const uint64_t nt = std::min<uint64_t>((uint64_t)out.ws.n_tasks, shard->task_cap);
+                shard->task_snap.resize(nt * 4);
+                CU(cudaMemcpyAsync(shard->task_snap.data(), base + a_tsnap, sizeof(uint64_t) * 4 * nt, cudaMemcpyDeviceToHost, st));
+                out.d2h += sizeof(uint64_t) * 4 * nt;
+            }
+        }
         if (parallel && hm.goal != CUBICS_SATISFY && n) {
             out.inc_vals.resize(n);
             CU(cudaMemcpyAsync(out.inc_vals.data(), base + a_inc, sizeof(uint16_t) * n, cudaMemcpyDeviceToHost, st));
@@ -1652,10 +1693,12 @@ namespace {
 // Shared queue state (256 bytes in the owner GPU's HBM, CUDA IPC-mapped by the other ranks):
 //   [0]  u32 claim counter              (next frontier subtree to claim)
 //   [8]  u64 shared incumbent, encoded   (bound_enc in search.cuh; all ones = none)
+//   [16] u64 first 64 key bits of the best first solution any rank found (all ones = none)
 struct QueueState {
     uint32_t claim;
     uint32_t pad;
     unsigned long long g_inc;
+    unsigned long long g_first;
 };
 
 // The search device must reach the queue owner's memory: peer access inside one process (CUDA
@@ -1874,6 +1917,241 @@ int solve_shard_impl(const cubics_model* h, const cubics_search_config* cfg, int
 }
 } // namespace
 
+// Sharded exact first solution (fd::solve_satisfy, max_solutions == 1, search.cpp:174-186, across
+// GPUs). The reference's stats are those of the DFS prefix up to its first solution K*. Every
+// part of the sharded search is a sequence of segments, contiguous intervals of the DFS order
+// with a root key and stats: the frontier expansion's (intervals of the tree cut at the split
+// depth; each task records where it sits in one of them) and each rank's seeded subtrees'
+// (claimed / pre-published seeds and the right branches donated inside them). So the prefix up to
+// K* is, summed over all ranks: the segments whose root key is below K*, except K*'s own, plus
+// the snapshot of K*'s own segment taken at K* - in the frontier tree (rank 0) with K*'s task
+// (or K* itself when it lies above the frontier) in place of K*.
+struct cubics_first_shard {
+    int KW = 0, n = 0;
+    bool rank0 = false;
+    std::vector<int64_t> offset;
+    uint64_t raw[4] = {0, 0, 0, 0}; // this rank's own work (its stats when there is no solution)
+    // frontier expansion (identical on every rank)
+    uint64_t nfseg = 0;
+    std::vector<uint32_t> fseg_key;
+    std::vector<uint64_t> fseg_st;
+    std::vector<uint32_t> task_key;  // [nt][KW] in emission order
+    std::vector<uint64_t> task_snap; // [nt][4] segment, nodes, failures, rounds
+    Records fsol;                    // solutions above the frontier (keys, segments, snapshots)
+    // this rank's seeded run
+    uint64_t nseg = 0;
+    std::vector<uint32_t> seg_key;
+    std::vector<uint64_t> seg_st;
+    Records sol;
+
+    bool less(const uint32_t* a, const uint32_t* b) const { return std::lexicographical_compare(a, a + KW, b, b + KW); }
+    bool equal(const uint32_t* a, const uint32_t* b) const { return std::equal(a, a + KW, b); }
+    // segments [0, count) with root key < K, except `skip`
+    static void sum_left(const cubics_first_shard& s, uint64_t count, const std::vector<uint32_t>& keys,
+                         const std::vector<uint64_t>& st, const uint32_t* K, int64_t skip, uint64_t* tot) {
+        for (uint64_t i = 0; i < count; ++i)
+            if ((int64_t)i != skip && s.less(&keys[i * s.KW], K))
+                for (int j = 0; j < 3; ++j) tot[j] += st[i * 3 + j];
+    }
+};
+
+namespace {
+int first_shard_impl(const cubics_model* h, const cubics_search_config* cfg, int32_t shard_index, int32_t shard_count,
+                     cubics_task_queue* queue, cubics_first_shard** res, cubics_result* out) {
+    if (!h || !cfg || !out || !res || shard_count < 1 || shard_index < 0 || shard_index >= shard_count)
+        return CUBICS_E_INVALID;
+    *res = nullptr;
+    return guarded([&]() -> int {
+        const double t0 = now_ms();
+        std::memset(out, 0, sizeof *out);
+        const HostModel& m = h->m;
+        if (m.goal != CUBICS_SATISFY)
+            throw StatusError{CUBICS_E_UNSUPPORTED, "sharded first solution needs a satisfy goal"};
+        cubics_search_config c = *cfg;
+        c.engine = CUBICS_ENGINE_PARALLEL;
+        c.max_solutions = 1;
+        pick_engine(c, false); // rejects node_limit
+        const int n = m.n_vars();
+        const int dev = current_device(c.device);
+        ensure_queue_access(dev, queue);
+        QueueState* qs = queue ? reinterpret_cast<QueueState*>(queue->counter) : nullptr;
+        std::unique_ptr<cubics_first_shard> fs(new cubics_first_shard);
+        fs->n = n;
+        fs->rank0 = shard_index == 0;
+        fs->offset = m.offset;
+        Prepared P;
+        prepare(m, m.words.data(), P);
+        const int KW = static_cast<int>((P.depth_bound + 1 + 31) / 32);
+        fs->KW = KW;
+        const size_t OS = P.NWP + dev::round4((size_t)KW + 2);
+        std::lock_guard<std::recursive_mutex> lock(g_dev_mu[dev]);
+        // 1. the deterministic frontier, with segment bookkeeping (no abandoning: the task set
+        //    must not depend on timing) and its solutions recorded
+        const uint64_t want = 256ull * (uint64_t)shard_count;
+        RunOut ex;
+        ShardIO io;
+        for (int depth = 8;; depth += 4) {
+            io = ShardIO{};
+            io.split_depth = depth;
+            io.first = 2;
+            io.task_cap = std::max<uint64_t>(4096, 8 * want);
+            for (;;) {
+                io.task_dev = reinterpret_cast<uint32_t*>(device_arena(dev, sizeof(uint32_t) * OS * io.task_cap, 1));
+                ex = RunOut{};
+                cubics_search_config all = c;
+                all.max_solutions = std::numeric_limits<uint64_t>::max();
+                run_search(m, c, CUBICS_ENGINE_PARALLEL, true, default_sol_cap(m, all), ex, true, &io);
+                if (ex.ws.sol_count > ex.rec.count)
+                    throw StatusError{CUBICS_E_CAPACITY, "frontier solution buffer overflow"};
+                if (io.n_tasks <= io.task_cap) break;
+                io.task_cap = io.n_tasks;
+            }
+            if (io.n_tasks >= want || io.n_tasks == 0 || depth >= 64 || (uint64_t)depth >= P.depth_bound) break;
+        }
+        const uint64_t nt = io.n_tasks;
+        fs->nfseg = io.n_seg;
+        fs->fseg_key = std::move(io.seg_key);
+        fs->fseg_st = std::move(io.seg_st);
+        fs->task_snap = std::move(io.task_snap);
+        fs->task_key.resize(nt * KW);
+        if (nt)
+            CU(cudaMemcpy2D(fs->task_key.data(), sizeof(uint32_t) * KW, io.task_dev + P.NWP, sizeof(uint32_t) * OS,
+                            sizeof(uint32_t) * KW, nt, cudaMemcpyDeviceToHost));
+        fs->fsol = std::move(ex.rec);
+        // 2. this rank's subtrees in DFS order (static: t = shard_index mod shard_count of the
+        //    DFS-ordered tasks; shared queue: all of them, claimed)
+        std::vector<int32_t> order(nt);
+        std::iota(order.begin(), order.end(), 0);
+        std::sort(order.begin(), order.end(), [&](int32_t x, int32_t y) {
+            return fs->less(&fs->task_key[(size_t)x * KW], &fs->task_key[(size_t)y * KW]);
+        });
+        std::vector<int32_t> mine;
+        if (qs)
+            mine = order;
+        else
+            for (uint64_t r = shard_index; r < nt; r += shard_count) mine.push_back(order[r]);
+        // 3. the exact-first parallel search of those subtrees (abandoning right of this rank's best)
+        RunOut run;
+        if (!mine.empty()) {
+            ShardIO seeded;
+            seeded.task_dev = io.task_dev;
+            seeded.seeds = &mine;
+            seeded.claim = qs ? &qs->claim : nullptr;
+            seeded.g_first = qs ? &qs->g_first : nullptr;
+            seeded.first = 1;
+            run_search(m, c, CUBICS_ENGINE_PARALLEL, true, 65536, run, true, &seeded);
+            if (run.ws.sol_count > run.rec.count)
+                throw StatusError{CUBICS_E_CAPACITY, "first-solution bookkeeping capacity"};
+            fs->nseg = seeded.n_seg;
+            fs->seg_key = std::move(seeded.seg_key);
+            fs->seg_st = std::move(seeded.seg_st);
+            fs->sol = std::move(run.rec);
+        }
+        fill_result(run, out);
+        for (int i = 0; i < 4; ++i) fs->raw[i] = run.ws.stats[i] + (fs->rank0 ? ex.ws.stats[i] : 0);
+        out->stats.nodes = fs->raw[0];
+        out->stats.failures = fs->raw[1];
+        out->stats.rounds = fs->raw[2];
+        out->stats.solutions = fs->raw[3];
+        out->device_ms = run.device_ms + ex.device_ms;
+        out->h2d_bytes += ex.h2d;
+        out->d2h_bytes += ex.d2h + sizeof(uint32_t) * KW * nt;
+        out->kernel_launches += ex.launches;
+        out->has_solution = fs->sol.count + fs->fsol.count > 0;
+        out->complete = 0;
+        out->total_ms = now_ms() - t0;
+        *res = fs.release();
+        return CUBICS_OK;
+    });
+}
+} // namespace
+
+extern "C" int cubics_solve_first_shard(const cubics_model* h, const cubics_search_config* cfg, int32_t shard_index,
+                                        int32_t shard_count, cubics_task_queue* queue, cubics_first_shard** res,
+                                        cubics_result* out) {
+    return first_shard_impl(h, cfg, shard_index, shard_count, queue, res, out);
+}
+
+extern "C" int cubics_first_shard_best(const cubics_first_shard* s, uint32_t* key, int32_t* key_words, int64_t* values,
+                                       int32_t* has) {
+    if (!s || !key_words || !has) return CUBICS_E_INVALID;
+    const uint32_t* best = nullptr;
+    const uint16_t* row = nullptr;
+    for (const Records* r : {&s->fsol, &s->sol})
+        for (uint64_t i = 0; i < r->count; ++i)
+            if (!best || s->less(&r->keys[i * s->KW], best)) {
+                best = &r->keys[i * s->KW];
+                row = r->rows() + i * s->n;
+            }
+    *has = best != nullptr;
+    const int32_t cap = *key_words;
+    *key_words = s->KW;
+    if (!best) return CUBICS_OK;
+    if (key) {
+        if (cap < s->KW) return CUBICS_E_INVALID;
+        std::copy_n(best, s->KW, key);
+    }
+    if (values)
+        for (int v = 0; v < s->n; ++v) values[v] = s->offset[v] + row[v];
+    return CUBICS_OK;
+}
+
+extern "C" int cubics_first_shard_prefix(const cubics_first_shard* s, const uint32_t* key, int32_t key_words,
+                                         cubics_stats* out) {
+    if (!s || !out) return CUBICS_E_INVALID;
+    std::memset(out, 0, sizeof *out);
+    if (!key) { // no solution on any rank: the complete search, this rank's share
+        out->nodes = s->raw[0];
+        out->failures = s->raw[1];
+        out->rounds = s->raw[2];
+        return CUBICS_OK;
+    }
+    if (key_words != s->KW) return CUBICS_E_INVALID;
+    uint64_t tot[3] = {0, 0, 0};
+    auto find = [&](const Records& r) -> int64_t { // K*'s record in r, or -1
+        for (uint64_t i = 0; i < r.count; ++i)
+            if (s->equal(&r.keys[i * s->KW], key)) return (int64_t)i;
+        return -1;
+    };
+    auto take = [&](const Records& r, int64_t i) { // K*'s segment; its snapshot joins the sum
+        for (int j = 0; j < 3; ++j) tot[j] += r.stats[i * 3 + j];
+        return (int64_t)r.seg[i];
+    };
+    const int64_t fi = find(s->fsol); // K* above the frontier (every rank has those records)
+    int64_t sseg = -1;
+    if (fi < 0) {
+        const int64_t si = find(s->sol);
+        if (si >= 0) sseg = take(s->sol, si);
+    }
+    cubics_first_shard::sum_left(*s, s->nseg, s->seg_key, s->seg_st, key, sseg, tot);
+    if (s->rank0) { // the frontier tree: K* itself when above the frontier, else the task holding it
+        int64_t fseg = -1;
+        const uint32_t* at = key;
+        if (fi >= 0) {
+            fseg = take(s->fsol, fi);
+        } else {
+            const uint64_t nt = s->task_snap.size() / 4;
+            int64_t t = -1;
+            for (uint64_t i = 0; i < nt; ++i)
+                if (!s->less(key, &s->task_key[i * s->KW]) &&
+                    (t < 0 || s->less(&s->task_key[(size_t)t * s->KW], &s->task_key[i * s->KW])))
+                    t = (int64_t)i;
+            if (t < 0) return CUBICS_E_INVALID; // a key from no task of this search
+            fseg = (int64_t)s->task_snap[t * 4];
+            for (int j = 0; j < 3; ++j) tot[j] += s->task_snap[t * 4 + 1 + j];
+            at = &s->task_key[(size_t)t * s->KW];
+        }
+        cubics_first_shard::sum_left(*s, s->nfseg, s->fseg_key, s->fseg_st, at, fseg, tot);
+        out->solutions = 1;
+    }
+    out->nodes = tot[0];
+    out->failures = tot[1];
+    out->rounds = tot[2];
+    return CUBICS_OK;
+}
+
+extern "C" void cubics_first_shard_free(cubics_first_shard* s) { delete s; }
+
 extern "C" int cubics_solve_shard(const cubics_model* h, const cubics_search_config* cfg, int32_t shard_index,
                                   int32_t shard_count, cubics_keyed_solution_cb cb, void* user, cubics_result* out) {
     return solve_shard_impl(h, cfg, shard_index, shard_count, nullptr, cb, user, out, false, nullptr);
@@ -1905,6 +2183,7 @@ extern "C" int cubics_task_queue_create(int32_t device, cubics_task_queue** out,
         CU(cudaMemset(p, 0, 256));
         QueueState init{};
         init.g_inc = ~0ull; // no incumbent
+        init.g_first = ~0ull;
         CU(cudaMemcpy(p, &init, sizeof init, cudaMemcpyHostToDevice));
         if (handle) {
             cudaIpcMemHandle_t hd;
@@ -1942,6 +2221,7 @@ extern "C" int cubics_task_queue_reset(cubics_task_queue* q) {
         CU(cudaSetDevice(q->device));
         QueueState init{};
         init.g_inc = ~0ull; // no incumbent
+        init.g_first = ~0ull;
         CU(cudaMemset(q->counter, 0, 256));
         CU(cudaMemcpy(q->counter, &init, sizeof init, cudaMemcpyHostToDevice));
         CU(cudaDeviceSynchronize());

@@ -179,6 +179,10 @@ static __device__ __noinline__ void ev_end_segment(const SearchParams& P, uint32
     if (t >= 0) ev_commit(P, t, EV_END, seg, a, b, c);
 }
 
+__device__ __forceinline__ unsigned long long key_prefix64(uint32_t w0, uint32_t w1) {
+    return ((unsigned long long)w0 << 32) | w1;
+}
+
 // DFS path key: decision at depth d is bit (31 - d%32) of word d/32, so comparing the words as
 // unsigned integers, most significant first, is the reference's DFS (preorder) order.
 // path_right_word: word i of the key of the right child taken at depth d (prefix [0,d) kept,
@@ -288,7 +292,12 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
     long long idle_cyc = 0, steals = 0, donations = 0;
     const long long t_start = clock64();
     // first mode: current segment and the counters at its start; thread 0 caches the best key
-    const bool first_mode = (F & F_FIRST) != 0 && (F & F_PARITY) == 0 && P.first_mode != 0; // compile-time off in lean kernels
+    // segment bookkeeping (F_FIRST kernels, P.first_mode != 0): every subtree handed out records
+    // its root key and stats, solutions their segment-local snapshots. first_mode (== 1) also
+    // abandons subtrees right of the best solution found; 2 = bookkeeping only (the frontier
+    // expansion of a sharded first-solution search, whose task set must not depend on timing)
+    const bool seg_book = (F & F_FIRST) != 0 && (F & F_PARITY) == 0 && P.first_mode != 0; // compile-time off in lean kernels
+    const bool first_mode = seg_book && P.first_mode == 1;
     // streaming delivery: compiled into the reference-order kernels and the parallel kernels
     // with segment bookkeeping (F_FIRST); the lean parallel kernels never stream
     const bool stream = (F & (F_FIRST | F_PARITY)) != 0 && P.stream != 0;
@@ -296,7 +305,7 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
     unsigned long long seg_n0 = 0, seg_f0 = 0, seg_r0 = 0;
     int gbest_idx = -1;
     auto flush_seg = [&]() {
-        if (first_mode && tid == 0 && seg >= 0 && seg < P.seg_cap) {
+        if (seg_book && tid == 0 && seg >= 0 && seg < P.seg_cap) {
             P.seg_stats[seg * 3 + 0] = nodes - seg_n0;
             P.seg_stats[seg * 3 + 1] = failures - seg_f0;
             P.seg_stats[seg * 3 + 2] = rounds - seg_r0;
@@ -307,7 +316,9 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
         }
     };
     // first mode: is the current path key right of the best solution key (thread 0 only)?
+    // (sharded: or is its 64-bit prefix above the best any GPU found)
     auto right_of_best = [&]() -> bool {
+        if (P.g_first && key_prefix64(path[0], KW > 1 ? path[1] : 0u) > ld_relaxed_sys_u64(P.g_first)) return true;
         const int bi = (int)hot.w;
         if (bi < 0) return false;
         if (bi != gbest_idx) {
@@ -320,6 +331,9 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
     };
     // first mode: is the right branch taken at depth d (key: path prefix, bit d) right of the best?
     auto frame_right_of_best = [&](int d) -> bool {
+        if (P.g_first && key_prefix64(path_right_word(path[0], 0, d), KW > 1 ? path_right_word(path[1], 1, d) : 0u) >
+                             ld_relaxed_sys_u64(P.g_first))
+            return true;
         const int bi = (int)hot.w;
         if (bi < 0) return false;
         if (bi != gbest_idx) {
@@ -342,7 +356,7 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
             // shared queue first (claiming keeps this context outstanding), then the ring
             int got = claim_open ? claim_task(P.task_claim, P.n_seed, P.n_ctx) : -1;
             if (got >= 0) {
-                s_ll = -1;
+                s_ll = (long long)(got - P.n_ctx) + 1; // claimed seed i is segment 1 + i
             } else {
                 claim_open = false;
                 atomicSub(&ws->outstanding, 1);
@@ -360,7 +374,7 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
                     ns = ns < 1024 ? ns * 2 : ns;
                 }
                 if (got >= 0) __threadfence();
-                s_ll = (long long)t + 1; // segment id of the subtree published under ticket t
+                s_ll = (long long)t + 1 + P.seg_base; // segment id of the subtree published under ticket t
             }
             if (got >= 0) ++steals;
             idle_cyc += clock64() - t0;
@@ -389,9 +403,9 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
         sp = base = 0;
         first_all = false;
         trig_var = tvar;
+        if (seg_book && seg < P.seg_cap)
+            for (int i = tid; i < KW; i += T) P.seg_key[(size_t)seg * KW + i] = path[i];
         if (first_mode) {
-            if (seg < P.seg_cap)
-                for (int i = tid; i < KW; i += T) P.seg_key[(size_t)seg * KW + i] = path[i];
             if (tid == 0) {
                 hot = ld_volatile_v4(reinterpret_cast<const uint4*>(&ws->hot));
                 s_flag = right_of_best(); // the whole subtree lies right of a known solution
@@ -431,6 +445,13 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
                 if (tid == 0) {
                     tb[NWP + KW] = (uint32_t)depth;
                     tb[NWP + KW + 1] = (uint32_t)trig_var;
+                    if (seg_book) { // where the task sits in the frontier's DFS: segment + snapshot
+                        uint64_t* ts = P.task_snap + (size_t)t * 4;
+                        ts[0] = (unsigned long long)seg;
+                        ts[1] = nodes - seg_n0;
+                        ts[2] = failures - seg_f0;
+                        ts[3] = rounds - seg_r0;
+                    }
                 }
             }
             backtrack = true;
@@ -557,11 +578,11 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
                 } else if (P.record && sidx >= 0 && idx < P.sol_cap) {
                     for (int v = tid; v < n; v += T) P.sol_vals[idx * n + v] = (uint16_t)dom_first<W>(dom + (size_t)v * W);
                     for (int i = tid; i < KW; i += T) P.sol_keys[idx * KW + i] = path[i];
-                    if (tid == 0 && (!parallel || first_mode)) { // parity: global; first mode: segment-local
+                    if (tid == 0 && (!parallel || seg_book)) { // parity: global; segments: segment-local
                         P.sol_stats[idx * 3 + 0] = nodes - seg_n0;
                         P.sol_stats[idx * 3 + 1] = failures - seg_f0;
                         P.sol_stats[idx * 3 + 2] = rounds - seg_r0;
-                        if (first_mode) P.sol_seg[idx] = (int32_t)seg;
+                        if (seg_book) P.sol_seg[idx] = (int32_t)seg;
                     }
                 }
                 if (first_mode) {
@@ -581,6 +602,7 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
                         }
                         if (better) *gb = (int32_t)idx;
                         spin_unlock(&ws->best_lock);
+                        if (better && P.g_first) atomicMin_system(P.g_first, key_prefix64(path[0], KW > 1 ? path[1] : 0u));
                     }
                     // everything this context would visit next lies right of this solution
                     sp = base;
@@ -705,7 +727,7 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
                         P.outbox_busy[ctx] = 1;
                         atomicAdd(&ws->outstanding, 1);
                         const uint32_t s = atomicAdd(&ws->hot.push_ticket, 1u);
-                        if (stream) ev_new_segment(P, s + 1u, ob + NWP); // known to the host first
+                        if (stream) ev_new_segment(P, s + 1u + (uint32_t)P.seg_base, ob + NWP); // known to the host first
                         __threadfence();
                         st_volatile_u64(P.ring + (s % P.ring_cap), ((unsigned long long)(s + 1u) << 32) | (unsigned)ctx);
                         ++donations;

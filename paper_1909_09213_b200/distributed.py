@@ -65,12 +65,66 @@ def _optimize_shard(model, cfg, rank, world, queue=None):
     return S.solve_optimize_shard(model, cfg, rank, world, queue=queue)
 
 
+def _first_distributed(model, cfg, rank, world, shard_fn=None, device=None, queue=None):
+    """Exact first solution across ranks (cubics_solve_first_shard): one all-gather of the ranks'
+    DFS-first keys picks K* (the minimum), one all-reduce sums each rank's share of the
+    reference's prefix up to K* (nodes above the frontier, whole subtrees left of K*, and the
+    snapshot of K*'s own subtree segment)."""
+    import torch
+    import torch.distributed as dist
+
+    part, err = None, None
+    if queue is not None:
+        try:
+            if rank == 0:
+                queue.reset()
+        except Exception as e:  # noqa: BLE001 - re-raised after the collectives
+            err = e
+        dist.barrier()
+    if err is None:
+        try:
+            part = shard_fn(model, cfg, rank, world) if shard_fn else S.solve_first_shard(model, cfg, rank, world, queue)
+        except Exception as e:  # noqa: BLE001 - re-raised after the collectives
+            err = e
+    mine = None
+    if part is not None:
+        try:
+            mine = part.best()
+        except Exception as e:  # noqa: BLE001
+            err = e
+    allb = [None] * world
+    dist.all_gather_object(allb, (err is not None, mine))
+    if any(f for f, _ in allb):
+        if err is not None:
+            raise err
+        raise RuntimeError("solve_distributed: another rank's shard failed")
+    cands = [b for _, b in allb if b is not None]
+    key, vals = min(cands, key=lambda b: b[0]) if cands else (None, None)
+    dev = device if device is not None else "cpu"
+    stats, flag = [0, 0, 0, 0], 0
+    try:
+        stats = list(part.prefix(key).as_tuple())
+    except Exception as e:  # noqa: BLE001
+        err, flag = e, 1
+    t = torch.tensor(stats + [flag], dtype=torch.int64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    ms = torch.tensor([part.result.device_ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    if int(t[4].item()):
+        if err is not None:
+            raise err
+        raise RuntimeError("solve_distributed: another rank's prefix failed")
+    total = tuple(int(x) for x in t[:4].tolist())
+    return total, ([vals] if vals is not None else []), float(ms.item())
+
+
 def solve_distributed(model, cfg: S.SearchConfig, rank: int, world: int, collect: bool = True,
                       shard_fn=None, device=None, queue=None):
     """Run this rank's shard and combine over the default torch.distributed process group.
 
     Satisfy goals: returns (stats tuple, solutions in DFS order or None on ranks != 0, max device
-    ms over ranks). Minimize / maximize goals (branch and bound, cubics_solve_optimize_shard):
+    ms over ranks). max_solutions == 1: the exact first solution (cubics_solve_first_shard; the
+    stats are the reference's prefix up to it, and the list holds that one solution on every rank). Minimize / maximize goals (branch and bound, cubics_solve_optimize_shard):
     returns (stats tuple, best Solution over all ranks or None, max device ms); with a queue the
     GPUs share the incumbent while they search.
     shard_fn(model, cfg, rank, world, collect) -> (SatisfyResult, [(key, values)]) (satisfy) or
@@ -84,6 +138,8 @@ def solve_distributed(model, cfg: S.SearchConfig, rank: int, world: int, collect
     import torch.distributed as dist
 
     optimize = model.goal != 0
+    if not optimize and cfg.max_solutions == 1:
+        return _first_distributed(model, cfg, rank, world, shard_fn, device, queue)
     r, sols, err = None, [], None
     if queue is not None:
         try:

@@ -639,6 +639,78 @@ def solve_optimize_shard(model: Model, cfg: SearchConfig, shard_index: int, shar
     return OptimizeResult(sol, bool(res.complete), _stats(res), res.engine, res.contexts, res.device_ms, res.total_ms)
 
 
+class FirstShard:
+    """One rank's part of a multi-GPU exact first solution (cubics_solve_first_shard).
+
+    best() -> (key_words, values) of this rank's DFS-first solution, or None; the caller takes the
+    minimum key K* over ranks. prefix(K*) -> this rank's share of the reference's stats up to K*
+    (shares sum across ranks to the reference's (nodes, failures, rounds, 1)); prefix(None) when
+    no rank found a solution gives the complete search's share."""
+
+    def __init__(self, ptr, result: SatisfyResult, n_vars: int):
+        self.ptr = ptr
+        self.result = result
+        self.n_vars = n_vars
+
+    def best(self):
+        kw = C.c_int32(0)
+        has = C.c_int32(0)
+        _check(lib().cubics_first_shard_best(self.ptr, None, C.byref(kw), None, C.byref(has)), "first_shard_best")
+        if not has.value:
+            return None
+        key = (C.c_uint32 * max(1, kw.value))()
+        vals = (C.c_int64 * max(1, self.n_vars))()
+        _check(lib().cubics_first_shard_best(self.ptr, key, C.byref(kw), vals, C.byref(has)), "first_shard_best")
+        return [key[i] for i in range(kw.value)], [vals[i] for i in range(self.n_vars)]
+
+    def prefix(self, key) -> SearchStats:
+        st = A.Stats()
+        if key is None:
+            _check(lib().cubics_first_shard_prefix(self.ptr, None, 0, C.byref(st)), "first_shard_prefix")
+        else:
+            arr = (C.c_uint32 * len(key))(*key)
+            _check(lib().cubics_first_shard_prefix(self.ptr, arr, len(key), C.byref(st)), "first_shard_prefix")
+        return SearchStats(st.nodes, st.failures, st.rounds, st.solutions)
+
+    def close(self):
+        if self.ptr:
+            lib().cubics_first_shard_free(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 - interpreter teardown
+            pass
+
+
+def solve_first_shard(model: Model, cfg: SearchConfig, shard_index: int, shard_count: int,
+                      queue: TaskQueue | None = None) -> FirstShard:
+    """One rank's share of a multi-GPU exact first-solution search (cubics_solve_first_shard)."""
+    res = A.Result()
+    ptr = C.c_void_p()
+    c = cfg.to_c()
+    _check(lib().cubics_solve_first_shard(model.handle, C.byref(c), shard_index, shard_count,
+                                          queue.ptr if queue is not None else None, C.byref(ptr), C.byref(res)),
+           "solve_first_shard")
+    r = SatisfyResult(_stats(res), bool(res.complete), res.engine, res.contexts, res.device_ms, res.total_ms,
+                      res.h2d_bytes, res.d2h_bytes, res.kernel_launches)
+    return FirstShard(ptr.value, r, model.n_vars)
+
+
+def merge_first(shards):
+    """Sequential driver of the two-phase protocol over FirstShard parts held in one process:
+    (stats, values of the DFS-first solution or None) - what distributed.solve_distributed does
+    with one all-gather and one all-reduce."""
+    bests = [b for b in (s.best() for s in shards) if b is not None]
+    key, vals = min(bests, key=lambda b: b[0]) if bests else (None, None)
+    tot = [0, 0, 0, 0]
+    for s in shards:
+        p = s.prefix(key)
+        tot = [a + b for a, b in zip(tot, p.as_tuple())]
+    return SearchStats(*tot), vals
+
+
 # ------------------------------------------------------------------ propagation
 def propagate_fixpoint(model: Model, domains=None, alldiff=A.ARC_CONSISTENT, max_rounds=0):
     """fd::propagate_fixpoint over `domains` (default: the model's); returns (domains, FixpointResult)."""

@@ -137,3 +137,55 @@ def test_failing_rank_raises_on_every_rank_instead_of_hanging():
     out = _run_opt(2, fail_rank=1)
     assert out[1][0] == "raised" and out[1][1] == "CapacityError"
     assert out[0][0] == "raised" and "another rank" in out[0][2]
+
+
+def _worker_first(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    from paper_1909_09213_b200 import distributed as D
+    from paper_1909_09213_b200 import solver as S
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        m = S.parse_model(G.model_text("nq8"))
+
+        class FakePart:  # the two-phase protocol of cubics_solve_first_shard
+            def __init__(self, r):
+                self.r = r
+                self.result = S.SatisfyResult(S.SearchStats(), False, device_ms=float(r + 3))
+
+            def best(self):  # rank 1 holds the DFS-first key [5], rank 0 a later one [9]
+                return ([9], [0] * 8) if self.r == 0 else ([5], list(range(8)))
+
+            def prefix(self, key):
+                assert key == [5]  # every rank sees the global minimum
+                return S.SearchStats(10 * (self.r + 1), self.r, 100, 1 if self.r == 0 else 0)
+
+        stats, sols, ms = D.solve_distributed(m, S.SearchConfig(max_solutions=1), rank, world,
+                                              shard_fn=lambda *a: FakePart(a[2]))
+        q.put((rank, stats, sols, ms))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gloo_first_solution_min_key_and_prefix_sum():
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker_first, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = {}
+    for _ in range(world):
+        rank, stats, sols, ms = q.get(timeout=120)
+        out[rank] = (stats, sols, ms)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank in range(world):
+        stats, sols, ms = out[rank]
+        assert stats == (30, 1, 200, 1)
+        assert sols == [list(range(8))]
+        assert ms == 4.0

@@ -13,6 +13,8 @@ import socket
 import pytest
 
 import golden_cases as G
+import oracle_binding as O
+from paper_1909_09213_b200 import models
 from paper_1909_09213_b200 import solver as S
 
 pytestmark = pytest.mark.gpu
@@ -113,3 +115,99 @@ def test_distributed_branch_and_bound_two_processes_ipc():
         for stats, obj, vals in got[rank]:
             assert obj == g["objective"] and vals == g["best"]
             assert stats[0] > 0
+
+
+# ---- exact first solution across shards (cubics_solve_first_shard) ---------------------------
+FIRST_KEYS = ["nq8|--max 1", "nq14|--max 1", "nq24|--max 1", "magic4|--max 1", "magic5|--max 1",
+              "rcsp_1000|--max 1"]
+
+
+# static split: no state shared between the ranks, so a rank searches its subtrees up to its OWN
+# first solution (exact, but unbounded work on sparse models such as rcsp: those use the queue)
+FIRST_CASES = [(k, False) for k in FIRST_KEYS if not k.startswith("rcsp")] + [(k, True) for k in FIRST_KEYS]
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+@pytest.mark.parametrize("key,shared", FIRST_CASES)
+def test_first_solution_across_shards_is_the_reference(key, world, shared):
+    # every rank's part run one after another on this GPU; the two-phase merge (min key, summed
+    # prefixes) must give the reference's first solution and its exact stats (search.cpp:174-186).
+    # With the queue, subtrees are claimed in DFS order and the best key prefix is shared, so
+    # every GPU abandons subtrees right of any GPU's solution.
+    g = G.goldens()[key]
+    inst, flags = G.split_key(key)
+    m = S.parse_model(G.model_text(inst))
+    cfg = G.cfg_from_flags(flags)
+    cfg.device = 0
+    q = S.TaskQueue.create(0) if shared else None
+    try:
+        if q is not None:
+            q.reset()
+        parts = [S.solve_first_shard(m, cfg, r, world, queue=q) for r in range(world)]
+        stats, vals = S.merge_first(parts)
+    finally:
+        if q is not None:
+            q.close()
+    assert stats.as_tuple() == G.expected_tuple(g)
+    assert vals == g["first"]
+
+
+def test_first_solution_none_across_shards_counts_the_whole_search():
+    # an infeasible model: no rank finds a solution, the shares sum to the complete search
+    m = S.parse_model(models.gen_nqueens(3))
+    ost = S.SearchStats()
+    O.enumerate_solutions(m, S.SearchConfig(), ost)
+    for world in (1, 2, 3):
+        parts = [S.solve_first_shard(m, S.SearchConfig(max_solutions=1, device=0), r, world) for r in range(world)]
+        stats, vals = S.merge_first(parts)
+        assert vals is None and stats.as_tuple() == ost.as_tuple()
+
+
+def _first_worker(rank, world, port, key, out):
+    import os
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    from paper_1909_09213_b200 import distributed as D
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        inst, flags = G.split_key(key)
+        m = S.parse_model(G.model_text(inst))
+        cfg = G.cfg_from_flags(flags)
+        cfg.device = 0
+        q = D.shared_task_queue(rank, world, device=0)
+        res = []
+        for queue in (q, q):
+            stats, sols, _ = D.solve_distributed(m, cfg, rank, world, queue=queue)
+            res.append((stats, sols))
+        dist.barrier()
+        q.close()
+        dist.barrier()
+        out.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_distributed_first_solution_two_processes_ipc():
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    key, world = "rcsp_1000|--max 1", 2
+    ctx = mp.get_context("spawn")
+    out = ctx.Queue()
+    procs = [ctx.Process(target=_first_worker, args=(r, world, port, key, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(out.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    g = G.goldens()[key]
+    for rank in range(world):
+        for stats, sols in got[rank]:
+            assert stats == G.expected_tuple(g)
+            assert sols == [g["first"]]
