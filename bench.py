@@ -29,11 +29,56 @@ REF_DRIVER = os.path.join(ROOT, "oracle", "_ref", "fdref_driver")
 MODELS = os.path.join(ROOT, "tests", "golden", "models")
 
 
+# instance -> (mode, config.workload string, reference CLI flags, golden key). The headline is
+# nq14 (BASELINE configs[1]); golomb10 and rcsp_1000 are the N>1 branch-and-bound and
+# first-solution workloads of BASELINE configs[2] / configs[4].
+WORKLOADS = {
+    "nq14": ("all", "nq14 all solutions (N-Queens n=14, BASELINE configs[1])", ["--all"], "nq14|--all"),
+    "golomb10": ("optimize", "Golomb ruler m=10, branch and bound to the optimum 55 (BASELINE configs[2])", [],
+                 "golomb10"),
+    "rcsp_1000": ("first", "random binary CSP n=1000, exact first solution (BASELINE configs[4], 1k point)",
+                  ["--max", "1"], "rcsp_1000|--max 1"),
+}
+
+
+def workload(instance):
+    return WORKLOADS.get(instance, ("all", f"{instance} all solutions", ["--all"], f"{instance}|--all"))
+
+
 def workload_name(instance):
     """The config.workload string, identical on both arms (this one and --impl reference)."""
-    if instance == "nq14":
-        return "nq14 all solutions (N-Queens n=14, BASELINE configs[1])"
-    return f"{instance} all solutions"
+    return workload(instance)[1]
+
+
+def host_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu": model}
+
+
+def l2_probe(device):
+    """Measured L2 read bandwidth: a 48 MiB buffer (resident in the 126 MB L2) summed 50 times,
+    CUDA events (the roofline denominator for L2-resident traffic; MEASURED_PEAKS has HBM only)."""
+    import torch
+
+    x = torch.ones(12 << 20, dtype=torch.float32, device=f"cuda:{device}")
+    for _ in range(5):
+        x.sum()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(device)
+    e0.record()
+    for _ in range(50):
+        x.sum()
+    e1.record()
+    torch.cuda.synchronize(device)
+    return x.numel() * 4 * 50 / (e0.elapsed_time(e1) / 1e3) / 1e9
 
 
 def load_peaks():
@@ -54,6 +99,15 @@ def ncu_traffic(instance):
         return rec["dram_read_bytes"] + rec["dram_write_bytes"], rec["report"]
     except Exception:  # noqa: BLE001
         return None, None
+
+
+def ncu_counts(instance):
+    """Per-launch instruction / shared-memory counts of the committed ncu capture (with its nodes)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_ncu_traffic.json")) as f:
+            return json.load(f)[instance]
+    except Exception:  # noqa: BLE001
+        return None
 
 
 def algorithmic_bytes(model, stats):
@@ -125,7 +179,8 @@ def run_reference(path, flags, threads=1, timeout=3600):
 
 
 def cpu_sample(instance, node_limit, threads):
-    out = run_reference(os.path.join(MODELS, instance + ".fd"), ["--all", "--node-limit", str(node_limit)], threads)
+    flags = workload(instance)[2] + (["--node-limit", str(node_limit)] if node_limit else [])
+    out = run_reference(os.path.join(MODELS, instance + ".fd"), flags, threads)
     return out["nodes"] / (out["time_ms"] / 1e3), out
 
 
@@ -144,11 +199,12 @@ def impl_reference(args):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/fdref_driver not built"}))
         return 0
     nproc = os.cpu_count() or 1
-    # bounded sample of the same workload: the first N nodes of the nq14 all-solutions DFS
-    limit = args.ref_node_limit
+    # bounded sample of the same workload: the first N nodes of the reference's DFS for it
+    # (branch and bound / first solution: a few seconds of the reference's much slower nodes)
+    limit = args.ref_node_limit if workload(args.instance)[0] == "all" else min(args.ref_node_limit, 10000)
     # the reference's only parallel knob (OpenMP propagation) slows this workload down
     # (SURVEY.md 2.3); pick whichever of 1 / nproc threads is faster on a short probe
-    probe = {t: cpu_sample(args.instance, 20000, t)[0] for t in sorted({1, nproc})}
+    probe = {t: cpu_sample(args.instance, 20000 if limit > 20000 else 2000, t)[0] for t in sorted({1, nproc})}
     threads = max(probe, key=probe.get)
     vals = []
     for i in range(args.warmup + args.steps):
@@ -163,8 +219,9 @@ def impl_reference(args):
         "data": "synthetic", "config": {"workload": workload_name(args.instance)},
         "run": {"sample": f"first {limit} DFS nodes"},
         "cpu_baseline": {"value": value, "unit": "nodes/s", "cores": threads, "kind": "reference",
-                         "sample": f"first {limit} nodes of the {args.instance} all-solutions DFS, threads={threads}",
-                         "probe_nodes_per_s": probe},
+                         "sample": f"first {limit} nodes of the reference's DFS for: {workload_name(args.instance)}, "
+                                   f"threads={threads}",
+                         "probe_nodes_per_s": probe, "host": host_info()},
         "e2e": {"value": value, "unit": "nodes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -174,17 +231,38 @@ def impl_reference(args):
 GOLDEN = os.path.join(ROOT, "tests", "golden", "goldens.json")
 
 
-def run_extras(S, A, device):
-    """The other BASELINE.json configs, one run each (device time; stats vs the reference goldens).
-    Reference CPU times are the survey-box / golden-run figures recorded in goldens.json."""
+def ref_same_run(key, g, budget_ms=4000):
+    """The unmodified reference (oracle/_ref/fdref_driver, 1 thread) on THIS host for one config:
+    the full search when the golden run took <= 2 x budget on the build box, else the first N nodes
+    of the same DFS (N sized for ~budget) and the full time extrapolated from the golden node count."""
+    inst, _, fl = key.partition("|")
+    path = os.path.join(MODELS, inst + ".fd")
+    if not g or not g.get("time_ms") or not os.path.exists(REF_DRIVER) or not os.path.exists(path):
+        return None
+    full = g["time_ms"] <= 2 * budget_ms
+    lim = None if full else max(1000, int(g["nodes"] * budget_ms / g["time_ms"]))
+    out = run_reference(path, fl.split() + (["--node-limit", str(lim)] if lim else []), 1)
+    rate = out["nodes"] / (out["time_ms"] / 1e3)
+    rec = {"ms": out["time_ms"] if full else None, "nodes_per_s": rate, "threads": 1, "same_host": True,
+           "sample": "full search" if full else f"first {lim} nodes of the same DFS"}
+    if not full:
+        rec["est_full_ms"] = g["nodes"] / rate * 1e3
+    return rec
+
+
+def run_extras(S, A, device, cpu=True):
+    """The other BASELINE.json configs, one run each (device time; stats vs the reference goldens),
+    each beside the unmodified reference run on this same host (ref_same_run)."""
     gold = json.load(open(GOLDEN))
     out = {}
     cases = [
         ("golomb10", "golomb10", A.ENGINE_PARALLEL, {}, "B&B to optimum, parallel engine (node count schedule-dependent)"),
         ("golomb10_parity", "golomb10", A.ENGINE_PARITY, {}, "B&B, parity engine (reference node order)"),
-        ("magic5_first", "magic5|--max 1", A.ENGINE_PARITY, {"max_solutions": 1}, "first solution, parity engine"),
+        ("magic5_first", "magic5|--max 1", A.ENGINE_AUTO, {"max_solutions": 1},
+         "exact first solution (AUTO: parallel engine, reference stats)"),
         ("magic4_all", "magic4|--all", A.ENGINE_PARALLEL, {}, "all solutions, parallel engine"),
-        ("rcsp_1000_first", "rcsp_1000|--max 1", A.ENGINE_PARITY, {"max_solutions": 1}, "first solution, parity engine"),
+        ("rcsp_1000_first", "rcsp_1000|--max 1", A.ENGINE_AUTO, {"max_solutions": 1},
+         "exact first solution (AUTO: parallel engine, reference stats)"),
         ("rcsp_100000_limit200", "rcsp_100000|--max 1 --node-limit 200", A.ENGINE_AUTO,
          {"max_solutions": 1, "node_limit": 200}, "node-limited, reference node order (grid-wide context)"),
         # BASELINE config 5 as stated: random binary CSP with extensional tables near the phase
@@ -217,7 +295,11 @@ def run_extras(S, A, device):
                    "engine": {1: "parity", 2: "parallel", 3: "grid"}.get(r.engine, r.engine),
                    "nodes_per_s": st[0] / (r.device_ms / 1e3) if r.device_ms else None,
                    "stats_equal_reference": (st == exp) if exp else None,
-                   "reference_cpu_ms": g.get("time_ms") if g else None, **extra}
+                   "reference_cpu": ref_same_run(key, g) if cpu else None,
+                   "reference_cpu_ms_build_box": g.get("time_ms") if g else None, **extra}
+            ref = rec["reference_cpu"]
+            if ref and r.device_ms:
+                rec["speedup_vs_reference_cpu"] = (ref["ms"] or ref["est_full_ms"]) / r.device_ms
             if m.goal != 0 and g:
                 rec["objective_equal_reference"] = extra["objective"] == g.get("objective")
             out[name] = rec
@@ -272,8 +354,10 @@ def impl_ours(args):
         return t.tolist()
     text = open(os.path.join(MODELS, args.instance + ".fd")).read()
     model = S.parse_model(text)
+    mode, _, _, gkey = workload(args.instance)
+    gold = json.load(open(GOLDEN)).get(gkey)
     cfg = S.SearchConfig(engine=A.ENGINE_PARALLEL, device=device, count_only=True, contexts=args.contexts,
-                         block_threads=args.block)
+                         block_threads=args.block, max_solutions=1 if mode == "first" else A.UINT64_MAX)
 
     # N > 1: frontier subtrees are claimed dynamically through one counter in rank 0's HBM that
     # every rank maps over NVLink (CUDA IPC); CUBICS_BENCH_STATIC=1 selects the static t % N split
@@ -294,7 +378,15 @@ def impl_ours(args):
                 if rank == 0:
                     queue.reset()
                 dist.barrier()
+            if mode == "optimize":  # shared incumbent through the queue state
+                return S.solve_optimize_shard(model, c, rank, world, queue=queue)
+            if mode == "first":  # DFS-order claims, shared best-key prefix
+                part = S.solve_first_shard(model, c, rank, world, queue=queue)
+                part.close()
+                return part.result
             return S.solve_shard(model, c, rank, world, queue=queue)
+        if mode == "optimize":
+            return S.solve_optimize(model, c)
         return S.solve_satisfy(model, c, (lambda s: True) if not count_only else None)
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{device}")  # > 126 MB L2
@@ -322,17 +414,29 @@ def impl_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         tot = S.SearchStats(*[int(x) for x in t.tolist()])
     e2e_ms, h2d, d2h, e2e_launches = [], 0, 0, 0
+    exact = None  # the reference's stats / objective reproduced by the public API call
     if world == 1:
-        # e2e: through the public C ABI (cubics_enumerate) with host buffers: model upload, search,
-        # device-side DFS ordering, and every solution copied back into a host int64 array
+        # e2e: through the public C ABI with host buffers: model upload, search, results back
+        full = S.SearchConfig(**{**cfg.__dict__, "count_only": False})
         for _ in range(args.steps):
             flush_l2()
             t0 = time.perf_counter()
-            arr, r2 = S.enumerate_array(model, S.SearchConfig(**{**cfg.__dict__, "count_only": False}))
+            if mode == "all":  # every solution, DFS-ordered on the device, into a host int64 array
+                arr, r2 = S.enumerate_array(model, full)
+                assert arr.shape[0] == r2.stats.solutions
+                exact = r2.stats.as_tuple()
+            elif mode == "optimize":  # the optimum's values
+                r2 = S.solve_optimize(model, full)
+                exact = r2.best.objective if r2.best else None
+            else:  # the DFS-first solution through the solution callback
+                got = []
+                r2 = S.solve_satisfy(model, full, lambda s: got.append(s.values) or True)
+                exact = r2.stats.as_tuple()
             e2e_ms.append((time.perf_counter() - t0) * 1e3)
             h2d, d2h, e2e_launches = r2.h2d_bytes, r2.d2h_bytes, r2.kernel_launches
-            assert arr.shape[0] == r2.stats.solutions
-        e2e_api = "cubics_enumerate (all solutions in DFS order into a host int64 array)"
+        e2e_api = {"all": "cubics_enumerate (all solutions in DFS order into a host int64 array)",
+                   "optimize": "cubics_solve_optimize (branch and bound; optimum values to the host)",
+                   "first": "cubics_solve_satisfy with a callback, max_solutions 1 (exact first solution)"}[mode]
     else:
         # e2e at N GPUs: the public multi-GPU API (distributed.solve_distributed -> cubics_solve_shard
         # + one all-reduce of the stats), wall time per rank, max over ranks
@@ -342,32 +446,81 @@ def impl_ours(args):
             flush_l2()
             barrier()
             t0 = time.perf_counter()
-            st, _, _ = D.solve_distributed(model, cfg, rank, world, collect=False, device=coll_dev, queue=queue)
+            st, res, _ = D.solve_distributed(model, cfg, rank, world, collect=False, device=coll_dev, queue=queue)
             e2e_ms.append((time.perf_counter() - t0) * 1e3)
-            assert tuple(st) == tot.as_tuple()
+            if mode == "all":
+                assert tuple(st) == tot.as_tuple()
+                exact = tuple(st)
+            elif mode == "optimize":
+                exact = res.objective if res else None
+            else:
+                exact = tuple(st)
         e2e_ms = max_over_ranks(e2e_ms)
         h2d, d2h = r.h2d_bytes, r.d2h_bytes
         e2e_launches = r.kernel_launches
-        e2e_api = ("distributed.solve_distributed (cubics_solve_shard%s per rank + all-reduce of the stats)"
-                   % ("_shared" if queue is not None else ""))
-    extras = run_extras(S, A, device) if (rank == 0 and not args.no_extras) else None
-    nodes = tot.nodes
+        e2e_api = ("distributed.solve_distributed (%s per rank + all-reduce of the stats)"
+                   % {"all": "cubics_solve_shard" + ("_shared" if queue is not None else ""),
+                      "optimize": "cubics_solve_optimize_shard, shared incumbent",
+                      "first": "cubics_solve_first_shard + min-key all-gather"}[mode])
+    extras = run_extras(S, A, device, cpu=not args.no_cpu) if (rank == 0 and not args.no_extras) else None
+    l2_gbs = l2_probe(device) if rank == 0 else None
     if rank != 0:
         dist.destroy_process_group()
         return 0
     mean_ms = sum(dev_ms) / len(dev_ms)
+    # all solutions: every node is visited exactly once, nodes = the reference's. Branch and bound
+    # and first solution: the GPUs search a different (speculative / schedule-dependent) node set,
+    # so value = the reference's node count for the same answer / time to the answer
+    # ("reference-equivalent nodes/s", a time-to-answer ratio against the CPU arm's nodes/s)
+    nodes = tot.nodes if mode == "all" or not gold else gold["nodes"]
     value = nodes / (mean_ms / 1e3)
+    if mode == "all":
+        parity_ok = gold is not None and exact == (gold["nodes"], gold["failures"], gold["rounds"], gold["solutions"])
+    elif mode == "optimize":
+        parity_ok = gold is not None and exact == gold.get("objective")
+    else:
+        parity_ok = gold is not None and exact == (gold["nodes"], gold["failures"], gold["rounds"], gold["solutions"])
+    parity = {gkey: parity_ok}
+    for name, rec in (extras or {}).items():
+        if rec.get("stats_equal_reference") is False and rec.get("objective_equal_reference") is not None:
+            parity[name + "_objective"] = rec["objective_equal_reference"]  # schedule-dependent node count
+        elif rec.get("stats_equal_reference") is not None:
+            parity[name] = rec["stats_equal_reference"]
     A_bytes, S_, V = algorithmic_bytes(model, tot)
     peak, peak_kind = load_peaks()
     achieved = A_bytes / (mean_ms / 1e3) / 1e9
     traffic, traffic_src = ncu_traffic(args.instance)
+    clocks = clk.summary()
+    sm_hz = (clocks.get("sm_mhz") or 1965) * 1e6
+    # the rooflines that bind this latency-bound search (counts per node from the committed ncu
+    # capture of this workload, scaled by this run's nodes and time)
+    issue = smem = None
+    cap = ncu_counts(args.instance)
+    if cap and cap.get("inst_executed") and cap.get("nodes"):
+        per_node = cap["inst_executed"] / cap["nodes"]
+        ach = per_node * tot.nodes / (mean_ms / 1e3)
+        peak_i = 148 * 4 * sm_hz  # 4 schedulers x 1 warp-instruction / cycle per SM
+        issue = {"achieved": ach / 1e9, "peak": peak_i / 1e9, "unit": "G warp-inst/s", "frac": ach / peak_i,
+                 "warp_inst_per_node": per_node, "source": cap["report"]}
+        if cap.get("smem_wavefronts"):
+            wn = cap["smem_wavefronts"] / cap["nodes"]
+            ach_s = wn * tot.nodes / (mean_ms / 1e3)
+            peak_s = 148 * sm_hz  # one shared-memory wavefront per cycle per SM
+            smem = {"achieved": ach_s / 1e9, "peak": peak_s / 1e9, "unit": "G wavefronts/s", "frac": ach_s / peak_s,
+                    "wavefronts_per_node": wn}
     # CPU baseline: the unmodified reference on this host, bounded sample
     cpu = None
     if os.path.exists(REF_DRIVER) and not args.no_cpu and world == 1:
-        v, out = cpu_sample(args.instance, args.cpu_node_limit, 1)
+        lim = args.cpu_node_limit if mode == "all" else min(args.cpu_node_limit, 10000)
+        v, out = cpu_sample(args.instance, lim, 1)
         cpu = {"value": v, "unit": "nodes/s", "cores": 1, "kind": "reference",
-               "sample": f"first {args.cpu_node_limit} nodes of the {args.instance} all-solutions DFS "
-                         f"(oracle/_ref/fdref_driver, thread_count=1, {out['time_ms']:.0f} ms)"}
+               "sample": f"first {lim} nodes of the reference's DFS for: {workload_name(args.instance)} "
+                         f"(oracle/_ref/fdref_driver, thread_count=1, {out['time_ms']:.0f} ms)",
+               "host": host_info()}
+        if args.cpu_full:  # the whole search, measured (not extrapolated): minutes for nq14
+            full = run_reference(os.path.join(MODELS, args.instance + ".fd"), workload(args.instance)[2], 1)
+            cpu["full_search_ms"] = full["time_ms"]
+            cpu["full_search_nodes"] = full["nodes"]
     e2e_mean = sum(e2e_ms) / len(e2e_ms)  # same statistic as value (mean over the timed steps)
     line = {
         "metric": METRIC, "value": value, "unit": "nodes/s", "n_gpus": world, "steps": args.steps,
@@ -382,22 +535,32 @@ def impl_ours(args):
                                  "in-GPU work-sharing ring" if queue is not None else
                                  "static t % N frontier split + in-GPU work-sharing ring"),
                    "stats": {"nodes": tot.nodes, "failures": tot.failures, "rounds": tot.rounds,
-                             "solutions": tot.solutions}},
-        "time_to_all_solutions_ms": mean_ms,
+                             "solutions": tot.solutions},
+                   "value_nodes": "nodes visited (exact)" if mode == "all" else
+                                  f"the reference's {nodes} nodes for this answer / device time to the answer "
+                                  f"(searched: {tot.nodes})"},
+        "time_to_all_solutions_ms" if mode == "all" else
+        ("time_to_optimum_ms" if mode == "optimize" else "time_to_first_solution_ms"): mean_ms,
         # rounds x constraints / device time (every constraint counted every round,
         # as the reference evaluates them; the engine itself skips untriggered ones)
         "propagator_evals_per_s": tot.rounds * model.n_cons / (mean_ms / 1e3),
         "e2e": {"value": nodes / (e2e_mean / 1e3), "unit": "nodes/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "time_to_all_solutions_ms": e2e_mean, "steps": len(e2e_ms), "api": e2e_api,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_mean, "steps": len(e2e_ms), "api": e2e_api,
                 "gpu_launches": e2e_launches},
         "gpu_launches": r.kernel_launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                      "peak_kind": peak_kind,
                      "algorithmic_bytes": A_bytes, "S_words": S_, "V_words": V,
-                     "note": "latency/barrier-bound search; A from SURVEY 8(d)"},
+                     "l2": {"achieved": achieved, "peak": l2_gbs, "unit": "GB/s",
+                            "frac": achieved / l2_gbs if l2_gbs else None,
+                            "peak_kind": "measured in this run (l2_probe: 48 MiB L2-resident read)"},
+                     "issue": issue, "smem": smem,
+                     "note": "the algorithmic bytes never reach DRAM (traffic = ncu dram bytes per launch); "
+                             "the binding limit is instruction issue (roofline.issue)"},
+        "parity": parity,
         "cpu_baseline": cpu,
-        "clocks": clk.summary(),
+        "clocks": clocks,
         "other_configs": extras,
     }
     print(json.dumps(line))
@@ -419,6 +582,7 @@ def main():
     ap.add_argument("--ref-node-limit", type=int, default=200000)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--cpu-full", action="store_true", help="also time the reference's complete search")
     args = ap.parse_args()
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
         return self_spawn(args)

@@ -147,6 +147,9 @@ class OptimizeResult:
     contexts: int = 1
     device_ms: float = 0.0
     total_ms: float = 0.0
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
+    kernel_launches: int = 0
 
 
 @dataclass
@@ -442,7 +445,8 @@ def solve_optimize(model: Model, cfg: SearchConfig | None = None) -> OptimizeRes
     sol = None
     if res.has_solution:
         sol = Solution([best[i] for i in range(model.n_vars)], res.objective)
-    return OptimizeResult(sol, bool(res.complete), _stats(res), res.engine, res.contexts, res.device_ms, res.total_ms)
+    return OptimizeResult(sol, bool(res.complete), _stats(res), res.engine, res.contexts, res.device_ms, res.total_ms,
+                          res.h2d_bytes, res.d2h_bytes, res.kernel_launches)
 
 
 def optimize_batch(model: Model, domain_words, bounds=None, cfg: SearchConfig | None = None):
@@ -636,7 +640,8 @@ def solve_optimize_shard(model: Model, cfg: SearchConfig, shard_index: int, shar
                                              queue.ptr if queue is not None else None, best, C.byref(res)),
            "solve_optimize_shard")
     sol = Solution([best[i] for i in range(model.n_vars)], res.objective) if res.has_solution else None
-    return OptimizeResult(sol, bool(res.complete), _stats(res), res.engine, res.contexts, res.device_ms, res.total_ms)
+    return OptimizeResult(sol, bool(res.complete), _stats(res), res.engine, res.contexts, res.device_ms, res.total_ms,
+                          res.h2d_bytes, res.d2h_bytes, res.kernel_launches)
 
 
 class FirstShard:
