@@ -10,7 +10,8 @@
 //   save-on-modify trail (state.cpp:12-36): both reinstate the state on entering the level.
 //   At most one frame per variable is live (each left branch fixes one more variable).
 // * Parallel engine: many contexts per GPU. A busy context donates its shallowest pending right
-//   branch to an idle one through a spin-locked queue in HBM; nodes are visited exactly once,
+//   branch to an idle one through a lock-free ticket ring in HBM (each idle context spins on its
+//   own ring slot); nodes are visited exactly once,
 //   so nodes/failures/rounds/solutions of a complete enumeration are exact sums. Each subtree
 //   carries its DFS path bits, the key that restores the reference's solution order.
 #pragma once
