@@ -174,6 +174,8 @@ typedef struct cubics_result {
     uint64_t h2d_bytes;    /* bytes copied host -> device by this call */
     uint64_t d2h_bytes;    /* bytes copied device -> host by this call */
     uint64_t kernel_launches; /* CUDA kernels this call launched */
+    uint64_t remote_tasks_in;  /* shared queue: subtrees this GPU took from other GPUs' donations */
+    uint64_t remote_tasks_out; /* shared queue: subtrees this GPU gave to idle GPUs */
 } cubics_result;
 
 /* Receives each solution (values indexed by var id, as fd::Solution::values) in the

@@ -91,6 +91,8 @@ class Result(C.Structure):
         ("h2d_bytes", C.c_uint64),
         ("d2h_bytes", C.c_uint64),
         ("kernel_launches", C.c_uint64),
+        ("remote_tasks_in", C.c_uint64),
+        ("remote_tasks_out", C.c_uint64),
     ]
 
 

@@ -79,6 +79,7 @@ enum DeviceError : int32_t {
     DERR_NONE = 0,
     DERR_OVERFLOW = 1,
     DERR_CAPACITY = 2,
+    DERR_GUIDE = 3, // a guided replay failed before its solution (internal error)
 };
 
 // Global coordination state for the parallel engine (one per launch, in HBM).
@@ -116,6 +117,24 @@ struct WorkState {
     int32_t pad2;
     uint64_t ev_head;      // streaming: event slots reserved
     uint64_t ev_tail;      // streaming: the host's consumed count as last read over PCIe
+    int32_t xs_thief;      // cross-GPU stealing: a waiting context holds the thief role
+    int32_t xs_idle;       // this GPU returned its busy token (all contexts idle)
+    int32_t xs_done;       // global termination seen: every waiting context exits
+    int32_t pad3;
+    int64_t xs_since;      // clock64 when this GPU's thief started waiting (any context may hold the role)
+    uint64_t xs_in;        // subtrees taken from the global pool
+    uint64_t xs_out;       // subtrees given to the global pool
+};
+
+// Cross-GPU stealing control block (in the shared queue owner's HBM, system-scope atomics).
+// work = GPUs still searching + subtrees in the pool; a GPU exits when it reads 0 (or abort).
+struct XsCtl {
+    uint32_t push;    // pool tickets handed out to donors
+    uint32_t pop;     // pool tickets taken by thieves (pop <= push)
+    int32_t work;
+    int32_t demand;   // subtrees idle GPUs asked for that no donor has committed to yet
+    int32_t abort;    // a GPU stopped (error / limit): nobody waits for work any more
+    int32_t pad[3];
 };
 
 struct SearchParams {
@@ -203,6 +222,23 @@ struct SearchParams {
     // engine the segment events that put them back into DFS order, go into a ring in host-mapped
     // pinned memory that the calling thread drains while the kernel runs (see search.cuh EvKind).
     // The host stops the search by setting ws->hot.stop from a second stream.
+    // cross-GPU stealing (cubics_solve_shard_shared): a global pool of right branches in the queue
+    // owner's HBM. A busy context donates its shallowest pending branch into it while some GPU's
+    // thief waits; an idle GPU's thief copies one into its own outbox and republishes it in its
+    // local ticket ring. Null: off.
+    XsCtl* xs_ctl;
+    uint8_t* xs_slots;                       // [xs_cap][xs_slot]: u32 seq (ticket + 1 when full) | pad | OS words
+    uint32_t xs_cap, xs_slot;
+    // exact parallel branch and bound (engine.cu exact_bnb): a phase keeps the bound it started
+    // with (the reference's bound between two improving solutions); no incumbent sharing
+    int32_t static_bound;
+    // guided replay (reference-order kernels): follow guide_key from the root; at every left
+    // decision on the path the still-pending right branch goes out as a task (outbox layout) into
+    // tasks[]; the B&B shrink at depth d uses guide_bound[d] / guide_has[d], the bound the
+    // reference had when it entered that node. Null: off.
+    const uint32_t* guide_key;
+    const int64_t* guide_bound;
+    const int32_t* guide_has;
     int32_t stream;
     uint32_t ev_cap;                         // slots
     uint32_t ev_slot;                        // bytes per slot

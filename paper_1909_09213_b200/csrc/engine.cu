@@ -44,6 +44,9 @@ constexpr int kFastAllDiffMembers = 64;  // warp fast path; larger ones take the
 constexpr int kMaxAllDiffMembers = 4096;  // generic path limit (n x n member bit rows per warp)
 constexpr long kMaxUniverseWords = 1024;  // generic path value universe (32768 values)
 constexpr size_t kSmemBudget = 200 * 1024;
+// shared task queue state (rank 0's HBM, IPC-mapped): 256-byte header + the cross-GPU pool
+constexpr size_t kXsBytes = size_t(32) << 20;
+constexpr size_t kQueueBytes = 256 + kXsBytes;
 
 struct CudaError {
     std::string msg;
@@ -592,6 +595,15 @@ struct ShardIO {
     unsigned int* claim = nullptr; // shared queue: seeds are claimed through this counter instead
     unsigned long long* g_inc = nullptr; // multi-GPU B&B: shared incumbent (queue state, IPC-mapped)
     unsigned long long* g_first = nullptr; // sharded first solution: best key prefix of all ranks
+    uint8_t* xs = nullptr; // cross-GPU stealing: the shared queue state (XsCtl at +128, pool at +256)
+    // exact parallel B&B (exact_bnb): phase 0 is an exact first solution over the whole tree
+    // (root_first); every phase keeps its starting bound (static_bound); a guided replay run
+    // (guide_key, reference-order kernel) emits the pending right branches of a recorded path
+    bool root_first = false;
+    bool static_bound = false;
+    const std::vector<uint32_t>* guide_key = nullptr;
+    std::vector<int64_t> guide_bound; // [KW * 32 + 1]
+    std::vector<int32_t> guide_has;
     // sharded first solution: 1 = seeded run with the exact-first bookkeeping (segments,
     // abandoning right of this rank's best); 2 = frontier expansion with segments only
     int first = 0;
@@ -822,10 +834,11 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
         engine = CUBICS_ENGINE_GRID;
     const bool grid = engine == CUBICS_ENGINE_GRID;
     const bool parallel = engine == CUBICS_ENGINE_PARALLEL;
-    const bool keyed = parallel || (shard && shard->split_depth > 0);
+    const bool keyed = parallel || (shard && (shard->split_depth > 0 || shard->guide_key));
     // exact parallel first solution: complete otherwise-equal search, max_solutions == 1
-    const bool first_mode = parallel && !shard && !sio && hm.goal == CUBICS_SATISFY && cfg.max_solutions == 1 &&
-                            cfg.node_limit == 0;
+    const bool first_mode = (parallel && !shard && !sio && hm.goal == CUBICS_SATISFY && cfg.max_solutions == 1 &&
+                             cfg.node_limit == 0) ||
+                            (parallel && shard && shard->root_first);
     if (sio && (shard || batch || (parallel && hm.goal != CUBICS_SATISFY)))
         throw StatusError{CUBICS_E_INVALID, "streaming: reference-order engines, or the parallel engine on satisfy goals"};
     if (first_mode) {
@@ -841,7 +854,7 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
     // small models run warp contexts (warp_ctx.cuh): K contexts per block of 32K threads
     // (sharded first-solution runs need the frontier split with segment bookkeeping, which the
     // lean warp kernels compile out: they run block contexts)
-    const bool use_warp = P.warp_ok && !grid && !batch && cfg.block_threads <= 0 && !(shard && shard->first) &&
+    const bool use_warp = P.warp_ok && !grid && !batch && cfg.block_threads <= 0 && !(shard && (shard->first || shard->root_first)) &&
                           (parallel || engine == CUBICS_ENGINE_PARITY) && !std::getenv("CUBICS_NO_WARP");
     const int warp_k = use_warp && parallel ? std::max(1, std::min(2, std::getenv("CUBICS_WARP_K") ? std::atoi(std::getenv("CUBICS_WARP_K")) : 1)) : 1;
     int block = cfg.block_threads > 0 ? ((cfg.block_threads + 31) / 32) * 32 : 0;
@@ -956,6 +969,11 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
     const size_t a_bstats = take(sizeof(uint64_t) * 4 * nb);
     const size_t a_bflags = take(sizeof(int32_t) * nb);
     const size_t a_binc = take(sizeof(uint16_t) * n * nb);
+    const bool guided = shard && shard->guide_key;
+    const size_t gdepth = (size_t)KW * 32 + 1;
+    const size_t a_gkey = take(guided ? sizeof(uint32_t) * KW : 0);
+    const size_t a_gbnd = take(guided ? sizeof(int64_t) * gdepth : 0);
+    const size_t a_ghas = take(guided ? sizeof(int32_t) * gdepth : 0);
     uint8_t* base = device_arena(dev, off);
 
     cudaStream_t st = g_dev[dev].stream;
@@ -1059,6 +1077,29 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
         S.task_claim = shard ? shard->claim : nullptr;
         S.g_inc = shard ? shard->g_inc : nullptr;
         S.g_first = shard ? shard->g_first : nullptr;
+        S.static_bound = shard && shard->static_bound ? 1 : 0;
+        if (guided) {
+            if (shard->guide_key->size() != (size_t)KW || shard->guide_bound.size() != gdepth ||
+                shard->guide_has.size() != gdepth)
+                throw StatusError{CUBICS_E_INVALID, "guided replay: key / bound sizes"};
+            CU(cudaMemcpyAsync(base + a_gkey, shard->guide_key->data(), sizeof(uint32_t) * KW, cudaMemcpyHostToDevice, st));
+            CU(cudaMemcpyAsync(base + a_gbnd, shard->guide_bound.data(), sizeof(int64_t) * gdepth, cudaMemcpyHostToDevice, st));
+            CU(cudaMemcpyAsync(base + a_ghas, shard->guide_has.data(), sizeof(int32_t) * gdepth, cudaMemcpyHostToDevice, st));
+            out.h2d += sizeof(uint32_t) * KW + (sizeof(int64_t) + sizeof(int32_t)) * gdepth;
+            S.guide_key = reinterpret_cast<const uint32_t*>(base + a_gkey);
+            S.guide_bound = reinterpret_cast<const int64_t*>(base + a_gbnd);
+            S.guide_has = reinterpret_cast<const int32_t*>(base + a_ghas);
+        }
+        if (shard && shard->xs && parallel && !seg_mode && !std::getenv("CUBICS_NO_XS")) { // pool slots: header + outbox
+            const size_t slot = (16 + 4 * OS + 15) & ~size_t(15);
+            const size_t cap = std::min<size_t>(4096, kXsBytes / slot);
+            if (cap >= 8) {
+                S.xs_ctl = reinterpret_cast<XsCtl*>(shard->xs + 128);
+                S.xs_slots = shard->xs + 256;
+                S.xs_cap = (uint32_t)cap;
+                S.xs_slot = (uint32_t)slot;
+            }
+        }
         S.first_mode = seg_mode;
         S.seg_base = shard && shard->claim ? n_seed : 0;
         S.task_snap = reinterpret_cast<uint64_t*>(base + a_tsnap);
@@ -1160,6 +1201,8 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
             }
             if (best >= 0) {
                 for (int i = 0; i < 3; ++i) tot[i] += sst[best * 3 + i];
+                out.first_key.assign(solk.begin() + best * KW, solk.begin() + (best + 1) * KW);
+                out.has_first = true;
                 out.rec.count = 1;
                 out.rec.ordered = true;
                 out.rec.vals.resize(n);
@@ -1282,13 +1325,14 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
         const double tot = (double)w.busy_cycles + (double)w.idle_cycles;
         std::fprintf(stderr,
                      "[cubics] engine=%s%s ctx=%d block=%d W=%d smem=%zu KW=%d ms=%.3f nodes=%llu donations=%llu "
-                     "steals=%llu busy=%.3f\n",
+                     "steals=%llu busy=%.3f xs_in=%llu xs_out=%llu\n",
                      parallel ? "parallel" : "parity", use_warp ? "(warp)" : "", n_ctx, block, P.W, smem_block, KW, out.device_ms,
                      (unsigned long long)w.stats[0], (unsigned long long)w.donations, (unsigned long long)w.steals,
-                     tot > 0 ? w.busy_cycles / tot : 0.0);
+                     tot > 0 ? w.busy_cycles / tot : 0.0, (unsigned long long)w.xs_in, (unsigned long long)w.xs_out);
     }
     if (out.ws.error == DERR_OVERFLOW) throw StatusError{CUBICS_E_OVERFLOW, "overflow in linear propagation"};
     if (out.ws.error == DERR_CAPACITY) throw StatusError{CUBICS_E_CAPACITY, "device decision stack capacity exceeded"};
+    if (out.ws.error == DERR_GUIDE) throw StatusError{CUBICS_E_INVALID, "guided replay left its recorded path"};
 }
 
 void fill_result(const RunOut& r, cubics_result* out) {
@@ -1302,6 +1346,8 @@ void fill_result(const RunOut& r, cubics_result* out) {
     out->h2d_bytes = r.h2d;
     out->d2h_bytes = r.d2h;
     out->kernel_launches = r.launches;
+    out->remote_tasks_in = r.ws.xs_in;
+    out->remote_tasks_out = r.ws.xs_out;
 }
 
 int pick_engine(const cubics_search_config& cfg, bool optimize_goal) {
@@ -1610,6 +1656,145 @@ extern "C" void cubics_solutions_free(cubics_solutions* s) {
     delete s;
 }
 
+namespace {
+// Exact parallel branch and bound: the reference's solve_optimize (search.cpp:187-201) - node
+// order, every stat, every incumbent - at parallel-engine speed. Between two improving solutions
+// K_i and K_i+1 (DFS order) the reference's bound is constant, v_i. So the search is a chain of
+// exact-first-solution searches, each with a static bound:
+//   phase 0: the DFS-first solution of the whole tree (no bound): K_1, and the reference's stats
+//            up to it (segment prefix sums, as for max_solutions == 1);
+//   phase i: replay K_i's path from the root on the reference-order kernel, with the bound the
+//            reference had when it entered each node on it (the last K_j left of that node), and
+//            emit the right branch of every left decision on the path - exactly the branches the
+//            reference still has pending when it reaches K_i; seed them (DFS order) into the
+//            parallel engine's exact-first search under the static bound v_i: K_i+1 and the
+//            stats from K_i to it. No K_i+1: that phase searched the rest of the tree.
+// The stats are the sums over the phases; the solutions are the K_i.
+void exact_bnb(const HostModel& m, const cubics_search_config& cfg0, std::vector<uint16_t>& best, cubics_result* out) {
+    const int n = m.n_vars();
+    const bool minimizing = m.goal == CUBICS_MINIMIZE;
+    cubics_search_config c = cfg0;
+    c.engine = CUBICS_ENGINE_PARALLEL;
+    uint64_t tot[3] = {0, 0, 0}, sols = 0;
+    std::vector<std::vector<uint32_t>> keys; // K_1, K_2, ... (increasing DFS order)
+    std::vector<int64_t> objs;
+    auto add = [&](const RunOut& r) {
+        out->device_ms += r.device_ms;
+        out->h2d_bytes += r.h2d;
+        out->d2h_bytes += r.d2h;
+        out->kernel_launches += r.launches;
+        out->contexts = std::max(out->contexts, r.contexts);
+    };
+    auto objective = [&](const uint16_t* row) { return m.offset[m.goal_var] + (int64_t)row[m.goal_var]; };
+    int KW = 0;
+    { // phase 0
+        RunOut r;
+        ShardIO io;
+        io.root_first = true;
+        io.first = 1;
+        io.static_bound = true;
+        run_search(m, c, CUBICS_ENGINE_PARALLEL, true, 65536, r, true, &io);
+        add(r);
+        KW = r.KW;
+        for (int i = 0; i < 3; ++i) tot[i] += r.ws.stats[i];
+        if (r.has_first) {
+            keys.push_back(r.first_key);
+            best.assign(r.rec.vals.begin(), r.rec.vals.begin() + n);
+            objs.push_back(objective(best.data()));
+            ++sols;
+        }
+    }
+    while (!keys.empty()) {
+        const std::vector<uint32_t>& K = keys.back();
+        // the bound in force when the reference entered the node at depth d of K's path
+        const size_t gd = (size_t)KW * 32 + 1;
+        ShardIO rp;
+        rp.guide_key = &K;
+        rp.guide_bound.assign(gd, 0);
+        rp.guide_has.assign(gd, 0);
+        std::vector<uint32_t> node(KW);
+        for (size_t d = 0; d < gd; ++d) {
+            for (int w = 0; w < KW; ++w) {
+                const long c0 = (long)d - 32L * w; // prefix bits of word w that are kept
+                node[w] = c0 <= 0 ? 0u : (c0 >= 32 ? K[w] : (K[w] & ~(0xffffffffu >> c0)));
+            }
+            int64_t b = cfg0.initial_bound;
+            int32_t hb = cfg0.has_initial_bound ? 1 : 0;
+            for (size_t j = 0; j < keys.size(); ++j)
+                if (std::lexicographical_compare(keys[j].begin(), keys[j].end(), node.begin(), node.end())) {
+                    b = objs[j];
+                    hb = 1;
+                }
+            rp.guide_bound[d] = b;
+            rp.guide_has[d] = hb;
+        }
+        const int dev = current_device(c.device);
+        Prepared P;
+        prepare(m, m.words.data(), P);
+        const size_t OS = P.NWP + dev::round4((size_t)KW + 2);
+        rp.task_cap = gd;
+        rp.task_dev = reinterpret_cast<uint32_t*>(device_arena(dev, sizeof(uint32_t) * OS * rp.task_cap, 1));
+        cubics_search_config cr = c;
+        cr.engine = CUBICS_ENGINE_PARITY;
+        RunOut rr;
+        run_search(m, cr, CUBICS_ENGINE_PARITY, false, 0, rr, false, &rp);
+        add(rr);
+        const uint64_t nt = rp.n_tasks;
+        if (nt == 0) break; // nothing right of K_i: the search is complete
+        std::vector<uint32_t> tkey(nt * KW);
+        CU(cudaMemcpy2D(tkey.data(), sizeof(uint32_t) * KW, rp.task_dev + P.NWP, sizeof(uint32_t) * OS,
+                        sizeof(uint32_t) * KW, nt, cudaMemcpyDeviceToHost));
+        std::vector<int32_t> seeds(nt);
+        std::iota(seeds.begin(), seeds.end(), 0);
+        std::sort(seeds.begin(), seeds.end(), [&](int32_t x, int32_t y) {
+            return std::lexicographical_compare(tkey.begin() + (size_t)x * KW, tkey.begin() + (size_t)(x + 1) * KW,
+                                                tkey.begin() + (size_t)y * KW, tkey.begin() + (size_t)(y + 1) * KW);
+        });
+        ShardIO ph;
+        ph.task_dev = rp.task_dev;
+        ph.seeds = &seeds;
+        ph.first = 1;
+        ph.static_bound = true;
+        cubics_search_config cp = c;
+        cp.has_initial_bound = 1;
+        cp.initial_bound = objs.back();
+        RunOut pr;
+        run_search(m, cp, CUBICS_ENGINE_PARALLEL, true, 65536, pr, true, &ph);
+        add(pr);
+        if (pr.ws.sol_count > pr.rec.count) throw StatusError{CUBICS_E_CAPACITY, "exact B&B solution bookkeeping"};
+        // K_i+1: the DFS-first solution of the phase; the stats up to it
+        int64_t bi = -1;
+        for (uint64_t i = 0; i < pr.rec.count; ++i)
+            if (bi < 0 || std::lexicographical_compare(pr.rec.keys.begin() + i * KW, pr.rec.keys.begin() + (i + 1) * KW,
+                                                       pr.rec.keys.begin() + bi * KW, pr.rec.keys.begin() + (bi + 1) * KW))
+                bi = (int64_t)i;
+        const int64_t own = bi >= 0 ? pr.rec.seg[bi] : -1;
+        for (uint64_t s = 0; s < ph.n_seg; ++s) {
+            if ((int64_t)s == own) continue;
+            if (bi >= 0 && !std::lexicographical_compare(ph.seg_key.begin() + s * KW, ph.seg_key.begin() + (s + 1) * KW,
+                                                         pr.rec.keys.begin() + bi * KW, pr.rec.keys.begin() + (bi + 1) * KW))
+                continue; // right of K_i+1
+            for (int i = 0; i < 3; ++i) tot[i] += ph.seg_st[s * 3 + i];
+        }
+        if (bi < 0) break; // no improving solution right of K_i: complete
+        for (int i = 0; i < 3; ++i) tot[i] += pr.rec.stats[bi * 3 + i];
+        keys.emplace_back(pr.rec.keys.begin() + bi * KW, pr.rec.keys.begin() + (bi + 1) * KW);
+        best.assign(pr.rec.vals.begin() + bi * n, pr.rec.vals.begin() + (bi + 1) * n);
+        const int64_t v = objective(best.data());
+        if (!(minimizing ? v < objs.back() : v > objs.back()))
+            throw StatusError{CUBICS_E_INVALID, "exact B&B: a phase returned a non-improving solution"};
+        objs.push_back(v);
+        ++sols;
+    }
+    out->stats.nodes = tot[0];
+    out->stats.failures = tot[1];
+    out->stats.rounds = tot[2];
+    out->stats.solutions = sols;
+    out->engine = CUBICS_ENGINE_PARALLEL;
+    out->complete = 1;
+}
+} // namespace
+
 extern "C" int cubics_solve_optimize(const cubics_model* h, const cubics_search_config* cfg, int64_t* best_values,
                                      cubics_result* out) {
     if (!h || !cfg || !out) return CUBICS_E_INVALID;
@@ -1619,6 +1804,31 @@ extern "C" int cubics_solve_optimize(const cubics_model* h, const cubics_search_
         const HostModel& m = h->m;
         if (m.goal == CUBICS_SATISFY) throw StatusError{CUBICS_E_NO_OBJECTIVE, "solve_optimize requires a minimize or maximize goal"};
         cubics_search_config c = *cfg;
+        const int n = m.n_vars();
+        // AUTO: the exact parallel branch and bound (reference stats and incumbents); the
+        // reference-order engine for node-limited / solution-capped searches
+        if (c.engine == CUBICS_ENGINE_AUTO && c.node_limit == 0 &&
+            c.max_solutions == std::numeric_limits<uint64_t>::max() && n > 0 && !std::getenv("CUBICS_NO_EXACT_BNB")) {
+            std::vector<uint16_t> best;
+            bool done = false;
+            try {
+                exact_bnb(m, c, best, out);
+                done = true;
+            } catch (const StatusError& e) {
+                if (e.code != CUBICS_E_CAPACITY) throw;
+                std::memset(out, 0, sizeof *out); // bookkeeping capacity: the reference-order engine
+            }
+            if (done) {
+                out->has_solution = !best.empty();
+                if (!best.empty()) {
+                    out->objective = m.offset[m.goal_var] + best[m.goal_var];
+                    if (best_values)
+                        for (int v = 0; v < n; ++v) best_values[v] = m.offset[v] + best[v];
+                }
+                out->total_ms = now_ms() - t0;
+                return (int)CUBICS_OK;
+            }
+        }
         if (c.engine == CUBICS_ENGINE_AUTO) c.engine = CUBICS_ENGINE_PARITY;
         const int engine = pick_engine(c, true);
         RunOut r;
@@ -1626,7 +1836,6 @@ extern "C" int cubics_solve_optimize(const cubics_model* h, const cubics_search_
         const bool parallel = engine == CUBICS_ENGINE_PARALLEL;
         run_search(m, c, engine, !parallel, parallel ? 0 : default_sol_cap(m, c), r);
         fill_result(r, out);
-        const int n = m.n_vars();
         out->complete = !r.ws.limit_hit;
         std::vector<uint16_t> best;
         if (parallel) {
@@ -1641,7 +1850,7 @@ extern "C" int cubics_solve_optimize(const cubics_model* h, const cubics_search_
                 for (int v = 0; v < n; ++v) best_values[v] = m.offset[v] + best[v];
         }
         out->total_ms = now_ms() - t0;
-        return CUBICS_OK;
+        return (int)CUBICS_OK;
     });
 }
 
@@ -1694,6 +1903,8 @@ namespace {
 //   [0]  u32 claim counter              (next frontier subtree to claim)
 //   [8]  u64 shared incumbent, encoded   (bound_enc in search.cuh; all ones = none)
 //   [16] u64 first 64 key bits of the best first solution any rank found (all ones = none)
+//   [128] XsCtl: cross-GPU stealing counters (device_model.hpp)
+//   [256] the global pool of stolen right branches: kXsBytes of slots, geometry per search
 struct QueueState {
     uint32_t claim;
     uint32_t pad;
@@ -1890,6 +2101,7 @@ int solve_shard_impl(const cubics_model* h, const cubics_search_config* cfg, int
             seeded.seeds = &mine;
             seeded.claim = qs ? &qs->claim : nullptr;
             seeded.g_inc = qs && optimize ? &qs->g_inc : nullptr;
+            seeded.xs = qs ? reinterpret_cast<uint8_t*>(qs) : nullptr;
             auto go = [&](uint64_t cap) {
                 run_search(m, cs, CUBICS_ENGINE_PARALLEL, record, record ? cap : 0, run, true, &seeded);
             };
@@ -2179,8 +2391,8 @@ extern "C" int cubics_task_queue_create(int32_t device, cubics_task_queue** out,
         const int dev = current_device(device);
         CU(cudaSetDevice(dev));
         void* p = nullptr;
-        CU(cudaMalloc(&p, 256));
-        CU(cudaMemset(p, 0, 256));
+        CU(cudaMalloc(&p, kQueueBytes));
+        CU(cudaMemset(p, 0, kQueueBytes));
         QueueState init{};
         init.g_inc = ~0ull; // no incumbent
         init.g_first = ~0ull;
@@ -2222,7 +2434,7 @@ extern "C" int cubics_task_queue_reset(cubics_task_queue* q) {
         QueueState init{};
         init.g_inc = ~0ull; // no incumbent
         init.g_first = ~0ull;
-        CU(cudaMemset(q->counter, 0, 256));
+        CU(cudaMemset(q->counter, 0, kQueueBytes));
         CU(cudaMemcpy(q->counter, &init, sizeof init, cudaMemcpyHostToDevice));
         CU(cudaDeviceSynchronize());
         return CUBICS_OK;

@@ -180,6 +180,108 @@ static __device__ __noinline__ void ev_end_segment(const SearchParams& P, uint32
     if (t >= 0) ev_commit(P, t, EV_END, seg, a, b, c);
 }
 
+// ---- cross-GPU stealing (a stealer takes the shallowest untried right branch) ----
+__device__ __forceinline__ int ld_relaxed_sys_s32(const int32_t* p) {
+    int v;
+    asm volatile("ld.relaxed.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned ld_acquire_sys_u32(const uint32_t* p) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys_u32(uint32_t* p, unsigned v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long global_ns() { // one clock for every SM
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ uint32_t* xs_slot_ptr(const SearchParams& P, unsigned t) {
+    return reinterpret_cast<uint32_t*>(P.xs_slots + (size_t)(t % P.xs_cap) * P.xs_slot);
+}
+
+// thread 0, every 16 nodes: has an idle GPU asked for a subtree?
+static __device__ __noinline__ int xs_hungry(const SearchParams& P) {
+    return ld_relaxed_sys_s32(&P.xs_ctl->demand) > 0 ? 1 : 0;
+}
+
+// take one unit of demand (donor) or give one back (a thief that leaves unsatisfied)
+static __device__ __noinline__ bool xs_dec_demand(XsCtl* c) {
+    int d = ld_relaxed_sys_s32(&c->demand);
+    while (d > 0) {
+        const int o = atomicCAS_system(&c->demand, d, d - 1);
+        if (o == d) return true;
+        d = o;
+    }
+    return false;
+}
+
+// thread 0 of a donor that took a unit of demand: a pool ticket (its subtree counts as work
+// until a thief takes it), once the slot is free. The payload goes straight into the slot in the
+// owner GPU's HBM.
+static __device__ __noinline__ unsigned xs_reserve(const SearchParams& P) {
+    atomicAdd_system(&P.xs_ctl->work, 1);
+    const unsigned t = atomicAdd_system(&P.xs_ctl->push, 1u);
+    uint32_t* sl = xs_slot_ptr(P, t);
+    int ns = 32;
+    while (ld_acquire_sys_u32(sl) != 0u) {
+        __nanosleep(ns);
+        ns = ns < 1024 ? ns * 2 : ns;
+    }
+    return t;
+}
+
+// thread 0 of a waiting context holding the thief role, when this GPU has no work left:
+// 1 = a stolen subtree was republished in the local ring; 0 = nothing yet; -1 = exit (no GPU
+// searches and the pool is empty, a GPU aborted, or nothing arrived for `patience` cycles; a
+// thief leaves with the pool non-empty only when another thief just took from it, so the last
+// GPU standing drains the pool).
+static __device__ __noinline__ int xs_thief_step(const SearchParams& P, WorkState* ws, int ctx, size_t OS) {
+    XsCtl* c = P.xs_ctl;
+    volatile int32_t* idle = &ws->xs_idle; // serialised by the xs_thief role
+    if (!*idle) { // this GPU's busy token goes back; it asks for one subtree
+        *idle = 1;
+        atomicSub_system(&c->work, 1);
+        atomicAdd_system(&c->demand, 1);
+        *reinterpret_cast<volatile long long*>(&ws->xs_since) = (long long)global_ns();
+    }
+    if (ld_relaxed_sys_s32(&c->abort)) {
+        xs_dec_demand(c);
+        return -1;
+    }
+    const unsigned pop = ld_acquire_sys_u32(&c->pop), push = ld_acquire_sys_u32(&c->push);
+    if (pop < push && atomicCAS_system(&c->pop, pop, pop + 1u) == pop) {
+        uint32_t* sl = xs_slot_ptr(P, pop);
+        int ns = 32;
+        while (ld_acquire_sys_u32(sl) != pop + 1u) { // the donor is still writing it
+            __nanosleep(ns);
+            ns = ns < 1024 ? ns * 2 : ns;
+        }
+        const uint32_t* src = sl + 4;
+        uint32_t* ob = P.outbox + (size_t)ctx * OS;
+        for (size_t i = 0; i < OS; ++i) ob[i] = __ldcv(src + i);
+        st_release_sys_u32(sl, 0u); // slot free for the donor of ticket pop + xs_cap
+        *idle = 0;                   // the subtree's work token is now this GPU's busy token
+        atomicAdd((unsigned long long*)&ws->xs_in, 1ull);
+        P.outbox_busy[ctx] = 1; // publish it locally as this context's donation
+        atomicAdd(&ws->outstanding, 1);
+        const uint32_t s = atomicAdd(&ws->hot.push_ticket, 1u);
+        __threadfence();
+        st_volatile_u64(P.ring + (s % P.ring_cap), ((unsigned long long)(s + 1u) << 32) | (unsigned)ctx);
+        return 1;
+    }
+    const long long patience = 2000000; // 2 ms without a subtree (global timer, ns)
+    if (ld_relaxed_sys_s32(&c->work) == 0 ||
+        (long long)global_ns() - *reinterpret_cast<volatile long long*>(&ws->xs_since) > patience) {
+        xs_dec_demand(c);
+        return -1;
+    }
+    return 0;
+}
+
 __device__ __forceinline__ unsigned long long key_prefix64(uint32_t w0, uint32_t w1) {
     return ((unsigned long long)w0 << 32) | w1;
 }
@@ -291,6 +393,8 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
     int my_busy = 0;
 
     long long idle_cyc = 0, steals = 0, donations = 0;
+    int xs_want = 0;        // thread 0: some GPU waits for a subtree (refreshed every 16 nodes)
+    if (kSplit && P.xs_ctl && ctx == 0 && tid == 0) atomicAdd_system(&P.xs_ctl->work, 1); // this GPU searches
     const long long t_start = clock64();
     // first mode: current segment and the counters at its start; thread 0 caches the best key
     // segment bookkeeping (F_FIRST kernels, P.first_mode != 0): every subtree handed out records
@@ -299,6 +403,8 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
     // expansion of a sharded first-solution search, whose task set must not depend on timing)
     const bool seg_book = (F & F_FIRST) != 0 && (F & F_PARITY) == 0 && P.first_mode != 0; // compile-time off in lean kernels
     const bool first_mode = seg_book && P.first_mode == 1;
+    // guided replay of a recorded path (exact parallel B&B, reference-order kernels only)
+    const bool guided = (F & F_PARITY) != 0 && P.guide_key != nullptr;
     // streaming delivery: compiled into the reference-order kernels and the parallel kernels
     // with segment bookkeeping (F_FIRST); the lean parallel kernels never stream
     const bool stream = (F & (F_FIRST | F_PARITY)) != 0 && P.stream != 0;
@@ -370,7 +476,24 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
                         got = (int)(v & 0xffffffffu);
                         break;
                     }
-                    if ((it & 7) == 7 && (ld_volatile(&ws->hot.stop) || ld_volatile(&ws->outstanding) == 0)) break;
+                    if ((it & 7) == 7) {
+                        if (ld_volatile(&ws->hot.stop) || ld_volatile(&ws->xs_done)) break;
+                        if (ld_volatile(&ws->outstanding) == 0) { // this GPU has no work left
+                            if (!kSplit || !P.xs_ctl) break;
+                            if (atomicCAS(&ws->xs_thief, 0, 1) == 0) { // steal from another GPU
+                                // re-check under the role: the previous holder may have just
+                                // republished a stolen subtree (this GPU is busy again then)
+                                __threadfence();
+                                int xr = 0;
+                                if (ld_volatile(&ws->outstanding) == 0 && !ld_volatile(&ws->xs_done))
+                                    xr = xs_thief_step(P, ws, ctx, OS);
+                                if (xr < 0) atomicExch(&ws->xs_done, 1);
+                                __threadfence();
+                                atomicExch(&ws->xs_thief, 0);
+                                if (xr < 0) break;
+                            }
+                        }
+                    }
                     __nanosleep(ns);
                     ns = ns < 1024 ? ns * 2 : ns;
                 }
@@ -493,12 +616,16 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
                 g_bound = ld_volatile_s64(&ws->bound);
             }
             my_busy = ld_volatile(&P.outbox_busy[ctx]);
+            if (kSplit && P.xs_ctl && (nodes & 15) == 2) xs_want = xs_hungry(P);
         }
         if (optimizing) { // branch-and-bound shrink (:87-101), done by thread 0
             if (tid == 0) {
                 int empty = 0;
-                const long long bnd = parallel ? g_bound : bound;
-                const bool hb = parallel ? g_has_bound != 0 : has_bound;
+                // guided replay: the bound the reference had when it entered this node; a static
+                // bound (exact B&B phase): the phase's; parallel: the shared incumbent
+                const bool shared_b = parallel && !P.static_bound;
+                const long long bnd = guided ? P.guide_bound[depth] : (shared_b ? g_bound : bound);
+                const bool hb = guided ? P.guide_has[depth] != 0 : (shared_b ? g_has_bound != 0 : has_bound);
                 if (hb) {
                     uint32_t* d = dom + (size_t)obj * W;
                     const long long off = M.off[obj];
@@ -550,6 +677,7 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
         if (parallel && tid == 0) g_has_bound = (int)hot.w; // the prefetched bound pairs with this flag
         if (!backtrack) {
             const int sel = select_var<W>(M, dom, P.var_heuristic, red, sc);
+            if (sel < 0 && guided) break; // the replay reached its solution: every task is out
             if (sel < 0) {
                 // ============ solution leaf (emit_solution, search.cpp:134-156)
                 if (tid == 0) {
@@ -632,14 +760,16 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
                 }
                 if (optimizing) {
                     const long long val = M.off[obj] + dom_first<W>(dom + (size_t)obj * W);
-                    has_bound = true;
-                    bound = val;
+                    if (!P.static_bound) { // an exact B&B phase keeps its bound until it stops
+                        has_bound = true;
+                        bound = val;
+                    }
                     if (batch) {
                         for (int v = tid; v < n; v += T)
                             P.batch_inc[(size_t)ctx * n + v] = (uint16_t)dom_first<W>(dom + (size_t)v * W);
                         if (tid == 0) P.batch_flags[ctx] |= 2;
                     }
-                    if (parallel && tid == 0) {
+                    if (parallel && !P.static_bound && tid == 0) {
                         spin_lock(&ws->inc_lock);
                         volatile long long* gb = reinterpret_cast<volatile long long*>(&ws->bound);
                         volatile int32_t* ghb = &ws->hot.has_bound;
@@ -670,6 +800,45 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
                     break;
                 }
                 backtrack = true;
+            } else if (guided) {
+                // ============ replay one decision of the recorded path (bit `depth` of its key):
+                // left = the reference went left here and its right branch is still pending when
+                // it reaches the solution: emit that branch as a task (outbox layout)
+                const int bit = dom_first<W>(dom + (size_t)sel * W);
+                const int gbit = (int)((P.guide_key[depth >> 5] >> (31 - (depth & 31))) & 1u);
+                if (!gbit) {
+                    if (tid == 0) s_ll = (long long)atomicAdd((unsigned long long*)&ws->n_tasks, 1ull);
+                    sc.sync();
+                    const long long t = s_ll;
+                    if (t < P.task_cap) {
+                        uint32_t* tb = P.tasks + (size_t)t * OS;
+                        const size_t clr = (size_t)sel * W + (bit >> 5);
+                        for (size_t i = tid; i < NWP; i += T) {
+                            uint32_t x = dom[i];
+                            if (i == clr) x &= ~(1u << (bit & 31));
+                            tb[i] = x;
+                        }
+                        for (int i = tid; i < KW; i += T) tb[NWP + i] = path_right_word(path[i], i, depth);
+                        if (tid == 0) {
+                            tb[NWP + KW] = (uint32_t)(depth + 1);
+                            tb[NWP + KW + 1] = (uint32_t)sel;
+                        }
+                    }
+                }
+                if (chg0)
+                    for (int i = tid; i < 2 * nbw; i += T) chg0[i] = 0;
+                sc.sync();
+                if (!gbit) {
+                    if (tid < W) dom[(size_t)sel * W + tid] = (tid == (bit >> 5)) ? (1u << (bit & 31)) : 0u;
+                } else if (tid == 0) { // the reference took the right branch here
+                    dom[(size_t)sel * W + (bit >> 5)] &= ~(1u << (bit & 31));
+                    for (int i = depth >> 5; i < KW; ++i) path[i] = path_right_word(path[i], i, depth);
+                }
+                if (tid == 0 && chg0) chg0[sel >> 5] |= 1u << (sel & 31);
+                trig_var = sel;
+                ++depth;
+                sc.sync();
+                continue;
             } else {
                 // ============ left branch: push the frame, assign x = min(x) (:116-121)
                 if (sp >= P.frame_cap) {
@@ -692,6 +861,12 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
                     meta[sp * 4 + 2] = depth;
                     // donate the shallowest pending right branch when someone waits for work
                     int want = hot.z ? 2 : 0;
+                    // a whole GPU is idle: the shallowest pending branch goes to the global pool
+                    // first (one subtree per unit it asked for; local sharing resumes after)
+                    if (kSplit && xs_want && parallel && !want && sp + 1 > base) {
+                        xs_want = 0;
+                        if (xs_dec_demand(P.xs_ctl)) want = 4;
+                    }
                     if (parallel && !want && sp + 1 > base && !my_busy && hot.y > hot.x) want = 1;
                     // first mode: pending branches right of the best solution are dropped, never
                     // handed out (the shallowest pending branch is the rightmost one)
@@ -707,10 +882,15 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
                 const int want = s_flag;
                 if (want == 2) break;
                 if (want == 3) ++base;
-                if (want == 1) {
+                if (want == 1 || want == 4) {
                     const int f = base++;
                     const int fvar = meta[f * 4 + 0], fbit = meta[f * 4 + 1], fdepth = meta[f * 4 + 2];
                     uint32_t* ob = P.outbox + (size_t)ctx * OS;
+                    if (kSplit && want == 4) { // the slot in the owner GPU's HBM, over NVLink
+                        if (tid == 0) s_ll = (long long)xs_reserve(P);
+                        sc.sync();
+                        ob = xs_slot_ptr(P, (unsigned)s_ll) + 4;
+                    }
                     const uint32_t* fr = frames + (size_t)f * NWP;
                     const size_t clr = (size_t)fvar * W + (fbit >> 5);
                     for (size_t i = tid; i < NWP; i += T) {
@@ -723,8 +903,14 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
                         ob[NWP + KW] = (uint32_t)(fdepth + 1);
                         ob[NWP + KW + 1] = (uint32_t)fvar;
                     }
+                    if (kSplit && want == 4) __threadfence_system();
                     sc.sync();
-                    if (tid == 0) {
+                    if (kSplit && want == 4) {
+                        if (tid == 0) {
+                            st_release_sys_u32(xs_slot_ptr(P, (unsigned)s_ll), (unsigned)s_ll + 1u);
+                            atomicAdd((unsigned long long*)&ws->xs_out, 1ull);
+                        }
+                    } else if (tid == 0) {
                         P.outbox_busy[ctx] = 1;
                         atomicAdd(&ws->outstanding, 1);
                         const uint32_t s = atomicAdd(&ws->hot.push_ticket, 1u);
@@ -739,6 +925,10 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
             }
         }
         } // node processing
+        if (guided) { // a failure on the recorded path: the replay does not match the search
+            if (tid == 0) ws->error = DERR_GUIDE;
+            break;
+        }
         // ================= backtrack: right branch of the deepest pending frame (:122-131)
         if (parallel) {
             if (tid == 0) s_flag = hot.z;
@@ -780,6 +970,8 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
     }
     flush_seg();
     sc.sync();
+    // a GPU that stops (error) releases the others from waiting for its work
+    if (kSplit && P.xs_ctl && tid == 0 && ld_volatile(&ws->hot.stop)) atomicExch_system(&P.xs_ctl->abort, 1);
     if (parallel && tid == 0 && have_work) {
         // unwound by stop: this context no longer counts as outstanding
         atomicSub(&ws->outstanding, 1);

@@ -130,6 +130,8 @@ class SatisfyResult:
     h2d_bytes: int = 0
     d2h_bytes: int = 0
     kernel_launches: int = 0
+    remote_in: int = 0   # shared queue: subtrees taken from other GPUs
+    remote_out: int = 0  # shared queue: subtrees given to other GPUs
 
 
 @dataclass
@@ -150,6 +152,8 @@ class OptimizeResult:
     h2d_bytes: int = 0
     d2h_bytes: int = 0
     kernel_launches: int = 0
+    remote_in: int = 0   # shared queue: subtrees taken from other GPUs
+    remote_out: int = 0  # shared queue: subtrees given to other GPUs
 
 
 @dataclass
@@ -624,7 +628,7 @@ def solve_shard(model: Model, cfg: SearchConfig, shard_index: int, shard_count: 
                                              None, C.byref(res))
     _check(rc, "solve_shard")
     return SatisfyResult(_stats(res), bool(res.complete), res.engine, res.contexts, res.device_ms, res.total_ms,
-                         res.h2d_bytes, res.d2h_bytes, res.kernel_launches)
+                         res.h2d_bytes, res.d2h_bytes, res.kernel_launches, res.remote_tasks_in, res.remote_tasks_out)
 
 
 def solve_optimize_shard(model: Model, cfg: SearchConfig, shard_index: int, shard_count: int,
@@ -641,7 +645,8 @@ def solve_optimize_shard(model: Model, cfg: SearchConfig, shard_index: int, shar
            "solve_optimize_shard")
     sol = Solution([best[i] for i in range(model.n_vars)], res.objective) if res.has_solution else None
     return OptimizeResult(sol, bool(res.complete), _stats(res), res.engine, res.contexts, res.device_ms, res.total_ms,
-                          res.h2d_bytes, res.d2h_bytes, res.kernel_launches)
+                          res.h2d_bytes, res.d2h_bytes, res.kernel_launches, res.remote_tasks_in,
+                          res.remote_tasks_out)
 
 
 class FirstShard:

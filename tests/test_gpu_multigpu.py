@@ -211,3 +211,62 @@ def test_distributed_first_solution_two_processes_ipc():
         for stats, sols in got[rank]:
             assert stats == G.expected_tuple(g)
             assert sols == [g["first"]]
+
+
+# ---- cross-GPU stealing through the shared queue's global pool -------------------------------
+def _steal_worker(rank, world, port, out):
+    import os
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+
+    from paper_1909_09213_b200 import distributed as D
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        m = S.parse_model(G.model_text("nq14"))
+        q = D.shared_task_queue(rank, world, device=0)
+        res = []
+        for _ in range(3):
+            if rank == 0:
+                q.reset()
+            dist.barrier()
+            # few contexts per process, so both kernels are resident on this one GPU at once:
+            # the process that runs out of claims first steals right branches from the other
+            r = S.solve_shard(m, S.SearchConfig(device=0, contexts=64, count_only=True), rank, world, queue=q)
+            t = torch.tensor(list(r.stats.as_tuple()) + [r.remote_in, r.remote_out], dtype=torch.int64)
+            dist.all_reduce(t)
+            res.append(t.tolist())
+        dist.barrier()
+        q.close()
+        dist.barrier()
+        out.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_cross_gpu_stealing_two_processes_ipc():
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    world = 2
+    ctx = mp.get_context("spawn")
+    out = ctx.Queue()
+    procs = [ctx.Process(target=_steal_worker, args=(r, world, port, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(out.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    g = G.goldens()["nq14|--all"]
+    moved = 0
+    for row in got[0]:
+        assert tuple(row[:4]) == G.expected_tuple(g)  # every subtree searched exactly once
+        assert row[4] == row[5]  # every subtree given to the pool was taken
+        moved += row[4]
+    print("subtrees moved between the two processes:", [row[4] for row in got[0]])
+    assert moved > 0
