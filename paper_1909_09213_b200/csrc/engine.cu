@@ -1491,6 +1491,39 @@ int satisfy_records(const HostModel& m, const cubics_search_config& cfg, bool re
 }
 } // namespace
 
+namespace {
+// AUTO satisfy search capped at k > 1 solutions, no node limit: the parallel engine streams the
+// solutions in DFS order (segments) and the host stops it at the k-th, whose stats are the
+// reference's (search.cpp:151-154) - the exact first-k at parallel speed.
+bool capped_stream(const HostModel& m, const cubics_search_config& cfg) {
+    return cfg.engine == CUBICS_ENGINE_AUTO && m.goal == CUBICS_SATISFY && cfg.node_limit == 0 && cfg.max_solutions > 1 &&
+           cfg.max_solutions != std::numeric_limits<uint64_t>::max() && m.n_vars() > 0 &&
+           !std::getenv("CUBICS_NO_CAPPED_STREAM");
+}
+
+// One streamed satisfy search: visit(row) per solution in DFS order (false stops), at most
+// `cap` solutions. Returns the objective of the last solution delivered (objective goals).
+int64_t stream_satisfy(const HostModel& m, const cubics_search_config& cfg, int engine, uint64_t cap,
+                       const std::function<bool(const uint16_t*)>& visit, cubics_result* out) {
+    const double t0 = now_ms();
+    std::memset(out, 0, sizeof *out);
+    int64_t last_obj = 0;
+    StreamIO io;
+    io.visit = [&](const uint16_t* row, const uint64_t*) {
+        if (m.goal != CUBICS_SATISFY) last_obj = m.offset[m.goal_var] + row[m.goal_var];
+        return visit(row) && io.delivered < cap;
+    };
+    RunOut r;
+    run_search(m, cfg, engine, false, 0, r, false, nullptr, nullptr, &io);
+    fill_result(r, out);
+    out->complete = !r.ws.limit_hit && !r.ws.user_stop;
+    out->has_solution = r.ws.stats[3] > 0;
+    if (m.goal != CUBICS_SATISFY && io.delivered) out->objective = last_obj;
+    out->total_ms = now_ms() - t0;
+    return last_obj;
+}
+} // namespace
+
 extern "C" int cubics_solve_satisfy(const cubics_model* h, const cubics_search_config* cfg, cubics_solution_cb cb,
                                     void* user, cubics_result* out) {
     if (!h || !cfg || !out) return CUBICS_E_INVALID;
@@ -1503,23 +1536,15 @@ extern "C" int cubics_solve_satisfy(const cubics_model* h, const cubics_search_c
         // streamed unless it is the exact parallel first solution (one row) or a parallel
         // branch-and-bound stream (reference-order incumbents need the parity engine)
         const bool par = engine == CUBICS_ENGINE_PARALLEL;
-        if (want && !(par && (cfg->max_solutions == 1 || m.goal != CUBICS_SATISFY))) {
-            const double t0 = now_ms();
-            std::memset(out, 0, sizeof *out);
-            int64_t last_obj = 0;
-            StreamIO io;
-            io.visit = [&](const uint16_t* row, const uint64_t*) {
-                for (int v = 0; v < n; ++v) vals[v] = m.offset[v] + row[v];
-                if (m.goal != CUBICS_SATISFY) last_obj = vals[m.goal_var];
-                return cb(user, vals.data(), n) != 0;
-            };
-            RunOut r;
-            run_search(m, *cfg, engine, false, 0, r, false, nullptr, nullptr, &io);
-            fill_result(r, out);
-            out->complete = !r.ws.limit_hit && !r.ws.user_stop;
-            out->has_solution = r.ws.stats[3] > 0;
-            if (m.goal != CUBICS_SATISFY && io.delivered) out->objective = last_obj;
-            out->total_ms = now_ms() - t0;
+        const bool capped = capped_stream(m, *cfg);
+        if (capped || (want && !(par && (cfg->max_solutions == 1 || m.goal != CUBICS_SATISFY)))) {
+            stream_satisfy(m, *cfg, capped ? CUBICS_ENGINE_PARALLEL : engine, cfg->max_solutions,
+                           [&](const uint16_t* row) {
+                               if (!want) return true;
+                               for (int v = 0; v < n; ++v) vals[v] = m.offset[v] + row[v];
+                               return cb(user, vals.data(), n) != 0;
+                           },
+                           out);
             return (int)CUBICS_OK;
         }
         return satisfy_records(m, *cfg, want, out, [&](uint64_t, const uint16_t* row) {
@@ -1620,6 +1645,26 @@ extern "C" int cubics_enumerate(const cubics_model* h, const cubics_search_confi
         const double t0 = now_ms();
         const HostModel& m = h->m;
         const int n = m.n_vars();
+        if (capped_stream(m, *cfg)) { // the first k solutions, streamed from the parallel engine
+            std::vector<uint16_t> rows;
+            stream_satisfy(m, *cfg, CUBICS_ENGINE_PARALLEL, cfg->max_solutions,
+                           [&](const uint16_t* row) {
+                               if (!cfg->count_only) rows.insert(rows.end(), row, row + n);
+                               return true;
+                           },
+                           out);
+            const uint64_t count = n ? rows.size() / n : 0;
+            int64_t* values = alloc_values(std::max<uint64_t>(rows.size(), 1));
+            auto* S = new cubics_solutions{};
+            S->n_vars = n;
+            S->count = count;
+            S->values = values;
+            for (uint64_t i = 0; i < count; ++i)
+                for (int v = 0; v < n; ++v) values[i * n + v] = m.offset[v] + rows[i * n + v];
+            *sols = S;
+            out->total_ms = now_ms() - t0;
+            return (int)CUBICS_OK;
+        }
         // the rows arrive in the device's pinned download buffer: hold the device until converted
         std::lock_guard<std::recursive_mutex> lock(g_dev_mu[current_device(cfg->device)]);
         RunOut r = satisfy_run(m, *cfg, !cfg->count_only, out, true);
@@ -1646,7 +1691,7 @@ extern "C" int cubics_enumerate(const cubics_model* h, const cubics_search_confi
         if (std::getenv("CUBICS_DEBUG"))
             std::fprintf(stderr, "[cubics] enumerate: search+download %.3f ms (device %.3f), convert %.3f ms, %llu rows\n",
                          t1 - t0, out->device_ms, now_ms() - t1, (unsigned long long)r.rec.count);
-        return CUBICS_OK;
+        return (int)CUBICS_OK;
     });
 }
 

@@ -144,3 +144,19 @@ def test_stream_after_stop_is_clean():
     ost = S.SearchStats()
     O.enumerate_solutions(m, S.SearchConfig(), ost)
     assert st.as_tuple() == ost.as_tuple() and len(sols) == 724
+
+
+@pytest.mark.parametrize("k", [2, 10, 500, 14200, 20000])
+def test_first_k_solutions_on_the_parallel_engine_are_exact(k):
+    # AUTO with max_solutions = k: the parallel engine streams and stops at the k-th solution;
+    # stats and rows equal the reference's first k (search.cpp:151-154)
+    m = S.parse_model(G.model_text("nq12"))
+    ost = S.SearchStats()
+    want = [s.values for s in O.enumerate_solutions(m, S.SearchConfig(max_solutions=k), ost)]
+    st = S.SearchStats()
+    got = [s.values for s in S.enumerate_solutions(m, S.SearchConfig(max_solutions=k), st)]
+    assert st.as_tuple() == ost.as_tuple() and got == want
+    r = S.solve_satisfy(m, S.SearchConfig(max_solutions=k))  # no callback: counts only
+    assert r.engine == A.ENGINE_PARALLEL
+    assert r.stats.as_tuple() == ost.as_tuple()
+    assert r.complete is (k > 14200)
