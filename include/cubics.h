@@ -19,9 +19,12 @@
  *                                                       include/fd/propagation.hpp:78-89
  *   cubics_model_parse         fd::parse_model          include/fd/parser.hpp:38 (host-side loader)
  *   cubics_model_validate      fd::model_validate       include/fd/model.hpp:93
+ *   cubics_enumerate           fd::enumerate_solutions  include/fd/search.hpp:65-66 (one host array)
  *   cubics_solve_shard         (new) one rank's share of a multi-GPU search; SURVEY.md 8(e)
  *   cubics_solve_shard_shared  (new) the same, subtrees claimed dynamically from a shared
- *   cubics_task_queue_*              queue over NVLink peer memory; SURVEY.md 8(e)
+ *   cubics_task_queue_*              queue over NVLink peer memory, with cross-GPU stealing
+ *   cubics_solve_optimize_shard (new) multi-GPU branch and bound, incumbent shared over NVLink
+ *   cubics_solve_first_shard   (new) multi-GPU exact first solution (two-phase merge)
  *
  * Threading: every call is synchronous and blocks until the device finishes. Calls on
  * different models may run from different host threads. Error details for the last failing
@@ -186,6 +189,9 @@ typedef struct cubics_result {
  * The callback must not start another search on the same device (CUBICS_E_INVALID). */
 typedef int32_t (*cubics_solution_cb)(void* user, const int64_t* values, int32_t n_vars);
 
+/* AUTO engine: complete enumerations and first-k searches (max_solutions = k, no node limit)
+ * run on the parallel engine; the first k are streamed in DFS order and the search stops at the
+ * k-th with the reference's stats. */
 int cubics_solve_satisfy(const cubics_model* m, const cubics_search_config* cfg,
                          cubics_solution_cb cb, void* user, cubics_result* out);
 
@@ -201,7 +207,12 @@ int cubics_enumerate(const cubics_model* m, const cubics_search_config* cfg, cub
                      cubics_result* out);
 void cubics_solutions_free(cubics_solutions* s);
 
-/* best_values (n_vars entries, may be NULL) receives the optimal / last incumbent. */
+/* best_values (n_vars entries, may be NULL) receives the optimal / last incumbent.
+ * AUTO without node_limit / max_solutions: the exact parallel branch and bound - a chain of
+ * static-bound exact-first searches, each seeded by a replay of the previous incumbent's path -
+ * whose stats and incumbents are the reference's (search.cpp:87-101, 187-201). Otherwise, or
+ * with CUBICS_ENGINE_PARITY, one reference-order search context; CUBICS_ENGINE_PARALLEL: a
+ * shared-bound parallel B&B (exact optimum, schedule-dependent node count). */
 int cubics_solve_optimize(const cubics_model* m, const cubics_search_config* cfg,
                           int64_t* best_values, cubics_result* out);
 
@@ -236,7 +247,11 @@ int cubics_solve_shard(const cubics_model* m, const cubics_search_config* cfg,
  * idle search context claims the next one with a system-scope atomicAdd on the counter over
  * NVLink; once the counter passes the task count the contexts fall back to the in-GPU
  * work-sharing ring. Each subtree is searched exactly once across the ranks, so stats sum
- * exactly as for cubics_solve_shard. The counter must be reset (cubics_task_queue_reset on the
+ * exactly as for cubics_solve_shard. Once the counter drains, a GPU whose contexts are all idle
+ * steals: it posts a demand in the queue state, busy contexts on the other GPUs write their
+ * shallowest pending right branch into a global pool there (one per demand), and the idle GPU
+ * republishes it in its own work-sharing ring; remote_tasks_in / _out count them. A GPU exits
+ * when no GPU searches and the pool is empty. The counter must be reset (cubics_task_queue_reset on the
  * owner, then a barrier) before every search that uses it. A queue opened in the creating
  * process is not supported by CUDA IPC: pass the creator's queue to every local call instead;
  * a call on another device of that process enables peer access to the owner's GPU first

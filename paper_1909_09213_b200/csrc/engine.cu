@@ -890,7 +890,8 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
     const int feat = (P.nl ? 1 : 0) | (P.ntb + P.ntn ? 2 : 0) | (P.big_words ? 4 : 0) |
                      (seg_mode || sio ? 8 : 0) |
                      (P.lin_g > 1 ? dev::F_LONG : 0) |
-                     (hm.goal == CUBICS_SATISFY && !shard ? dev::F_NOOPT | dev::F_NOSPLIT : 0);
+                     (hm.goal == CUBICS_SATISFY ? dev::F_NOOPT : 0) | (!shard ? dev::F_NOSPLIT : 0) |
+                     (shard && shard->split_depth > 0 ? dev::F_FRONTIER : 0);
     int n_ctx = batch ? batch->count : 1;
     if (parallel) {
         int per_sm = 0;

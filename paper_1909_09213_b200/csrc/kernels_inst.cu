@@ -34,7 +34,7 @@ static size_t g_propgrid_smem = 48 * 1024;
 using SearchFn = void (*)(const SearchParams);
 
 static SearchFn pick_search(int feat) {
-    feat &= ~(dev::F_NOOPT | dev::F_NOSPLIT); // lean bits select warp kernels only
+    feat &= ~(dev::F_NOOPT | dev::F_NOSPLIT | dev::F_FRONTIER); // lean bits select warp kernels only
     if constexpr (CUBICS_W <= 4) {
         if (feat == 0) return dev::search_kernel<CUBICS_W, 0>;
         if (feat == dev::F_LINEAR) return dev::search_kernel<CUBICS_W, dev::F_LINEAR>;
@@ -52,12 +52,20 @@ static SearchFn pick_warp(int feat, bool parity) {
     if (parity) return lin ? search_kernel_warp<F_PARITY | F_LINEAR> : search_kernel_warp<F_PARITY>;
     if (first) return lin ? search_kernel_warp<F_LINEAR | F_FIRST | L> : search_kernel_warp<F_FIRST | L>;
     if (lean) return lin ? search_kernel_warp<F_LINEAR | L> : search_kernel_warp<L>;
+    // the frontier expansion of a sharded search (always a satisfy goal: B&B expands without it)
+    if (feat & F_FRONTIER)
+        return lin ? search_kernel_warp<F_LINEAR | F_NOOPT | F_FRONTIER> : search_kernel_warp<F_NOOPT | F_FRONTIER>;
+    // seeded sharded satisfy searches: shared-queue claims, cross-GPU stealing; no B&B
+    if (feat & F_NOOPT) return lin ? search_kernel_warp<F_LINEAR | F_NOOPT> : search_kernel_warp<F_NOOPT>;
     return lin ? search_kernel_warp<F_LINEAR> : search_kernel_warp<0>;
 }
-static size_t g_warp_smem[8] = {48 * 1024, 48 * 1024, 48 * 1024, 48 * 1024, 48 * 1024, 48 * 1024, 48 * 1024, 48 * 1024};
+static size_t g_warp_smem[12] = {48 * 1024, 48 * 1024, 48 * 1024, 48 * 1024, 48 * 1024, 48 * 1024,
+                                  48 * 1024, 48 * 1024, 48 * 1024, 48 * 1024, 48 * 1024, 48 * 1024};
 static int warp_slot(int feat, bool parity) {
     const bool lean = (feat & (dev::F_NOOPT | dev::F_NOSPLIT)) == (dev::F_NOOPT | dev::F_NOSPLIT);
     if (parity) return 6 | ((feat & dev::F_LINEAR) ? 1 : 0);
+    if (!lean && !(feat & dev::F_FIRST) && (feat & dev::F_FRONTIER)) return 10 | ((feat & dev::F_LINEAR) ? 1 : 0);
+    if (!lean && !(feat & dev::F_FIRST) && (feat & dev::F_NOOPT)) return 8 | ((feat & dev::F_LINEAR) ? 1 : 0);
     return ((feat & dev::F_LINEAR) ? 1 : 0) | ((feat & dev::F_FIRST) ? 2 : (lean ? 4 : 0));
 }
 
@@ -86,7 +94,7 @@ cudaError_t launch_search<CUBICS_W>(const SearchParams& P, int feat, int grid, i
     if (P.mode == MODE_PARITY && block <= 512) return launch_search_parity<CUBICS_W>(P, grid, block, smem, st);
     if (P.batch) return cudaErrorInvalidConfiguration; // batched B&B runs in the parity kernel only
     SearchFn k = pick_search(feat);
-    feat &= ~(dev::F_NOOPT | dev::F_NOSPLIT);
+    feat &= ~(dev::F_NOOPT | dev::F_NOSPLIT | dev::F_FRONTIER);
     cudaError_t e = grant_smem(k, smem, feat == 0 ? g_search_smem0 : (feat == dev::F_LINEAR ? g_search_smem1 : g_search_smem));
     if (e != cudaSuccess) return e;
     k<<<grid, block, smem, st>>>(P);
@@ -96,7 +104,7 @@ cudaError_t launch_search<CUBICS_W>(const SearchParams& P, int feat, int grid, i
 template <>
 cudaError_t occupancy_search<CUBICS_W>(int feat, int block, size_t smem, int* out) {
     SearchFn k = pick_search(feat);
-    feat &= ~(dev::F_NOOPT | dev::F_NOSPLIT);
+    feat &= ~(dev::F_NOOPT | dev::F_NOSPLIT | dev::F_FRONTIER);
     cudaError_t e = grant_smem(k, smem, feat == 0 ? g_search_smem0 : (feat == dev::F_LINEAR ? g_search_smem1 : g_search_smem));
     if (e != cudaSuccess) return e;
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, k, block, smem);

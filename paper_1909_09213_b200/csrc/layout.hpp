@@ -21,11 +21,13 @@ namespace dev {
 // F_REGS marks the 128-register parity kernel: register-hungry fast paths are compiled in only
 // there (in the 64-register kernels they cost more in spills than they save).
 // F_LONG: linear sums of more than 4 terms (lane-group form); lean kernels compile it out.
-// F_NOOPT / F_NOSPLIT (lean warp kernels): branch-and-bound, and the frontier expansion and
-// shared-queue claims of sharded runs, are compiled out.
+// F_NOOPT / F_NOSPLIT (lean warp kernels): branch-and-bound, and the shared-queue claims and
+// cross-GPU stealing of sharded runs, are compiled out. F_FRONTIER: the frontier expansion of a
+// sharded run (warp kernels compile it only into the instantiations that run the expansion; it
+// costs the seeded search ~15% per node on nq14).
 enum Feature : int {
     F_LINEAR = 1, F_TABLE = 2, F_BIGAD = 4, F_FIRST = 8, F_LONG = 64, F_ALL = 15 | 64, F_PARITY = 16, F_REGS = 32,
-    F_NOOPT = 128, F_NOSPLIT = 256
+    F_NOOPT = 128, F_NOSPLIT = 256, F_FRONTIER = 512
 };
 
 

@@ -22,6 +22,8 @@ struct Ctl {
     uint4 hot; // warp contexts: the prefetched HotState (cp.async target)
     int err, min, flag, src;
     long long ll;
+    int xs_want, pad; // thread 0: some GPU asked for a subtree (cross-GPU stealing)
+    uint4 xs;         // warp contexts: {push, pop, work, demand} of the pool, prefetched by cp.async
     unsigned red[32];
 };
 

@@ -203,11 +203,6 @@ __device__ __forceinline__ uint32_t* xs_slot_ptr(const SearchParams& P, unsigned
     return reinterpret_cast<uint32_t*>(P.xs_slots + (size_t)(t % P.xs_cap) * P.xs_slot);
 }
 
-// thread 0, every 16 nodes: has an idle GPU asked for a subtree?
-static __device__ __noinline__ int xs_hungry(const SearchParams& P) {
-    return ld_relaxed_sys_s32(&P.xs_ctl->demand) > 0 ? 1 : 0;
-}
-
 // take one unit of demand (donor) or give one back (a thief that leaves unsatisfied)
 static __device__ __noinline__ bool xs_dec_demand(XsCtl* c) {
     int d = ld_relaxed_sys_s32(&c->demand);
@@ -219,10 +214,12 @@ static __device__ __noinline__ bool xs_dec_demand(XsCtl* c) {
     return false;
 }
 
-// thread 0 of a donor that took a unit of demand: a pool ticket (its subtree counts as work
-// until a thief takes it), once the slot is free. The payload goes straight into the slot in the
-// owner GPU's HBM.
-static __device__ __noinline__ unsigned xs_reserve(const SearchParams& P) {
+// thread 0 of a donor: take a unit of demand (-1: another donor was faster), then a pool ticket
+// (its subtree counts as work until a thief takes it), once the slot is free. The payload goes
+// straight into the slot in the owner GPU's HBM. One call site, on the donation path only, so the
+// search loop keeps its registers.
+static __device__ __noinline__ long long xs_reserve(const SearchParams& P) {
+    if (!xs_dec_demand(P.xs_ctl)) return -1;
     atomicAdd_system(&P.xs_ctl->work, 1);
     const unsigned t = atomicAdd_system(&P.xs_ctl->push, 1u);
     uint32_t* sl = xs_slot_ptr(P, t);
@@ -231,7 +228,7 @@ static __device__ __noinline__ unsigned xs_reserve(const SearchParams& P) {
         __nanosleep(ns);
         ns = ns < 1024 ? ns * 2 : ns;
     }
-    return t;
+    return (long long)t;
 }
 
 // thread 0 of a waiting context holding the thief role, when this GPU has no work left:
@@ -282,6 +279,54 @@ static __device__ __noinline__ int xs_thief_step(const SearchParams& P, WorkStat
     return 0;
 }
 
+// Thread 0 of an idle context in a sharded search: the next subtree (outbox index, or -1 when the
+// search is over). Shared queue first (a claiming context stays outstanding), then a ticket of the
+// in-GPU ring; when this GPU has no work left, one waiting context at a time is the thief of
+// cross-GPU stealing. Out of line: the sharded kernels' search loop keeps its registers (the lean
+// kernels inline their plain ticket wait).
+struct WaitOut {
+    int got;
+    int claim_open;
+    long long seg; // segment id of the subtree
+};
+static __device__ __noinline__ WaitOut wait_sharded(const SearchParams& P, WorkState* ws, int ctx, size_t OS,
+                                                    int claim_open, bool xs) {
+    int got = claim_open ? claim_task(P.task_claim, P.n_seed, P.n_ctx) : -1;
+    if (got >= 0) return WaitOut{got, 1, (long long)(got - P.n_ctx) + 1}; // claimed seed i: segment 1 + i
+    atomicSub(&ws->outstanding, 1);
+    const uint32_t t = atomicAdd(&ws->hot.pop_ticket, 1u);
+    const unsigned long long* slot = P.ring + (t % P.ring_cap);
+    int ns = 32;
+    for (int it = 0;; ++it) {
+        const unsigned long long v = ld_volatile_u64(slot);
+        if ((uint32_t)(v >> 32) == t + 1u) {
+            got = (int)(v & 0xffffffffu);
+            break;
+        }
+        if ((it & 7) == 7) {
+            if (ld_volatile(&ws->hot.stop) || ld_volatile(&ws->xs_done)) break;
+            if (ld_volatile(&ws->outstanding) == 0) { // this GPU has no work left
+                if (!xs || !P.xs_ctl) break;
+                if (atomicCAS(&ws->xs_thief, 0, 1) == 0) { // steal from another GPU
+                    // re-check under the role: the previous holder may have just republished a
+                    // stolen subtree (this GPU is busy again then)
+                    __threadfence();
+                    int xr = 0;
+                    if (ld_volatile(&ws->outstanding) == 0 && !ld_volatile(&ws->xs_done)) xr = xs_thief_step(P, ws, ctx, OS);
+                    if (xr < 0) atomicExch(&ws->xs_done, 1);
+                    __threadfence();
+                    atomicExch(&ws->xs_thief, 0);
+                    if (xr < 0) break;
+                }
+            }
+        }
+        __nanosleep(ns);
+        ns = ns < 1024 ? ns * 2 : ns;
+    }
+    if (got >= 0) __threadfence();
+    return WaitOut{got, 0, (long long)t + 1 + P.seg_base}; // the subtree published under ticket t
+}
+
 __device__ __forceinline__ unsigned long long key_prefix64(uint32_t w0, uint32_t w1) {
     return ((unsigned long long)w0 << 32) | w1;
 }
@@ -296,6 +341,38 @@ __device__ __forceinline__ uint32_t path_right_word(uint32_t word, int i, int d)
     uint32_t x = word & keep;
     if (c >= 0 && c < 32) x |= 0x80000000u >> c;
     return x;
+}
+
+// A busy context's shallowest pending right branch (frame fr, meta {var, bit, depth}) into the
+// global pool, all threads of the context; false when the demand was already taken. Out of line:
+// it runs once per subtree given away, and the search loop keeps its registers.
+template <int W, class SC>
+static __device__ __noinline__ bool xs_donate(const SearchParams& P, SC& sc, const uint32_t* fr, const int32_t* meta,
+                                              const uint32_t* path, int KW, size_t NWP, long long& s_ll, int tid, int T) {
+    if (tid == 0) s_ll = xs_reserve(P);
+    sc.sync();
+    const long long xt = s_ll;
+    if (xt < 0) return false;
+    const int fvar = meta[0], fbit = meta[1], fdepth = meta[2];
+    uint32_t* ob = xs_slot_ptr(P, (unsigned)xt) + 4;
+    const size_t clr = (size_t)fvar * W + (fbit >> 5);
+    for (size_t i = tid; i < NWP; i += T) {
+        uint32_t x = fr[i];
+        if (i == clr) x &= ~(1u << (fbit & 31));
+        ob[i] = x;
+    }
+    for (int i = tid; i < KW; i += T) ob[NWP + i] = path_right_word(path[i], i, fdepth);
+    if (tid == 0) {
+        ob[NWP + KW] = (uint32_t)(fdepth + 1);
+        ob[NWP + KW + 1] = (uint32_t)fvar;
+    }
+    __threadfence_system();
+    sc.sync();
+    if (tid == 0) {
+        st_release_sys_u32(xs_slot_ptr(P, (unsigned)xt), (unsigned)xt + 1u);
+        atomicAdd((unsigned long long*)&P.ws->xs_out, 1ull);
+    }
+    return true;
 }
 
 // block argmin of (size, id) over unbound vars; -1 when every domain is a singleton
@@ -377,6 +454,13 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
     const bool batch = (F & F_PARITY) != 0 && !SC::kWarp && P.batch != 0; // parity block kernels only
     // lean warp kernels compile out branch-and-bound and the frontier expansion / shared claims
     constexpr bool kOpt = (F & F_NOOPT) == 0, kSplit = (F & F_NOSPLIT) == 0;
+#ifdef CUBICS_XS_OFF
+    constexpr bool kXs = false; // A/B builds only
+#else
+    constexpr bool kXs = kSplit; // cross-GPU stealing rides on the sharded kernels
+#endif
+    // block kernels keep the frontier expansion; warp kernels only in F_FRONTIER instantiations
+    constexpr bool kFrontier = kSplit && (!SC::kWarp || (F & F_FRONTIER) != 0);
     bool has_bound = batch ? P.batch_has_bound[ctx] != 0 : P.has_init_bound != 0;
     long long bound = batch ? P.batch_bound[ctx] : P.init_bound;
     bool has_first = false;
@@ -393,8 +477,9 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
     int my_busy = 0;
 
     long long idle_cyc = 0, steals = 0, donations = 0;
-    int xs_want = 0;        // thread 0: some GPU waits for a subtree (refreshed every 16 nodes)
-    if (kSplit && P.xs_ctl && ctx == 0 && tid == 0) atomicAdd_system(&P.xs_ctl->work, 1); // this GPU searches
+    int& xs_want = C.xs_want; // thread 0: some GPU waits for a subtree (refreshed every 16 nodes)
+    if (tid == 0) xs_want = 0;
+    if (kXs && P.xs_ctl && ctx == 0 && tid == 0) atomicAdd_system(&P.xs_ctl->work, 1); // this GPU searches
     const long long t_start = clock64();
     // first mode: current segment and the counters at its start; thread 0 caches the best key
     // segment bookkeeping (F_FIRST kernels, P.first_mode != 0): every subtree handed out records
@@ -460,12 +545,13 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
     auto get_work = [&]() -> bool {
         if (tid == 0) {
             const long long t0 = clock64();
-            // shared queue first (claiming keeps this context outstanding), then the ring
-            int got = claim_open ? claim_task(P.task_claim, P.n_seed, P.n_ctx) : -1;
-            if (got >= 0) {
-                s_ll = (long long)(got - P.n_ctx) + 1; // claimed seed i is segment 1 + i
+            int got = -1;
+            if constexpr (kSplit) {
+                const WaitOut w = wait_sharded(P, ws, ctx, OS, claim_open ? 1 : 0, kXs);
+                claim_open = w.claim_open != 0;
+                s_ll = w.seg;
+                got = w.got;
             } else {
-                claim_open = false;
                 atomicSub(&ws->outstanding, 1);
                 const uint32_t t = atomicAdd(&ws->hot.pop_ticket, 1u);
                 const unsigned long long* slot = P.ring + (t % P.ring_cap);
@@ -476,24 +562,7 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
                         got = (int)(v & 0xffffffffu);
                         break;
                     }
-                    if ((it & 7) == 7) {
-                        if (ld_volatile(&ws->hot.stop) || ld_volatile(&ws->xs_done)) break;
-                        if (ld_volatile(&ws->outstanding) == 0) { // this GPU has no work left
-                            if (!kSplit || !P.xs_ctl) break;
-                            if (atomicCAS(&ws->xs_thief, 0, 1) == 0) { // steal from another GPU
-                                // re-check under the role: the previous holder may have just
-                                // republished a stolen subtree (this GPU is busy again then)
-                                __threadfence();
-                                int xr = 0;
-                                if (ld_volatile(&ws->outstanding) == 0 && !ld_volatile(&ws->xs_done))
-                                    xr = xs_thief_step(P, ws, ctx, OS);
-                                if (xr < 0) atomicExch(&ws->xs_done, 1);
-                                __threadfence();
-                                atomicExch(&ws->xs_thief, 0);
-                                if (xr < 0) break;
-                            }
-                        }
-                    }
+                    if ((it & 7) == 7 && (ld_volatile(&ws->hot.stop) || ld_volatile(&ws->outstanding) == 0)) break;
                     __nanosleep(ns);
                     ns = ns < 1024 ? ns * 2 : ns;
                 }
@@ -557,7 +626,7 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
         if (skip_node) {
             skip_node = false;
             backtrack = true;
-        } else if (kSplit && P.split_depth >= 0 && depth >= P.split_depth) {
+        } else if (kFrontier && P.split_depth >= 0 && depth >= P.split_depth) {
             // ============ frontier expansion: this open node becomes a task (counted by its shard)
             if (tid == 0) s_ll = (long long)atomicAdd((unsigned long long*)&ws->n_tasks, 1ull);
             sc.sync();
@@ -616,7 +685,14 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
                 g_bound = ld_volatile_s64(&ws->bound);
             }
             my_busy = ld_volatile(&P.outbox_busy[ctx]);
-            if (kSplit && P.xs_ctl && (nodes & 15) == 2) xs_want = xs_hungry(P);
+            if (kXs && P.xs_ctl && (nodes & 15) == 2) { // every 16 nodes: does a GPU ask for work?
+                if constexpr (SC::kWarp) // asynchronous, consumed after the fixpoint with the hot word
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(&C.xs)),
+                                 "l"(P.xs_ctl)
+                                 : "memory");
+                else
+                    xs_want = ld_relaxed_sys_s32(&P.xs_ctl->demand) > 0;
+            }
         }
         if (optimizing) { // branch-and-bound shrink (:87-101), done by thread 0
             if (tid == 0) {
@@ -675,6 +751,8 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
         if constexpr (SC::kWarp)
             if (parallel && tid == 0) asm volatile("cp.async.wait_all;" ::: "memory");
         if (parallel && tid == 0) g_has_bound = (int)hot.w; // the prefetched bound pairs with this flag
+        if constexpr (SC::kWarp && kXs)
+            if (parallel && tid == 0 && P.xs_ctl && (nodes & 15) == 2) xs_want = (int)C.xs.w > 0;
         if (!backtrack) {
             const int sel = select_var<W>(M, dom, P.var_heuristic, red, sc);
             if (sel < 0 && guided) break; // the replay reached its solution: every task is out
@@ -863,9 +941,9 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
                     int want = hot.z ? 2 : 0;
                     // a whole GPU is idle: the shallowest pending branch goes to the global pool
                     // first (one subtree per unit it asked for; local sharing resumes after)
-                    if (kSplit && xs_want && parallel && !want && sp + 1 > base) {
+                    if (kXs && xs_want && parallel && !want && sp + 1 > base) { // one unit: xs_reserve
                         xs_want = 0;
-                        if (xs_dec_demand(P.xs_ctl)) want = 4;
+                        want = 4;
                     }
                     if (parallel && !want && sp + 1 > base && !my_busy && hot.y > hot.x) want = 1;
                     // first mode: pending branches right of the best solution are dropped, never
@@ -882,15 +960,13 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
                 const int want = s_flag;
                 if (want == 2) break;
                 if (want == 3) ++base;
-                if (want == 1 || want == 4) {
+                if (kXs && want == 4) { // out of line: a slot in the owner GPU's HBM, if the demand holds
+                    if (xs_donate<W>(P, sc, frames + (size_t)base * NWP, meta + base * 4, path, KW, NWP, s_ll, tid, T))
+                        ++base;
+                } else if (want == 1) {
                     const int f = base++;
                     const int fvar = meta[f * 4 + 0], fbit = meta[f * 4 + 1], fdepth = meta[f * 4 + 2];
                     uint32_t* ob = P.outbox + (size_t)ctx * OS;
-                    if (kSplit && want == 4) { // the slot in the owner GPU's HBM, over NVLink
-                        if (tid == 0) s_ll = (long long)xs_reserve(P);
-                        sc.sync();
-                        ob = xs_slot_ptr(P, (unsigned)s_ll) + 4;
-                    }
                     const uint32_t* fr = frames + (size_t)f * NWP;
                     const size_t clr = (size_t)fvar * W + (fbit >> 5);
                     for (size_t i = tid; i < NWP; i += T) {
@@ -903,14 +979,8 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
                         ob[NWP + KW] = (uint32_t)(fdepth + 1);
                         ob[NWP + KW + 1] = (uint32_t)fvar;
                     }
-                    if (kSplit && want == 4) __threadfence_system();
                     sc.sync();
-                    if (kSplit && want == 4) {
-                        if (tid == 0) {
-                            st_release_sys_u32(xs_slot_ptr(P, (unsigned)s_ll), (unsigned)s_ll + 1u);
-                            atomicAdd((unsigned long long*)&ws->xs_out, 1ull);
-                        }
-                    } else if (tid == 0) {
+                    if (tid == 0) {
                         P.outbox_busy[ctx] = 1;
                         atomicAdd(&ws->outstanding, 1);
                         const uint32_t s = atomicAdd(&ws->hot.push_ticket, 1u);
@@ -971,7 +1041,7 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
     flush_seg();
     sc.sync();
     // a GPU that stops (error) releases the others from waiting for its work
-    if (kSplit && P.xs_ctl && tid == 0 && ld_volatile(&ws->hot.stop)) atomicExch_system(&P.xs_ctl->abort, 1);
+    if (kXs && P.xs_ctl && tid == 0 && ld_volatile(&ws->hot.stop)) atomicExch_system(&P.xs_ctl->abort, 1);
     if (parallel && tid == 0 && have_work) {
         // unwound by stop: this context no longer counts as outstanding
         atomicSub(&ws->outstanding, 1);
