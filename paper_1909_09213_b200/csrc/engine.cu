@@ -1493,6 +1493,9 @@ int satisfy_records(const HostModel& m, const cubics_search_config& cfg, bool re
 } // namespace
 
 namespace {
+void exact_bnb(const HostModel& m, const cubics_search_config& cfg0, std::vector<uint16_t>& best, cubics_result* out,
+               const std::function<bool(const uint16_t*)>* visit = nullptr);
+
 // AUTO satisfy search capped at k > 1 solutions, no node limit: the parallel engine streams the
 // solutions in DFS order (segments) and the host stops it at the k-th, whose stats are the
 // reference's (search.cpp:151-154) - the exact first-k at parallel speed.
@@ -1537,6 +1540,30 @@ extern "C" int cubics_solve_satisfy(const cubics_model* h, const cubics_search_c
         // streamed unless it is the exact parallel first solution (one row) or a parallel
         // branch-and-bound stream (reference-order incumbents need the parity engine)
         const bool par = engine == CUBICS_ENGINE_PARALLEL;
+        // an objective: the reference's stream is its sequence of incumbents - the exact parallel
+        // B&B delivers them in order (AUTO, no node limit)
+        if (m.goal != CUBICS_SATISFY && cfg->engine == CUBICS_ENGINE_AUTO && cfg->node_limit == 0 && n > 0 &&
+            cfg->max_solutions > 0 && !std::getenv("CUBICS_NO_EXACT_BNB")) {
+            const double t0 = now_ms();
+            std::memset(out, 0, sizeof *out);
+            std::vector<uint16_t> best;
+            uint64_t delivered = 0;
+            const std::function<bool(const uint16_t*)> visit = [&](const uint16_t* row) {
+                ++delivered;
+                if (!want) return true;
+                for (int v = 0; v < n; ++v) vals[v] = m.offset[v] + row[v];
+                return cb(user, vals.data(), n) != 0;
+            };
+            try {
+                exact_bnb(m, *cfg, best, out, &visit);
+                out->has_solution = !best.empty();
+                if (!best.empty()) out->objective = m.offset[m.goal_var] + best[m.goal_var];
+                out->total_ms = now_ms() - t0;
+                return (int)CUBICS_OK;
+            } catch (const StatusError& e) {
+                if (e.code != CUBICS_E_CAPACITY || delivered) throw; // incumbents already delivered
+            }
+        }
         const bool capped = capped_stream(m, *cfg);
         if (capped || (want && !(par && (cfg->max_solutions == 1 || m.goal != CUBICS_SATISFY)))) {
             stream_satisfy(m, *cfg, capped ? CUBICS_ENGINE_PARALLEL : engine, cfg->max_solutions,
@@ -1716,7 +1743,10 @@ namespace {
 //            parallel engine's exact-first search under the static bound v_i: K_i+1 and the
 //            stats from K_i to it. No K_i+1: that phase searched the rest of the tree.
 // The stats are the sums over the phases; the solutions are the K_i.
-void exact_bnb(const HostModel& m, const cubics_search_config& cfg0, std::vector<uint16_t>& best, cubics_result* out) {
+// visit (may be null) receives each incumbent in order (the reference's solution stream of a
+// B&B search); false stops, as does the cfg0.max_solutions-th incumbent (complete = 0).
+void exact_bnb(const HostModel& m, const cubics_search_config& cfg0, std::vector<uint16_t>& best, cubics_result* out,
+               const std::function<bool(const uint16_t*)>* visit) {
     const int n = m.n_vars();
     const bool minimizing = m.goal == CUBICS_MINIMIZE;
     cubics_search_config c = cfg0;
@@ -1733,6 +1763,11 @@ void exact_bnb(const HostModel& m, const cubics_search_config& cfg0, std::vector
     };
     auto objective = [&](const uint16_t* row) { return m.offset[m.goal_var] + (int64_t)row[m.goal_var]; };
     int KW = 0;
+    bool stopped = false;
+    auto incumbent = [&]() { // deliver K_i; true: stop here
+        if (visit && !(*visit)(best.data())) return stopped = true;
+        return stopped = sols >= cfg0.max_solutions;
+    };
     { // phase 0
         RunOut r;
         ShardIO io;
@@ -1748,9 +1783,10 @@ void exact_bnb(const HostModel& m, const cubics_search_config& cfg0, std::vector
             best.assign(r.rec.vals.begin(), r.rec.vals.begin() + n);
             objs.push_back(objective(best.data()));
             ++sols;
+            incumbent();
         }
     }
-    while (!keys.empty()) {
+    while (!keys.empty() && !stopped) {
         const std::vector<uint32_t>& K = keys.back();
         // the bound in force when the reference entered the node at depth d of K's path
         const size_t gd = (size_t)KW * 32 + 1;
@@ -1831,13 +1867,14 @@ void exact_bnb(const HostModel& m, const cubics_search_config& cfg0, std::vector
             throw StatusError{CUBICS_E_INVALID, "exact B&B: a phase returned a non-improving solution"};
         objs.push_back(v);
         ++sols;
+        incumbent();
     }
     out->stats.nodes = tot[0];
     out->stats.failures = tot[1];
     out->stats.rounds = tot[2];
     out->stats.solutions = sols;
     out->engine = CUBICS_ENGINE_PARALLEL;
-    out->complete = 1;
+    out->complete = stopped ? 0 : 1;
 }
 } // namespace
 
@@ -1853,8 +1890,8 @@ extern "C" int cubics_solve_optimize(const cubics_model* h, const cubics_search_
         const int n = m.n_vars();
         // AUTO: the exact parallel branch and bound (reference stats and incumbents); the
         // reference-order engine for node-limited / solution-capped searches
-        if (c.engine == CUBICS_ENGINE_AUTO && c.node_limit == 0 &&
-            c.max_solutions == std::numeric_limits<uint64_t>::max() && n > 0 && !std::getenv("CUBICS_NO_EXACT_BNB")) {
+        if (c.engine == CUBICS_ENGINE_AUTO && c.node_limit == 0 && c.max_solutions > 0 && n > 0 &&
+            !std::getenv("CUBICS_NO_EXACT_BNB")) {
             std::vector<uint16_t> best;
             bool done = false;
             try {
@@ -1865,6 +1902,7 @@ extern "C" int cubics_solve_optimize(const cubics_model* h, const cubics_search_
                 std::memset(out, 0, sizeof *out); // bookkeeping capacity: the reference-order engine
             }
             if (done) {
+                out->complete = 1; // fd::solve_optimize: complete = !limit_hit (search.cpp:197)
                 out->has_solution = !best.empty();
                 if (!best.empty()) {
                     out->objective = m.offset[m.goal_var] + best[m.goal_var];

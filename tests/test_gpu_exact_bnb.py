@@ -67,3 +67,26 @@ def test_initial_bound_is_honoured_exactly():
         o = O.solve_optimize(m, S.SearchConfig(initial_bound=b))
         assert r.stats.as_tuple() == o.stats.as_tuple(), b
         assert (r.best.values if r.best else None) == (o.best.values if o.best else None), b
+
+
+@pytest.mark.parametrize("k", [1, 3, 5])
+def test_solution_cap_stops_after_k_incumbents(k):
+    m = S.parse_model(G.model_text("golomb8"))
+    r = S.solve_optimize(m, S.SearchConfig(device=0, max_solutions=k))
+    o = O.solve_optimize(m, S.SearchConfig(max_solutions=k))
+    assert r.engine == A.ENGINE_PARALLEL
+    assert r.stats.as_tuple() == o.stats.as_tuple()
+    assert r.best.values == o.best.values and r.complete == o.complete
+
+
+@pytest.mark.parametrize("k", [1, 4, 19, 20, 50])
+def test_incumbent_stream_through_solve_satisfy(k):
+    # fd::solve_satisfy on a model with an objective: the callback sees the reference's
+    # incumbents in order (streamed phase by phase by the exact parallel B&B)
+    m = S.parse_model(models.assignment(9, seed=3))
+    seen, oseen = [], []
+    r = S.solve_satisfy(m, S.SearchConfig(device=0), lambda s: seen.append(s.values) or len(seen) < k)
+    o = O.solve_satisfy(m, S.SearchConfig(), lambda s: oseen.append(s.values) or len(oseen) < k)
+    assert r.engine == A.ENGINE_PARALLEL
+    assert seen == oseen
+    assert r.stats.as_tuple() == o.stats.as_tuple()
