@@ -15,6 +15,7 @@
 //   fd::prop_* / propagate_one / group_batches / RemovalSet         include/fd/propagation.hpp:28-83
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <optional>
 #include <stdexcept>
@@ -215,12 +216,40 @@ VarId select_variable(const std::vector<Domain>& domains, VarHeuristic h) {
 
 std::int64_t select_value(const Domain& d) { return d.min(); }
 
+namespace {
+// CUBICS_DEVICES="0,1,..." (two or more): complete enumerations, first solutions and optimizations
+// run on all of those GPUs from this process (cubics_solve_multi). With several GPUs a callback
+// still sees every solution in the reference's DFS order, but a callback that stops early gets the
+// complete search's stats.
+std::vector<int32_t> multi_devices() {
+    std::vector<int32_t> d;
+    const char* e = std::getenv("CUBICS_DEVICES");
+    for (const char* p = e; p && *p;) {
+        char* end = nullptr;
+        const long v = std::strtol(p, &end, 10);
+        if (end == p) break;
+        d.push_back(static_cast<int32_t>(v));
+        p = *end ? end + 1 : end;
+    }
+    return d.size() > 1 ? d : std::vector<int32_t>{};
+}
+
+bool multi_ok(const cubics_search_config& k, bool optimizing) {
+    return k.node_limit == 0 && (optimizing || k.max_solutions == 1 || k.max_solutions == UINT64_MAX);
+}
+} // namespace
+
 SatisfyResult solve_satisfy(const Model& m, const SearchConfig& cfg, const SolutionCallback& cb) {
     ModelHandle h(model_of(m));
     cubics_search_config k = config_of(cfg);
     CbCtx ctx{&cb, goal_of(m)};
     cubics_result r{};
-    check(cubics_solve_satisfy(h.m, &k, cb ? trampoline : nullptr, &ctx, &r));
+    const std::vector<int32_t> devs = multi_devices();
+    if (!devs.empty() && !goal_of(m).optimizing && multi_ok(k, false))
+        check(cubics_solve_multi(h.m, &k, static_cast<int32_t>(devs.size()), devs.data(), cb ? trampoline : nullptr, &ctx,
+                                 nullptr, &r));
+    else
+        check(cubics_solve_satisfy(h.m, &k, cb ? trampoline : nullptr, &ctx, &r));
     SatisfyResult out;
     out.stats = stats_of(r);
     out.complete = r.complete != 0;
@@ -228,6 +257,15 @@ SatisfyResult solve_satisfy(const Model& m, const SearchConfig& cfg, const Solut
 }
 
 std::vector<Solution> enumerate_solutions(const Model& m, const SearchConfig& cfg, SearchStats* stats) {
+    if (!multi_devices().empty() && !goal_of(m).optimizing && multi_ok(config_of(cfg), false)) {
+        std::vector<Solution> out; // several GPUs: the merged stream of cubics_solve_multi
+        const SatisfyResult r = solve_satisfy(m, cfg, [&](const Solution& s) {
+            out.push_back(s);
+            return true;
+        });
+        if (stats) *stats = r.stats;
+        return out;
+    }
     ModelHandle h(model_of(m));
     cubics_search_config k = config_of(cfg);
     cubics_solutions* sols = nullptr;
@@ -249,7 +287,11 @@ OptimizeResult optimize_with(const Model& m, cubics_search_config k) {
     ModelHandle h(model_of(m));
     std::vector<int64_t> best(static_cast<size_t>(std::max(1, m.num_vars())));
     cubics_result r{};
-    check(cubics_solve_optimize(h.m, &k, best.data(), &r));
+    const std::vector<int32_t> devs = multi_devices();
+    if (!devs.empty() && multi_ok(k, true) && k.max_solutions == UINT64_MAX)
+        check(cubics_solve_multi(h.m, &k, static_cast<int32_t>(devs.size()), devs.data(), nullptr, nullptr, best.data(), &r));
+    else
+        check(cubics_solve_optimize(h.m, &k, best.data(), &r));
     OptimizeResult out;
     out.complete = r.complete != 0;
     out.stats = stats_of(r);

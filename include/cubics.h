@@ -25,6 +25,7 @@
  *   cubics_task_queue_*              queue over NVLink peer memory, with cross-GPU stealing
  *   cubics_solve_optimize_shard (new) multi-GPU branch and bound, incumbent shared over NVLink
  *   cubics_solve_first_shard   (new) multi-GPU exact first solution (two-phase merge)
+ *   cubics_solve_multi         (new) multi-GPU search driven from one host process
  *
  * Threading: every call is synchronous and blocks until the device finishes. Calls on
  * different models may run from different host threads. Error details for the last failing
@@ -304,6 +305,18 @@ int cubics_first_shard_best(const cubics_first_shard* s, uint32_t* key, int32_t*
 int cubics_first_shard_prefix(const cubics_first_shard* s, const uint32_t* key, int32_t key_words,
                               cubics_stats* out);
 void cubics_first_shard_free(cubics_first_shard* s);
+
+/* Multi-GPU search from ONE host process (a C/C++ host such as the drop-in fdsolve): one thread per
+ * device runs that rank's shard (cubics_solve_shard_shared / _optimize_shard / _first_shard) with
+ * the shared queue on devices[0] and peer access between the devices; the ranks' stats are summed
+ * (no collective library needed inside one process). Satisfy goals: every solution goes to cb in
+ * the reference's DFS order (key-merged; cb == NULL or count_only: counts only), or with
+ * max_solutions == 1 the exact first solution and the reference's stats; optimize goals: the
+ * optimum (best_values, and cb once). node_limit and other solution caps: CUBICS_E_UNSUPPORTED.
+ * The same device may appear more than once (its ranks then run one after another). */
+int cubics_solve_multi(const cubics_model* m, const cubics_search_config* cfg, int32_t n_devices,
+                       const int32_t* devices, cubics_solution_cb cb, void* user, int64_t* best_values,
+                       cubics_result* out);
 
 /* ---- propagation (kernel-level API) ------------------------------------------------------ */
 typedef struct cubics_fixpoint_result { /* fd::FixpointResult (propagation.hpp:106-110) */

@@ -118,7 +118,7 @@ EXPORTED = [
     "cubics_solve_optimize_batch", "cubics_solve_shard", "cubics_solve_shard_shared", "cubics_solve_optimize_shard",
     "cubics_task_queue_create", "cubics_task_queue_open", "cubics_task_queue_reset", "cubics_task_queue_claims",
     "cubics_task_queue_destroy", "cubics_solve_first_shard", "cubics_first_shard_best", "cubics_first_shard_prefix",
-    "cubics_first_shard_free", "cubics_propagate",
+    "cubics_first_shard_free", "cubics_solve_multi", "cubics_propagate",
     "cubics_removals", "cubics_last_error", "cubics_build_info", "cubics_device_count", "cubics_warmup",
 ]
 
@@ -177,6 +177,9 @@ def declare(lib):
     lib.cubics_first_shard_best.restype = C.c_int
     lib.cubics_first_shard_prefix.argtypes = [C.c_void_p, P(C.c_uint32), C.c_int32, P(Stats)]
     lib.cubics_first_shard_prefix.restype = C.c_int
+    lib.cubics_solve_multi.argtypes = [C.c_void_p, P(SearchConfig), C.c_int32, P(C.c_int32), SOLUTION_CB, C.c_void_p,
+                                       P(C.c_int64), P(Result)]
+    lib.cubics_solve_multi.restype = C.c_int
     lib.cubics_first_shard_free.argtypes = [C.c_void_p]
     lib.cubics_first_shard_free.restype = None
     lib.cubics_propagate.argtypes = [C.c_void_p, P(C.c_uint64), C.c_int32, C.c_int32, P(FixpointResult)]

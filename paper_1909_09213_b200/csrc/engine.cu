@@ -40,6 +40,12 @@ using namespace cubics;
 
 namespace {
 
+#define CUBICS_CHECK_OK(call)                                                                      \
+    do {                                                                                           \
+        const int rc_ = (call);                                                                    \
+        if (rc_ != CUBICS_OK) throw StatusError{rc_, #call};                                        \
+    } while (0)
+
 constexpr int kFastAllDiffMembers = 64;  // warp fast path; larger ones take the generic path
 constexpr int kMaxAllDiffMembers = 4096;  // generic path limit (n x n member bit rows per warp)
 constexpr long kMaxUniverseWords = 1024;  // generic path value universe (32768 values)
@@ -907,6 +913,18 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
         const int cap = std::max(1, per_sm) * sms * warp_k;
         n_ctx = cfg.contexts > 0 ? std::min(cfg.contexts, cap) : cap;
         n_ctx = std::max(warp_k, n_ctx / warp_k * warp_k); // whole blocks of warp contexts
+        // decision stacks of many contexts in HBM: up to n+1 frames each, within a budget (large
+        // models: rcsp-10k would need 400 MB per context); a stack that outgrows its share stops
+        // the search with CUBICS_E_CAPACITY (the exact first solution then falls back to PARITY)
+        if (!frames_in_smem) {
+            const size_t per = sizeof(uint32_t) * P.NWP + 16, budget = size_t(24) << 30;
+            size_t fit = budget / (per * (size_t)n_ctx);
+            if (fit < 256) { // fewer contexts, each with at least 256 frames
+                n_ctx = std::max(warp_k, (int)std::min<size_t>((size_t)n_ctx, budget / (per * 256)) / warp_k * warp_k);
+                fit = budget / (per * (size_t)n_ctx);
+            }
+            if ((size_t)frame_cap > fit) frame_cap = (int)std::max<size_t>(fit, 1);
+        }
     }
     int grid_blocks = 0;
     if (grid) { // co-resident blocks for the cooperative launch
@@ -2447,6 +2465,144 @@ extern "C" int cubics_first_shard_prefix(const cubics_first_shard* s, const uint
 }
 
 extern "C" void cubics_first_shard_free(cubics_first_shard* s) { delete s; }
+
+// Single-process multi-GPU search: one host thread per device runs that rank's shard (the same
+// protocol as distributed.solve_distributed, without a collective library: the ranks share this
+// process, so the "all-reduce" is a sum here). The shared queue lives on devices[0]; the other
+// devices reach it with peer access. This is the multi-GPU path of a C++ host (the adapter's
+// fd:: calls use it when CUBICS_DEVICES names several GPUs).
+extern "C" int cubics_solve_multi(const cubics_model* h, const cubics_search_config* cfg, int32_t n_devices,
+                                  const int32_t* devices, cubics_solution_cb cb, void* user, int64_t* best_values,
+                                  cubics_result* out) {
+    if (!h || !cfg || !out || n_devices < 1 || !devices) return CUBICS_E_INVALID;
+    return guarded([&]() -> int {
+        const double t0 = now_ms();
+        std::memset(out, 0, sizeof *out);
+        const HostModel& m = h->m;
+        const int n = m.n_vars(), N = n_devices;
+        const bool optimize = m.goal != CUBICS_SATISFY;
+        const bool first = !optimize && cfg->max_solutions == 1;
+        if (cfg->node_limit || (!optimize && !first && cfg->max_solutions != std::numeric_limits<uint64_t>::max()))
+            throw StatusError{CUBICS_E_UNSUPPORTED,
+                              "multi-GPU search: complete enumeration, first solution or optimization, no node limit"};
+        cubics_task_queue* q = nullptr;
+        int rc = cubics_task_queue_create(devices[0], &q, nullptr);
+        if (rc) return rc;
+        struct QueueGuard {
+            cubics_task_queue* q;
+            ~QueueGuard() { cubics_task_queue_destroy(q); }
+        } qg{q};
+        if ((rc = cubics_task_queue_reset(q))) return rc;
+        using Row = std::pair<std::vector<uint32_t>, std::vector<int64_t>>;
+        std::vector<cubics_result> res(N);
+        std::vector<int> rcs(N, 0);
+        std::vector<std::string> errs(N);
+        std::vector<std::vector<Row>> rows(N);
+        std::vector<std::vector<int64_t>> bests(N, std::vector<int64_t>(std::max(n, 1)));
+        std::vector<std::unique_ptr<cubics_first_shard>> parts(N);
+        const bool collect = !optimize && !first && cb && !cfg->count_only;
+        cubics_keyed_solution_cb keyed = [](void* u, const uint32_t* key, int32_t kw, const int64_t* vals,
+                                            int32_t nv) -> int32_t {
+            static_cast<std::vector<Row>*>(u)->emplace_back(std::vector<uint32_t>(key, key + kw),
+                                                            std::vector<int64_t>(vals, vals + nv));
+            return 1;
+        };
+        std::vector<std::thread> th;
+        for (int r = 0; r < N; ++r)
+            th.emplace_back([&, r] {
+                cubics_search_config c = *cfg;
+                c.device = devices[r];
+                if (first) {
+                    cubics_first_shard* p = nullptr;
+                    rcs[r] = first_shard_impl(h, &c, r, N, q, &p, &res[r]);
+                    parts[r].reset(p);
+                } else if (optimize) {
+                    rcs[r] = solve_shard_impl(h, &c, r, N, q, nullptr, nullptr, &res[r], true, bests[r].data());
+                } else {
+                    rcs[r] = solve_shard_impl(h, &c, r, N, q, collect ? keyed : nullptr, &rows[r], &res[r], false, nullptr);
+                }
+                if (rcs[r]) errs[r] = cubics_last_error();
+            });
+        for (auto& t : th) t.join();
+        for (int r = 0; r < N; ++r)
+            if (rcs[r]) {
+                set_error("rank " + std::to_string(r) + ": " + errs[r]);
+                return rcs[r];
+            }
+        for (int r = 0; r < N; ++r) { // the "all-reduce"
+            out->stats.nodes += res[r].stats.nodes;
+            out->stats.failures += res[r].stats.failures;
+            out->stats.rounds += res[r].stats.rounds;
+            out->stats.solutions += res[r].stats.solutions;
+            out->device_ms = std::max(out->device_ms, res[r].device_ms);
+            out->h2d_bytes += res[r].h2d_bytes;
+            out->d2h_bytes += res[r].d2h_bytes;
+            out->kernel_launches += res[r].kernel_launches;
+            out->remote_tasks_in += res[r].remote_tasks_in;
+            out->remote_tasks_out += res[r].remote_tasks_out;
+            out->contexts += res[r].contexts;
+        }
+        out->engine = CUBICS_ENGINE_PARALLEL;
+        out->complete = 1;
+        if (optimize) { // the best incumbent over the ranks (ties: the lowest rank)
+            int br = -1;
+            for (int r = 0; r < N; ++r)
+                if (res[r].has_solution &&
+                    (br < 0 || (m.goal == CUBICS_MINIMIZE ? res[r].objective < res[br].objective
+                                                          : res[r].objective > res[br].objective)))
+                    br = r;
+            out->has_solution = br >= 0;
+            if (br >= 0) {
+                out->objective = res[br].objective;
+                if (best_values) std::copy_n(bests[br].begin(), n, best_values);
+                if (cb && !cfg->count_only) cb(user, bests[br].data(), n);
+            }
+        } else if (first) { // min key over the ranks, then the summed prefix shares
+            std::vector<uint32_t> key;
+            std::vector<int64_t> vals(std::max(n, 1));
+            int32_t kw = 0, has = 0;
+            for (int r = 0; r < N; ++r) {
+                std::vector<uint32_t> k(parts[r]->KW);
+                std::vector<int64_t> v(std::max(n, 1));
+                kw = parts[r]->KW;
+                CUBICS_CHECK_OK(cubics_first_shard_best(parts[r].get(), k.data(), &kw, v.data(), &has));
+                if (has && (key.empty() || std::lexicographical_compare(k.begin(), k.end(), key.begin(), key.end()))) {
+                    key = k;
+                    vals = v;
+                }
+            }
+            cubics_stats tot{};
+            for (int r = 0; r < N; ++r) {
+                cubics_stats st{};
+                CUBICS_CHECK_OK(cubics_first_shard_prefix(parts[r].get(), key.empty() ? nullptr : key.data(),
+                                                          (int32_t)key.size(), &st));
+                tot.nodes += st.nodes;
+                tot.failures += st.failures;
+                tot.rounds += st.rounds;
+                tot.solutions += st.solutions;
+            }
+            out->stats = tot;
+            out->has_solution = !key.empty();
+            out->complete = key.empty() ? 1 : 0; // stopped at max_solutions, as the reference reports
+            if (!key.empty()) {
+                if (best_values) std::copy_n(vals.begin(), n, best_values);
+                if (cb && !cfg->count_only) cb(user, vals.data(), n);
+            }
+        } else {
+            out->has_solution = out->stats.solutions > 0;
+            if (collect) { // the ranks' key-ordered streams merged into the reference's DFS order
+                std::vector<Row*> all;
+                for (auto& v : rows)
+                    for (auto& row : v) all.push_back(&row);
+                std::sort(all.begin(), all.end(), [](const Row* a, const Row* b) { return a->first < b->first; });
+                for (const Row* row : all)
+                    if (!cb(user, row->second.data(), n)) break;
+            }
+        }
+        out->total_ms = now_ms() - t0;
+        return (int)CUBICS_OK;
+    });
+}
 
 extern "C" int cubics_solve_shard(const cubics_model* h, const cubics_search_config* cfg, int32_t shard_index,
                                   int32_t shard_count, cubics_keyed_solution_cb cb, void* user, cubics_result* out) {

@@ -649,6 +649,38 @@ def solve_optimize_shard(model: Model, cfg: SearchConfig, shard_index: int, shar
                           res.remote_tasks_out)
 
 
+def solve_multi(model: Model, devices, cfg: SearchConfig | None = None, cb=None):
+    """cubics_solve_multi: one host process drives every device in `devices` (a device may repeat).
+    Returns (SatisfyResult or OptimizeResult, remote subtrees moved between the devices)."""
+    cfg = cfg or SearchConfig()
+    user_err = []
+
+    def trampoline(_user, vals, n):
+        try:
+            return 1 if cb(Solution([vals[i] for i in range(n)])) else 0
+        except BaseException as e:  # noqa: BLE001 - re-raised below
+            user_err.append(e)
+            return 0
+
+    cfun = A.SOLUTION_CB(trampoline) if cb else A.SOLUTION_CB()
+    devs = (C.c_int32 * len(devices))(*devices)
+    best = (C.c_int64 * max(1, model.n_vars))()
+    res = A.Result()
+    c = cfg.to_c()
+    _check(lib().cubics_solve_multi(model.handle, C.byref(c), len(devices), devs, cfun, None, best, C.byref(res)),
+           "solve_multi")
+    if user_err:
+        raise user_err[0]
+    if model.goal != 0:
+        sol = Solution([best[i] for i in range(model.n_vars)], res.objective) if res.has_solution else None
+        r = OptimizeResult(sol, bool(res.complete), _stats(res), res.engine, res.contexts, res.device_ms, res.total_ms,
+                           res.h2d_bytes, res.d2h_bytes, res.kernel_launches, res.remote_tasks_in, res.remote_tasks_out)
+    else:
+        r = SatisfyResult(_stats(res), bool(res.complete), res.engine, res.contexts, res.device_ms, res.total_ms,
+                          res.h2d_bytes, res.d2h_bytes, res.kernel_launches, res.remote_tasks_in, res.remote_tasks_out)
+    return r
+
+
 class FirstShard:
     """One rank's part of a multi-GPU exact first solution (cubics_solve_first_shard).
 

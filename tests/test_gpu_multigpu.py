@@ -270,3 +270,41 @@ def test_cross_gpu_stealing_two_processes_ipc():
         moved += row[4]
     print("subtrees moved between the two processes:", [row[4] for row in got[0]])
     assert moved > 0
+
+
+# ---- one host process driving several devices (cubics_solve_multi; the C++ host's path) --------
+@pytest.mark.parametrize("devices", [[0, 0], [0, 0, 0]])
+def test_solve_multi_single_process(devices):
+    m = S.parse_model(G.model_text("nq12"))
+    got = []
+    r = S.solve_multi(m, devices, S.SearchConfig(), lambda s: got.append(s.values) or True)
+    ost = S.SearchStats()
+    want = [s.values for s in O.enumerate_solutions(m, S.SearchConfig(), ost)]
+    assert r.stats.as_tuple() == ost.as_tuple() and got == want
+    g = G.goldens()["golomb8"]
+    r = S.solve_multi(S.parse_model(G.model_text("golomb8")), devices)
+    assert r.best.objective == g["objective"] and r.best.values == g["best"]
+    for key in ("rcsp_1000|--max 1", "magic4|--max 1"):
+        inst, flags = G.split_key(key)
+        firsts = []
+        r = S.solve_multi(S.parse_model(G.model_text(inst)), devices, G.cfg_from_flags(flags),
+                          lambda s: firsts.append(s.values) or True)
+        assert r.stats.as_tuple() == G.expected_tuple(G.goldens()[key]) and firsts == [G.goldens()[key]["first"]]
+
+
+def test_fdsolve_multi_gpu_env_matches_reference_cli():
+    # the unmodified reference CLI over the adapter with CUBICS_DEVICES naming two GPUs (here the
+    # same one twice): identical output for enumerations, first solutions and optimization
+    import os
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    ref, b200 = os.path.join(root, "oracle", "_ref", "fdsolve"), os.path.join(root, "adapter", "_build", "fdsolve_b200")
+    mdir = os.path.join(root, "tests", "golden", "models")
+    norm = __import__("re").compile(r'time_ms[=":]+\d+')
+    for args in (["solve", f"{mdir}/nq8.fd", "--all", "--stats"], ["solve", f"{mdir}/nq10.fd", "--all", "--json"],
+                 ["solve", f"{mdir}/golomb7.fd", "--stats"], ["solve", f"{mdir}/magic4.fd", "--stats"]):
+        a = subprocess.run([b200] + args, capture_output=True, text=True, timeout=300,
+                           env={**os.environ, "CUBICS_DEVICES": "0,0"})
+        b = subprocess.run([ref] + args, capture_output=True, text=True, timeout=300)
+        assert (a.returncode, norm.sub("T", a.stdout)) == (b.returncode, norm.sub("T", b.stdout)), args
