@@ -92,7 +92,8 @@ def load_peaks():
 
 def ncu_traffic(instance):
     """roofline.traffic: dram__bytes_read.sum + dram__bytes_write.sum of the search kernel from one
-    committed `ncu --set full` capture of this workload (scripts/ncu_traffic.py), per launch."""
+    committed ncu capture of this workload (scripts/ncu_traffic.py: per launch; for the multi-launch
+    B&B / first-solution steps scripts/ncu_step_counts.py: summed over one step)."""
     try:
         with open(os.path.join(ROOT, "profiles", "r02_ncu_traffic.json")) as f:
             rec = json.load(f)[instance]
@@ -501,14 +502,16 @@ def impl_ours(args):
     issue = smem = None
     cap = ncu_counts(args.instance)
     if cap and cap.get("inst_executed") and cap.get("nodes"):
+        # per node of the value's basis (the reference's nodes for B&B / first solution, where the
+        # capture sums every launch of one step: speculative work included)
         per_node = cap["inst_executed"] / cap["nodes"]
-        ach = per_node * tot.nodes / (mean_ms / 1e3)
+        ach = per_node * nodes / (mean_ms / 1e3)
         peak_i = 148 * 4 * sm_hz  # 4 schedulers x 1 warp-instruction / cycle per SM
         issue = {"achieved": ach / 1e9, "peak": peak_i / 1e9, "unit": "G warp-inst/s", "frac": ach / peak_i,
                  "warp_inst_per_node": per_node, "source": cap["report"]}
         if cap.get("smem_wavefronts"):
             wn = cap["smem_wavefronts"] / cap["nodes"]
-            ach_s = wn * tot.nodes / (mean_ms / 1e3)
+            ach_s = wn * nodes / (mean_ms / 1e3)
             peak_s = 148 * sm_hz  # one shared-memory wavefront per cycle per SM
             smem = {"achieved": ach_s / 1e9, "peak": peak_s / 1e9, "unit": "G wavefronts/s", "frac": ach_s / peak_s,
                     "wavefronts_per_node": wn}
