@@ -1276,6 +1276,7 @@ __device__ __forceinline__ void run_propagators(const DevModel& M, const RoundCt
             const int pw = prop_threads >> 5;
             constexpr int NB = W * 32;
             for (int base = warp * 32; base < M.n; base += pw * 32) {
+                if (trig && trig[base >> 5] == 0) continue; // no variable of this word changed
                 const int v = base + lane;
                 int b = -1;
                 if (v < M.n && (!trig || trig_bit(trig, v)) && M.ne_start[v] < M.ne_start[v + 1]) {
