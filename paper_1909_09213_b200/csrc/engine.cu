@@ -1976,11 +1976,44 @@ extern "C" int cubics_solve_optimize_batch(const cubics_model* h, const cubics_s
             b.has_bound[i] = has_bounds ? has_bounds[i] != 0 : (bounds != nullptr);
             b.bound[i] = bounds ? bounds[i] : 0;
         }
+        // No per-problem node limit (fd::lns_optimize without per_iteration_node_limit): the batch
+        // runs under a node budget, and a problem that exhausts it is searched again from scratch by
+        // the exact parallel B&B - the whole GPU, the reference's stats and incumbent - so an LNS
+        // iteration no longer waits for its slowest neighbourhood on one thread block.
+        const bool handoff = cfg->node_limit == 0 && cfg->max_solutions == std::numeric_limits<uint64_t>::max() &&
+                             n > 0 && !std::getenv("CUBICS_NO_BATCH_HANDOFF");
+        cubics_search_config cbud = *cfg;
+        if (handoff) cbud.node_limit = 4096;
         RunOut r;
-        run_search(m, *cfg, CUBICS_ENGINE_PARITY, false, 0, r, false, nullptr, &b);
+        run_search(m, cbud, CUBICS_ENGINE_PARITY, false, 0, r, false, nullptr, &b);
+        const size_t nw64 = m.words.size();
         for (int i = 0; i < count; ++i) {
             cubics_result& o = results[i];
             fill_result(r, &o);
+            if (handoff && (b.flags[i] & 1)) { // over budget: the exact parallel B&B instead
+                HostModel mi = m;
+                mi.words.assign(words + nw64 * i, words + nw64 * (i + 1));
+                cubics_search_config ce = *cfg;
+                ce.engine = CUBICS_ENGINE_AUTO;
+                ce.has_initial_bound = b.has_bound[i];
+                ce.initial_bound = b.bound[i];
+                std::vector<uint16_t> best;
+                cubics_result e{};
+                exact_bnb(mi, ce, best, &e);
+                o.stats = e.stats;
+                o.complete = 1;
+                o.has_solution = !best.empty();
+                o.device_ms += e.device_ms;
+                o.kernel_launches += e.kernel_launches;
+                if (!best.empty()) {
+                    o.objective = m.offset[m.goal_var] + best[m.goal_var];
+                    if (best_values)
+                        for (int v = 0; v < n; ++v) best_values[(size_t)n * i + v] = m.offset[v] + best[v];
+                }
+                o.contexts = count;
+                o.total_ms = now_ms() - t0;
+                continue;
+            }
             o.stats.nodes = b.stats[4 * i + 0];
             o.stats.failures = b.stats[4 * i + 1];
             o.stats.rounds = b.stats[4 * i + 2];

@@ -249,15 +249,28 @@ __device__ __forceinline__ bool fits64(i128 v) {
     return v >= (i128)(-9223372036854775807LL - 1) && v <= (i128)9223372036854775807LL;
 }
 
+// floor / ceil of a / b (b != 0). Unit coefficients (golomb, magic, most sums) skip the division;
+// operands that fit 64 bits take one hardware-emulated 64-bit division instead of two 128-bit ones
+// (|b| >= 2 there, so x / b cannot overflow).
 __device__ __forceinline__ i128 floor_div(i128 a, long long b) {
-    i128 q = a / b;
-    if ((a % b != 0) && ((a < 0) != (b < 0))) q -= 1;
-    return q;
+    if (b == 1) return a;
+    if (b == -1) return -a;
+    if (fits64(a)) {
+        const long long x = (long long)a, q = x / b, r = x - q * b;
+        return (i128)((r != 0 && ((x < 0) != (b < 0))) ? q - 1 : q);
+    }
+    const i128 q = a / b, r = a - q * (i128)b;
+    return (r != 0 && ((a < 0) != (b < 0))) ? q - 1 : q;
 }
 __device__ __forceinline__ i128 ceil_div(i128 a, long long b) {
-    i128 q = a / b;
-    if ((a % b != 0) && ((a < 0) == (b < 0))) q += 1;
-    return q;
+    if (b == 1) return a;
+    if (b == -1) return -a;
+    if (fits64(a)) {
+        const long long x = (long long)a, q = x / b, r = x - q * b;
+        return (i128)((r != 0 && ((x < 0) == (b < 0))) ? q + 1 : q);
+    }
+    const i128 q = a / b, r = a - q * (i128)b;
+    return (r != 0 && ((a < 0) == (b < 0))) ? q + 1 : q;
 }
 
 // filter_linear_le over terms [b, e) with coefficients sign*coeff; false on int64 overflow
