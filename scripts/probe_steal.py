@@ -1,5 +1,5 @@
 """Two processes on one GPU sharing a task queue (CUDA IPC): cross-GPU stealing diagnostics.
-usage: python scripts/probe_steal.py [ctx0] [ctx1] [instance]"""
+usage: python scripts/probe_steal.py [ctx0] [ctx1] [instance]   (WORLD=k: k processes, contexts cycle)"""
 import os
 import socket
 import sys
@@ -53,4 +53,6 @@ if __name__ == "__main__":
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
-    mp.spawn(worker, args=(2, port, ctxs, inst), nprocs=2)
+    world = int(os.environ.get("WORLD", "2"))
+    ctxs = [ctxs[i % 2] for i in range(world)]
+    mp.spawn(worker, args=(world, port, ctxs, inst), nprocs=world)
