@@ -925,6 +925,10 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
             }
             if ((size_t)frame_cap > fit) frame_cap = (int)std::max<size_t>(fit, 1);
         }
+    } else if (!frames_in_smem) { // one context (or one per batch problem): the same budget
+        const size_t per = sizeof(uint32_t) * P.NWP + 16, budget = size_t(32) << 30;
+        const size_t fit = std::max<size_t>(budget / (per * (size_t)n_ctx), 64);
+        if ((size_t)frame_cap > fit) frame_cap = (int)fit; // rcsp-100k: 80k of its 100k+1 frames
     }
     int grid_blocks = 0;
     if (grid) { // co-resident blocks for the cooperative launch

@@ -775,16 +775,24 @@ __device__ void prop_alldiff_gac(const DevModel& M, int a, const uint32_t* dom, 
         F[w] = __reduce_or_sync(FULL, D0[w] | D1[w]) & ~MV[w];
         sd0 |= (D0[w] & F[w]) != 0;
         sd1 |= (D1[w] & F[w]) != 0;
+        // two owner lookups per step: independent shared-memory loads in flight together
+        // (the reference-order kernels run few warps, so the lookup latency is the cost)
         uint32_t x0 = D0[w] & MV[w];
         while (x0) {
-            p0 |= (MS)1 << ws.owner[w * 32 + __ffs(x0) - 1];
+            const int b1 = __ffs(x0) - 1;
             x0 &= x0 - 1;
+            const int b2 = x0 ? __ffs(x0) - 1 : b1;
+            x0 &= x0 - 1;
+            p0 |= ((MS)1 << ws.owner[w * 32 + b1]) | ((MS)1 << ws.owner[w * 32 + b2]);
         }
         if constexpr (TWO) {
             uint32_t x1 = D1[w] & MV[w];
             while (x1) {
-                p1 |= (MS)1 << ws.owner[w * 32 + __ffs(x1) - 1];
+                const int b1 = __ffs(x1) - 1;
                 x1 &= x1 - 1;
+                const int b2 = x1 ? __ffs(x1) - 1 : b1;
+                x1 &= x1 - 1;
+                p1 |= ((MS)1 << ws.owner[w * 32 + b1]) | ((MS)1 << ws.owner[w * 32 + b2]);
             }
         }
     }
@@ -820,11 +828,15 @@ __device__ void prop_alldiff_gac(const DevModel& M, int a, const uint32_t* dom, 
         for (int w = 0; w < U; ++w) {
             uint32_t cand = (sl ? D1[w] : D0[w]) & ~KEEP[w] & ~bitword(mk, w);
             uint32_t x = cand;
-            while (x) {
+            while (x) { // two candidates per step (independent owner / ancestor loads)
                 const int bit = __ffs(x) - 1;
                 x &= x - 1;
-                const int m = ws.owner[w * 32 + bit];
-                if (((ak >> m) & 1u) && ((((MS)ws.anc[m]) >> k) & 1u)) cand &= ~(1u << bit);
+                const int bit2 = x ? __ffs(x) - 1 : bit;
+                x &= x - 1;
+                const int m = ws.owner[w * 32 + bit], m2 = ws.owner[w * 32 + bit2];
+                const MS a1 = (MS)ws.anc[m], a2 = (MS)ws.anc[m2];
+                if (((ak >> m) & 1u) && ((a1 >> k) & 1u)) cand &= ~(1u << bit);
+                if (((ak >> m2) & 1u) && ((a2 >> k) & 1u)) cand &= ~(1u << bit2);
             }
             rem[w] = cand;
             anyr |= cand != 0;
