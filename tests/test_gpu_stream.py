@@ -160,3 +160,28 @@ def test_first_k_solutions_on_the_parallel_engine_are_exact(k):
     assert r.engine == A.ENGINE_PARALLEL
     assert r.stats.as_tuple() == ost.as_tuple()
     assert r.complete is (k > 14200)
+
+
+def test_stream_from_the_grid_context_on_a_large_model():
+    # AUTO on a 100k-variable model picks the grid-wide reference-order context; its solutions and
+    # stop flag go through the same ring (search.cuh EvKind)
+    key = "rcsp_100000|--max 1 --node-limit 200"
+    g = G.goldens()[key]
+    inst, flags = G.split_key(key)
+    m = S.parse_model(G.model_text(inst))
+    seen = []
+    r = S.solve_satisfy(m, G.cfg_from_flags(flags), lambda s: seen.append(s.values) or True)
+    assert r.engine == A.ENGINE_GRID
+    assert r.stats.as_tuple() == G.expected_tuple(g)
+    assert (seen[0] if seen else None) == g.get("first")
+
+
+@pytest.mark.parametrize("k", [1, 5, 40])
+def test_stream_stop_on_table_models(k):
+    # extensional constraints (BASELINE config 5, checked against the oracle's table extension)
+    m = S.parse_model(models.random_binary_csp(12, 4, 18, 0.35, seed=7))
+    seen = []
+    r = S.solve_satisfy(m, S.SearchConfig(), stop_after(k, seen))
+    ro, oseen = oracle_stop(m, k)
+    assert seen == oseen
+    assert r.stats.as_tuple() == ro.stats.as_tuple()
