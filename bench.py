@@ -301,6 +301,9 @@ def run_extras(S, A, device, cpu=True):
                    "stats_equal_reference": (st == exp) if exp else None,
                    "reference_cpu": ref_same_run(key, g) if cpu else None,
                    "reference_cpu_ms_build_box": g.get("time_ms") if g else None, **extra}
+            if name.startswith("config5_"):  # extensional constraints: no reference counterpart
+                rec["parity_note"] = ("unpinned: the reference has no table constraint; the table propagators are "
+                                      "checked against the oracle's table extension and brute force in tests/")
             ref = rec["reference_cpu"]
             if ref and r.device_ms:
                 rec["speedup_vs_reference_cpu"] = (ref["ms"] or ref["est_full_ms"]) / r.device_ms
