@@ -16,10 +16,11 @@ from paper_1909_09213_b200 import solver as S  # noqa: E402
 
 W = int(sys.argv[1]) if len(sys.argv) > 1 else 512
 K = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+STRIDE = int(sys.argv[3]) if len(sys.argv) > 3 else 1  # shards 0, STRIDE, 2*STRIDE, ...
 m = S.parse_model(G.model_text("magic5"))
 tot = [0, 0, 0, 0]
 ms = 0.0
-for r in range(K):
+for r in range(0, K * STRIDE, STRIDE):
     t0 = time.perf_counter()
     res = S.solve_shard(m, S.SearchConfig(device=0, count_only=True), r, W)
     wall = (time.perf_counter() - t0) * 1e3
