@@ -80,11 +80,11 @@ struct Arena {
 };
 // one search at a time per device: the arenas below are reused by every call
 std::recursive_mutex g_dev_mu[64];
-Arena g_arena[2][64];
+Arena g_arena[3][64];
 Arena g_pinned[2][64];
 
-// slot 0: per-call search state; slot 1: solution-ordering scratch (kept apart so growing one
-// never invalidates the other while both are live)
+// slot 0: per-call search state; slot 1: solution-ordering scratch; slot 2: int64 solution rows
+// (kept apart so growing one never invalidates another while both are live)
 uint8_t* device_arena(int dev, size_t bytes, int slot = 0) {
     Arena& a = g_arena[slot][dev];
     if (a.cap < bytes) {
@@ -108,6 +108,61 @@ uint8_t* pinned_arena(int dev, size_t bytes, int slot = 0) {
         a.cap = want;
     }
     return static_cast<uint8_t*>(a.ptr);
+}
+
+// Pinned result arrays (cubics_enumerate): the int64 rows go from the device straight into one of
+// these with a DMA copy, and cubics_solutions_free returns it here instead of freeing it, so the
+// next call reuses it (a fresh 40 MB pinned allocation costs milliseconds).
+class PinnedPool {
+public:
+    static PinnedPool& get() {
+        static PinnedPool* p = new PinnedPool(); // never destroyed: buffers may outlive static teardown
+        return *p;
+    }
+    int64_t* take(size_t bytes) {
+        std::lock_guard<std::mutex> lk(mu_);
+        size_t best = free_.size();
+        for (size_t i = 0; i < free_.size(); ++i)
+            if (free_[i].second >= bytes && (best == free_.size() || free_[i].second < free_[best].second)) best = i;
+        void* p = nullptr;
+        size_t cap = 0;
+        if (best < free_.size()) {
+            p = free_[best].first;
+            cap = free_[best].second;
+            free_.erase(free_.begin() + best);
+        } else {
+            cap = (std::max<size_t>(bytes, 8) + (size_t(2) << 20) - 1) & ~((size_t(2) << 20) - 1);
+            if (cudaHostAlloc(&p, cap, cudaHostAllocPortable) != cudaSuccess) {
+                cudaGetLastError();
+                return nullptr;
+            }
+        }
+        live_[p] = cap;
+        return static_cast<int64_t*>(p);
+    }
+    bool give_back(void* p) {
+        std::lock_guard<std::mutex> lk(mu_);
+        auto it = live_.find(p);
+        if (it == live_.end()) return false;
+        free_.emplace_back(p, it->second);
+        live_.erase(it);
+        while (free_.size() > 3) { // keep a few for the calls to come
+            cudaFreeHost(free_.front().first);
+            free_.erase(free_.begin());
+        }
+        return true;
+    }
+
+private:
+    std::mutex mu_;
+    std::vector<std::pair<void*, size_t>> free_;
+    std::unordered_map<void*, size_t> live_;
+};
+
+__global__ void rows_to_int64(const uint16_t* rows, const int64_t* off, int nv, uint64_t count, int64_t* out) {
+    const uint64_t total = count * (uint64_t)nv;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = off[i % nv] + (int64_t)rows[i];
 }
 
 // host-mapped pinned memory (streaming event ring), grow-only per device
@@ -585,6 +640,8 @@ struct RunOut {
     double device_ms = 0;
     uint64_t h2d = 0, d2h = 0, launches = 0;
     bool pinned_rows = false; // in: download solution rows into pinned slot 1 (cubics_enumerate)
+    bool int64_rows = false;  // in: rows converted to int64 on the device, DMA'd into values64
+    int64_t* values64 = nullptr; // out: a PinnedPool buffer holding rec.count rows (int64_rows)
     std::vector<uint16_t> inc_vals;
     std::vector<uint32_t> first_key;  // parallel: DFS-first solution key/values
     std::vector<uint16_t> first_vals;
@@ -1259,8 +1316,23 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
                                       st, &out.launches);
                 out.rec.ordered = true;
             }
-            CU(cudaMemcpyAsync(dst, src, sizeof(uint16_t) * n * recorded, cudaMemcpyDeviceToHost, st));
-            out.d2h += sizeof(uint16_t) * n * recorded;
+            int64_t* v64 = out.int64_rows && (!parallel || out.rec.ordered || recorded == 1)
+                               ? PinnedPool::get().take(sizeof(int64_t) * n * recorded)
+                               : nullptr;
+            if (v64) { // offsets added on the device, one DMA of the final array
+                int64_t* d64 = reinterpret_cast<int64_t*>(device_arena(dev, sizeof(int64_t) * n * recorded, 2));
+                const int g2 = (int)std::max<uint64_t>(1, std::min<uint64_t>(8192, (recorded * n + 255) / 256));
+                rows_to_int64<<<g2, 256, 0, st>>>(src, S.M.off, n, recorded, d64);
+                CU(cudaGetLastError());
+                out.launches += 1;
+                CU(cudaMemcpyAsync(v64, d64, sizeof(int64_t) * n * recorded, cudaMemcpyDeviceToHost, st));
+                out.d2h += sizeof(int64_t) * n * recorded;
+                out.values64 = v64;
+                out.rec.ordered = true;
+            } else {
+                CU(cudaMemcpyAsync(dst, src, sizeof(uint16_t) * n * recorded, cudaMemcpyDeviceToHost, st));
+                out.d2h += sizeof(uint16_t) * n * recorded;
+            }
             if (!parallel) out.rec.ordered = true;
             if (KW && want_keys) {
                 out.rec.keys.resize(recorded * KW);
@@ -1437,7 +1509,7 @@ namespace {
 // Search for every solution with records materialised (rerun once with an exact buffer when the
 // first guess overflowed); the records come back in the reference's DFS order.
 RunOut satisfy_run(const HostModel& m, const cubics_search_config& cfg, bool record, cubics_result* out,
-                   bool pinned_rows = false) {
+                   bool pinned_rows = false, bool int64_rows = false) {
     std::memset(out, 0, sizeof *out);
     // an objective makes the stream a sequence of incumbents, whose order only the reference
     // node order reproduces: AUTO picks the parity engine then
@@ -1445,6 +1517,7 @@ RunOut satisfy_run(const HostModel& m, const cubics_search_config& cfg, bool rec
     uint64_t cap = default_sol_cap(m, cfg);
     RunOut r;
     r.pinned_rows = pinned_rows;
+    r.int64_rows = int64_rows && m.goal == CUBICS_SATISFY;
     try {
         run_search(m, cfg, engine, record, cap, r);
     } catch (const StatusError& e) {
@@ -1454,11 +1527,15 @@ RunOut satisfy_run(const HostModel& m, const cubics_search_config& cfg, bool rec
         engine = CUBICS_ENGINE_PARITY;
         r = RunOut{};
         r.pinned_rows = pinned_rows;
+        r.int64_rows = int64_rows && m.goal == CUBICS_SATISFY;
         run_search(m, cfg, engine, record, cap, r);
     }
     if (record && r.ws.stats[3] > r.rec.count && r.rec.count == cap) { // buffer overflow: rerun exact
         RunOut r2;
         r2.pinned_rows = pinned_rows;
+        r2.int64_rows = r.int64_rows;
+        if (r.values64) PinnedPool::get().give_back(r.values64); // the truncated first attempt
+        r.values64 = nullptr;
         run_search(m, cfg, engine, record, r.ws.stats[3], r2);
         r2.h2d += r.h2d;
         r2.d2h += r.d2h;
@@ -1717,8 +1794,20 @@ extern "C" int cubics_enumerate(const cubics_model* h, const cubics_search_confi
         }
         // the rows arrive in the device's pinned download buffer: hold the device until converted
         std::lock_guard<std::recursive_mutex> lock(g_dev_mu[current_device(cfg->device)]);
-        RunOut r = satisfy_run(m, *cfg, !cfg->count_only, out, true);
+        RunOut r = satisfy_run(m, *cfg, !cfg->count_only, out, true, true);
         const double t1 = now_ms();
+        if (r.values64) { // already int64 in a pinned buffer: no host conversion
+            auto* S = new cubics_solutions{};
+            S->n_vars = n;
+            S->count = r.rec.count;
+            S->values = r.values64;
+            *sols = S;
+            out->total_ms = now_ms() - t0;
+            if (std::getenv("CUBICS_DEBUG"))
+                std::fprintf(stderr, "[cubics] enumerate: search+download %.3f ms (device %.3f), int64 on the device, %llu rows\n",
+                             t1 - t0, out->device_ms, (unsigned long long)r.rec.count);
+            return (int)CUBICS_OK;
+        }
         const uint64_t total = r.rec.count * (uint64_t)n;
         int64_t* values = alloc_values(std::max<uint64_t>(total, 1)); // before the struct: no leak on throw
         auto* S = new cubics_solutions{};
@@ -1747,7 +1836,7 @@ extern "C" int cubics_enumerate(const cubics_model* h, const cubics_search_confi
 
 extern "C" void cubics_solutions_free(cubics_solutions* s) {
     if (!s) return;
-    std::free(s->values);
+    if (!PinnedPool::get().give_back(s->values)) std::free(s->values);
     delete s;
 }
 
