@@ -6,6 +6,7 @@
 // There is no CPU fallback: without a usable sm_100 device every entry point returns
 // CUBICS_E_CUDA with the CUDA error text in cubics_last_error().
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <sys/mman.h>
 #include <unistd.h>
 
@@ -39,6 +40,15 @@
 using namespace cubics;
 
 namespace {
+
+// NVTX ranges (Nsight timelines; near free without a tool attached): one per search launch,
+// per exact-B&B phase, per shard and per bulk enumeration
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 #define CUBICS_CHECK_OK(call)                                                                      \
     do {                                                                                           \
@@ -864,6 +874,8 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
                 StreamIO* sio = nullptr) {
     const int dev = current_device(cfg.device);
     std::lock_guard<std::recursive_mutex> lock(g_dev_mu[dev]);
+    NvtxRange nvtx(sio ? "cubics search (streaming)" : batch ? "cubics search (batch)" : shard ? "cubics search (shard)"
+                                                                                       : "cubics search");
     // a solution callback runs while its search still owns this device's arenas and stream
     if (g_dev[dev].streaming)
         throw StatusError{CUBICS_E_INVALID, "a solution callback cannot start another search on the same device"};
@@ -1858,6 +1870,7 @@ namespace {
 // B&B search); false stops, as does the cfg0.max_solutions-th incumbent (complete = 0).
 void exact_bnb(const HostModel& m, const cubics_search_config& cfg0, std::vector<uint16_t>& best, cubics_result* out,
                const std::function<bool(const uint16_t*)>* visit) {
+    NvtxRange nvtx("cubics exact B&B");
     const int n = m.n_vars();
     const bool minimizing = m.goal == CUBICS_MINIMIZE;
     cubics_search_config c = cfg0;
