@@ -2270,7 +2270,13 @@ int solve_shard_impl(const cubics_model* h, const cubics_search_config* cfg, int
         const uint64_t want = 256ull * (uint64_t)shard_count;
         RunOut ex;
         ShardIO io;
-        for (int depth = 8;; depth += 4) {
+        int depth0 = 8;
+        {
+            std::lock_guard<std::mutex> hl(h->hint_mu);
+            auto it = h->split_hint.find(shard_count);
+            if (it != h->split_hint.end()) depth0 = it->second;
+        }
+        for (int depth = depth0;; depth += 4) {
             io = ShardIO{};
             io.split_depth = depth;
             io.task_cap = std::max<uint64_t>(4096, 8 * want);
@@ -2289,7 +2295,11 @@ int solve_shard_impl(const cubics_model* h, const cubics_search_config* cfg, int
                 if (io.n_tasks <= io.task_cap) break;
                 io.task_cap = io.n_tasks;
             }
-            if (io.n_tasks >= want || io.n_tasks == 0 || depth >= 64 || (uint64_t)depth >= P.depth_bound) break;
+            if (io.n_tasks >= want || io.n_tasks == 0 || depth >= 64 || (uint64_t)depth >= P.depth_bound) {
+                std::lock_guard<std::mutex> hl(h->hint_mu);
+                h->split_hint[shard_count] = depth;
+                break;
+            }
         }
         if (optimize)
             for (uint64_t s = 0; s < ex.rec.count; ++s) offer(ex.rec.vals.data() + s * n);

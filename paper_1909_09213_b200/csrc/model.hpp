@@ -7,6 +7,8 @@
 #pragma once
 
 #include <cstdint>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -43,6 +45,11 @@ const char* last_error();
 
 struct cubics_model {
     cubics::HostModel m;
+    // sharded searches: the frontier split depth found for each shard count (the first of 8, 12,
+    // 16, ... with enough open nodes); later calls start there instead of re-expanding from 8.
+    // The result is the same depth, so every rank still builds the same frontier.
+    mutable std::mutex hint_mu;
+    mutable std::map<int, int> split_hint;
 };
 
 struct cubics_task_queue {
