@@ -24,6 +24,9 @@ struct Ctl {
     long long ll;
     int xs_want, pad; // thread 0: some GPU asked for a subtree (cross-GPU stealing)
     uint4 xs;         // warp contexts: {push, pop, work, demand} of the pool, prefetched by cp.async
+    // thread 0's work-sharing counters (the debug line / busy fraction): kept here, not in
+    // registers, so the search loop has 8 more registers under the 64-register cap
+    long long idle_cyc, steals, donations, t_start;
     unsigned red[32];
 };
 

@@ -476,11 +476,18 @@ __device__ __forceinline__ void search_body(const SearchParams& P, SC& sc, Ctl& 
     int g_has_bound = P.has_init_bound;
     int my_busy = 0;
 
-    long long idle_cyc = 0, steals = 0, donations = 0;
+    // sharded kernels keep thread 0's work-sharing counters in shared memory (registers are what
+    // their search loop runs short of); the lean kernels keep them in registers
+    struct { long long idle_cyc, steals, donations, t_start; } lc{0, 0, 0, 0};
+    long long& idle_cyc = kSplit ? C.idle_cyc : lc.idle_cyc;
+    long long& steals = kSplit ? C.steals : lc.steals;
+    long long& donations = kSplit ? C.donations : lc.donations;
+    long long& t_start = kSplit ? C.t_start : lc.t_start;
+    if (tid == 0) idle_cyc = steals = donations = 0;
     int& xs_want = C.xs_want; // thread 0: some GPU waits for a subtree (refreshed every 16 nodes)
     if (tid == 0) xs_want = 0;
     if (kXs && P.xs_ctl && ctx == 0 && tid == 0) atomicAdd_system(&P.xs_ctl->work, 1); // this GPU searches
-    const long long t_start = clock64();
+    if (tid == 0) t_start = clock64();
     // first mode: current segment and the counters at its start; thread 0 caches the best key
     // segment bookkeeping (F_FIRST kernels, P.first_mode != 0): every subtree handed out records
     // its root key and stats, solutions their segment-local snapshots. first_mode (== 1) also
