@@ -872,6 +872,7 @@ __global__ void gather_tasks(const uint32_t* src, const int32_t* idx, int n, siz
 void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine, bool record, uint64_t sol_cap,
                 RunOut& out, bool want_keys = false, ShardIO* shard = nullptr, BatchIO* batch = nullptr,
                 StreamIO* sio = nullptr) {
+    const double rs_t0 = now_ms();
     const int dev = current_device(cfg.device);
     std::lock_guard<std::recursive_mutex> lock(g_dev_mu[dev]);
     NvtxRange nvtx(sio ? "cubics search (streaming)" : batch ? "cubics search (batch)" : shard ? "cubics search (shard)"
@@ -1428,6 +1429,7 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
         out.ws.user_stop = 1;
     }
     if (std::getenv("CUBICS_DEBUG")) {
+        std::fprintf(stderr, "[cubics] run_search wall %.3f ms (device %.3f)\n", now_ms() - rs_t0, out.device_ms);
         const WorkState& w = out.ws;
         const double tot = (double)w.busy_cycles + (double)w.idle_cycles;
         std::fprintf(stderr,
@@ -1910,6 +1912,15 @@ void exact_bnb(const HostModel& m, const cubics_search_config& cfg0, std::vector
             incumbent();
         }
     }
+    // the outbox layout of the replay's tasks (once: prepare() flattens the whole model)
+    const int dev = current_device(c.device);
+    size_t NWP = 0;
+    if (!keys.empty() && !stopped) {
+        Prepared P0;
+        prepare(m, m.words.data(), P0);
+        NWP = P0.NWP;
+    }
+    const size_t OS = NWP + dev::round4((size_t)KW + 2);
     while (!keys.empty() && !stopped) {
         const std::vector<uint32_t>& K = keys.back();
         // the bound in force when the reference entered the node at depth d of K's path
@@ -1934,10 +1945,6 @@ void exact_bnb(const HostModel& m, const cubics_search_config& cfg0, std::vector
             rp.guide_bound[d] = b;
             rp.guide_has[d] = hb;
         }
-        const int dev = current_device(c.device);
-        Prepared P;
-        prepare(m, m.words.data(), P);
-        const size_t OS = P.NWP + dev::round4((size_t)KW + 2);
         rp.task_cap = gd;
         rp.task_dev = reinterpret_cast<uint32_t*>(device_arena(dev, sizeof(uint32_t) * OS * rp.task_cap, 1));
         cubics_search_config cr = c;
@@ -1948,7 +1955,7 @@ void exact_bnb(const HostModel& m, const cubics_search_config& cfg0, std::vector
         const uint64_t nt = rp.n_tasks;
         if (nt == 0) break; // nothing right of K_i: the search is complete
         std::vector<uint32_t> tkey(nt * KW);
-        CU(cudaMemcpy2D(tkey.data(), sizeof(uint32_t) * KW, rp.task_dev + P.NWP, sizeof(uint32_t) * OS,
+        CU(cudaMemcpy2D(tkey.data(), sizeof(uint32_t) * KW, rp.task_dev + NWP, sizeof(uint32_t) * OS,
                         sizeof(uint32_t) * KW, nt, cudaMemcpyDeviceToHost));
         std::vector<int32_t> seeds(nt);
         std::iota(seeds.begin(), seeds.end(), 0);
