@@ -228,13 +228,15 @@ def _steal_worker(rank, world, port, out):
         m = S.parse_model(G.model_text("nq14"))
         q = D.shared_task_queue(rank, world, device=0)
         res = []
-        for _ in range(3):
+        for _ in range(4):
             if rank == 0:
                 q.reset()
             dist.barrier()
-            # few contexts per process, so both kernels are resident on this one GPU at once:
-            # the process that runs out of claims first steals right branches from the other
-            r = S.solve_shard(m, S.SearchConfig(device=0, contexts=64, count_only=True), rank, world, queue=q)
+            # few contexts per process, so both kernels are resident on this one GPU at once; the
+            # process with many contexts runs out of work first and steals right branches from the
+            # one with few
+            ctxs = 256 if rank == 0 else 16
+            r = S.solve_shard(m, S.SearchConfig(device=0, contexts=ctxs, count_only=True), rank, world, queue=q)
             t = torch.tensor(list(r.stats.as_tuple()) + [r.remote_in, r.remote_out], dtype=torch.int64)
             dist.all_reduce(t)
             res.append(t.tolist())
