@@ -185,3 +185,26 @@ def test_stream_stop_on_table_models(k):
     ro, oseen = oracle_stop(m, k)
     assert seen == oseen
     assert r.stats.as_tuple() == ro.stats.as_tuple()
+
+
+def test_stream_stops_across_the_acceptance_corpus():
+    # the 200-instance acceptance corpus (acceptance.cpp:47-54), each streamed on the default
+    # config and stopped at a seeded random k: the delivered prefix and the stats equal the oracle's
+    import random
+
+    rnd = random.Random(20261019)
+    c = G.corpus()["corpus"]
+    checked = 0
+    for seed in range(200):
+        total = len(c[str(seed)]["all"]["all"])
+        if total == 0:
+            continue
+        k = rnd.randint(1, total + 1)
+        m = S.parse_model(models.corpus_instance(seed))
+        seen = []
+        r = S.solve_satisfy(m, S.SearchConfig(), stop_after(k, seen))
+        ro, oseen = oracle_stop(m, k)
+        assert seen == oseen, seed
+        assert r.stats.as_tuple() == ro.stats.as_tuple(), seed
+        checked += 1
+    assert checked > 50  # the instances with at least one solution
