@@ -1411,17 +1411,55 @@ __device__ __forceinline__ void run_propagators(const DevModel& M, const RoundCt
 
 // Phase B: dom &= ~rm. Returns R_CHANGED / R_STABLE / R_FAILED / R_ERROR.
 // failed_var (when non-null) receives the lowest empty var id on failure.
+// full == false: every domain was non-empty when the round started (any node but the root's first
+// round), so only a variable with removals can change or empty: the others are skipped on their
+// removal words alone (one 16-byte load per four one-word variables), without touching dom.
 template <int W, class SC>
 __device__ __forceinline__ int apply_removals(const DevModel& M, const RoundCtx& R, volatile int* s_err,
-                                              volatile int* s_min, int* failed_var, uint32_t* chg_out, SC& sc) {
+                                              volatile int* s_min, int* failed_var, uint32_t* chg_out, SC& sc,
+                                              bool full = true) {
     const int tid = sc.tid(), T = sc.nthreads();
     int changed = 0, empty_min = 0x7fffffff;
-    for (int v = tid; v < M.n; v += T) {
+    auto one = [&](int v, uint32_t rw) { // one-word variable v with removals rw != 0
+        uint32_t dw = R.dom[v];
+        if (dw & rw) {
+            dw &= ~rw;
+            R.dom[v] = dw;
+            changed = 1;
+            if (chg_out) atomicOr(chg_out + (v >> 5), 1u << (v & 31));
+        }
+        R.rm[v] = 0;
+        if (!dw && v < empty_min) empty_min = v;
+    };
+    if constexpr (W == 1) {
+        if (!full) {
+            const uint4* r4 = reinterpret_cast<const uint4*>(R.rm); // rows padded to 4 words
+            for (int q = tid; q < ((M.n + 3) >> 2); q += T) {
+                const uint4 rr = r4[q];
+                if (!(rr.x | rr.y | rr.z | rr.w)) continue;
+                const int v = q << 2;
+                if (rr.x) one(v, rr.x);
+                if (rr.y && v + 1 < M.n) one(v + 1, rr.y);
+                if (rr.z && v + 2 < M.n) one(v + 2, rr.z);
+                if (rr.w && v + 3 < M.n) one(v + 3, rr.w);
+            }
+        }
+    }
+    for (int v = tid; v < M.n && (full || W > 1); v += T) {
         uint32_t* d = R.dom + (size_t)v * W;
         uint32_t* r = R.rm + (size_t)v * W;
         uint32_t any = 0;
         bool vch = false;
         const int nv = vwords<W>(M, v);
+        if (!full) { // no removal for this variable: nothing to apply, and it cannot be empty
+            uint32_t rany = 0;
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                if (W > 4 && w >= nv) break;
+                rany |= r[w];
+            }
+            if (!rany) continue;
+        }
 #pragma unroll
         for (int w = 0; w < W; ++w) {
             if (W > 4 && w >= nv) break;
@@ -1476,7 +1514,7 @@ __device__ int block_fixpoint(const DevModel& M, const RoundCtx& R, volatile int
             for (int i = tid; i < nb; i += T) nxt[i] = 0;
         run_propagators<W, F>(M, R, s_err, all ? nullptr : cur, sc);
         sc.sync();
-        const int st = apply_removals<W>(M, R, s_err, s_min, failed_var, nxt, sc);
+        const int st = apply_removals<W>(M, R, s_err, s_min, failed_var, nxt, sc, all && r == 0);
         ++r;
         if (st != R_CHANGED || (max_rounds > 0 && r >= max_rounds)) {
             *rounds = r;
