@@ -941,6 +941,10 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
                                 ? 128
                                 : (P.W >= 8 || P.nr + P.nl + P.ntb + P.ntn > 256 ? 64 : 32))
                          : parity_block(P);
+    // exact-first searches (first solution, exact B&B phases, sharded first): fewer, wider
+    // contexts - less speculation right of the answer, faster per node (B200: golomb10 exact B&B
+    // 89 -> 65 ms at 128 threads, rcsp-1k first 137 -> 123 ms at 256)
+    if (parallel && seg_mode == 1 && !use_warp && cfg.block_threads <= 0) block = std::min(256, std::max(128, 4 * block));
     block = std::min(std::max(block, 32), batch ? 512 : 1024);
     const int nw = use_warp ? 1 : block / 32;
     bool in_smem = !grid; // the grid context keeps its domains in L2/HBM
