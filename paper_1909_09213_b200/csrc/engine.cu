@@ -930,7 +930,10 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
     // small models run warp contexts (warp_ctx.cuh): K contexts per block of 32K threads
     // (sharded first-solution runs need the frontier split with segment bookkeeping, which the
     // lean warp kernels compile out: they run block contexts)
+    // (exact-first searches run block contexts too: fewer, wider contexts win there - magic5 first
+    // 3.7 -> 2.7 ms at 128 threads)
     const bool use_warp = P.warp_ok && !grid && !batch && cfg.block_threads <= 0 && !(shard && (shard->first || shard->root_first)) &&
+                          !first_mode &&
                           (parallel || engine == CUBICS_ENGINE_PARITY) && !std::getenv("CUBICS_NO_WARP");
     const int warp_k = use_warp && parallel ? std::max(1, std::min(2, std::getenv("CUBICS_WARP_K") ? std::atoi(std::getenv("CUBICS_WARP_K")) : 1)) : 1;
     int block = cfg.block_threads > 0 ? ((cfg.block_threads + 31) / 32) * 32 : 0;
