@@ -2103,7 +2103,10 @@ extern "C" int cubics_solve_optimize_batch(const cubics_model* h, const cubics_s
         const bool handoff = cfg->node_limit == 0 && cfg->max_solutions == std::numeric_limits<uint64_t>::max() &&
                              n > 0 && !std::getenv("CUBICS_NO_BATCH_HANDOFF");
         cubics_search_config cbud = *cfg;
-        if (handoff) cbud.node_limit = 4096;
+        if (handoff) {
+            const char* b = std::getenv("CUBICS_BATCH_BUDGET"); // A/B only
+            cbud.node_limit = b ? std::max(1, std::atoi(b)) : 4096;
+        }
         RunOut r;
         run_search(m, cbud, CUBICS_ENGINE_PARITY, false, 0, r, false, nullptr, &b);
         const size_t nw64 = m.words.size();
