@@ -39,6 +39,7 @@ struct DevModel {
     int32_t nr_gen;              // records [0, nr_gen) are not var-form !=
     const int32_t* ne_start;     // [n+1] var-form != incidence: when v becomes a singleton at bit b,
     const int2* ne_edge;         //   each edge (p, s) removes bit b + s from var p
+    const uint32_t* ne_mask;     // [ceil(n/32)] bit v: v has var-form != edges
     const unsigned long long* neq; // [n*n] warp kernel (n <= 32, W = 1): the != edges u -> p folded
                                  //   into one mask, bit s + 32 per shift s in [-31, 31]; else null
     int32_t nl;

@@ -213,7 +213,7 @@ struct Prepared {
     size_t o_neq = 0;
     bool warp_ok = false;     // search_kernel_warp eligible: n <= 32, W = 1, small alldifferents, no tables
     bool mixed_width = false; // some variable needs <= W/4 words: per-variable word counts pay
-    size_t o_off, o_dom, o_rb, o_ls, o_lo, o_lb, o_lv, o_lc, o_as, o_av, o_ash, o_nes, o_nee, o_auw;
+    size_t o_off, o_dom, o_rb, o_ls, o_lo, o_lb, o_lv, o_lc, o_as, o_av, o_ash, o_nes, o_nee, o_auw, o_nem;
     size_t o_tbxy, o_tboff, o_tbsup, o_tns, o_tnv, o_tnn, o_tno, o_tnd;
     int ntb = 0, ntn = 0;
     size_t big_words = 0;
@@ -234,6 +234,7 @@ struct Prepared {
         M.nr_gen = nr_gen;
         M.ne_start = reinterpret_cast<const int32_t*>(base + o_nes);
         M.ne_edge = reinterpret_cast<const int2*>(base + o_nee);
+        M.ne_mask = reinterpret_cast<const uint32_t*>(base + o_nem);
         M.neq = warp_ok && nr_gen < nr ? reinterpret_cast<const unsigned long long*>(base + o_neq) : nullptr;
         M.nl = nl;
         M.lin_start = reinterpret_cast<const int32_t*>(base + o_ls);
@@ -495,6 +496,10 @@ void prepare(const HostModel& m, const uint64_t* words, Prepared& P) {
     P.o_tnd = P.blob.add(tn_data.data(), tn_data.size());
     P.o_nes = P.blob.add(nes.data(), nes.size());
     P.o_nee = P.blob.add(nee.data(), nee.size());
+    std::vector<uint32_t> nem(((size_t)n + 31) / 32 + 1, 0u); // variables with != edges, one bit each
+    for (int v = 0; v < n; ++v)
+        if (nes[v] < nes[v + 1]) nem[v >> 5] |= 1u << (v & 31);
+    P.o_nem = P.blob.add(nem.data(), nem.size());
     // warp contexts (warp_ctx.cuh): one lane per variable, one-word domains and alldifferent
     // universes, <= 32 members per alldifferent, no tables or generic-path alldifferents
     int max_members = 0;

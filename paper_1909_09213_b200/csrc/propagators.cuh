@@ -1301,10 +1301,12 @@ __device__ __forceinline__ void run_propagators(const DevModel& M, const RoundCt
             const int pw = prop_threads >> 5;
             constexpr int NB = W * 32;
             for (int base = warp * 32; base < M.n; base += pw * 32) {
-                if (trig && trig[base >> 5] == 0) continue; // no variable of this word changed
+                // variables of this word that changed and have != edges (one word test per lane)
+                const uint32_t cw = (trig ? trig[base >> 5] : 0xffffffffu) & M.ne_mask[base >> 5];
+                if (cw == 0) continue;
                 const int v = base + lane;
                 int b = -1;
-                if (v < M.n && (!trig || trig_bit(trig, v)) && M.ne_start[v] < M.ne_start[v + 1]) {
+                if (v < M.n && ((cw >> lane) & 1u)) {
                     const uint32_t* dv = R.dom + (size_t)v * W;
                     const int nv = vwords<W>(M, v);
                     if (dom_size_n<W>(dv, nv) == 1) b = dom_first_n<W>(dv, nv);
