@@ -310,3 +310,20 @@ def test_fdsolve_multi_gpu_env_matches_reference_cli():
                            env={**os.environ, "CUBICS_DEVICES": "0,0"})
         b = subprocess.run([ref] + args, capture_output=True, text=True, timeout=300)
         assert (a.returncode, norm.sub("T", a.stdout)) == (b.returncode, norm.sub("T", b.stdout)), args
+
+
+def test_solve_multi_edge_cases():
+    # an infeasible model: no first solution, the complete search's stats
+    m = S.parse_model(models.gen_nqueens(3))
+    ost = S.SearchStats()
+    O.enumerate_solutions(m, S.SearchConfig(), ost)
+    r = S.solve_multi(m, [0, 0], S.SearchConfig(max_solutions=1))
+    assert r.stats.as_tuple() == ost.as_tuple() and r.complete
+    # count only: no callback, exact counts
+    m = S.parse_model(G.model_text("nq10"))
+    seen = []
+    r = S.solve_multi(m, [0, 0], S.SearchConfig(count_only=True), lambda s: seen.append(s) or True)
+    assert r.stats.as_tuple() == G.expected_tuple(G.goldens()["nq10|--all"]) and seen == []
+    # node limits are not sharded: a clear error
+    with pytest.raises(S.UnsupportedInstance):
+        S.solve_multi(m, [0, 0], S.SearchConfig(node_limit=100))
