@@ -748,6 +748,9 @@ public:
             return;
         }
         Seg& s = it->second;
+        buffered_ += sizeof(uint16_t) * n_ + sizeof(uint64_t) * 3;
+        if (buffered_ > kMaxBuffered) // fail loudly rather than exhaust host memory
+            throw StatusError{CUBICS_E_CAPACITY, "stream: solutions waiting right of the delivery cursor exceed 16 GiB"};
         s.rows.insert(s.rows.end(), row, row + n_);
         s.snaps.insert(s.snaps.end(), snap, snap + 3);
     }
@@ -769,6 +772,7 @@ public:
             Seg& nx = segs_.at(cursor_);
             for (size_t r = 0; r * 3 < nx.snaps.size() && !io_.stopped; ++r)
                 deliver(nx.rows.data() + r * n_, nx.snaps.data() + r * 3);
+            buffered_ -= std::min<size_t>(buffered_, (nx.snaps.size() / 3) * (sizeof(uint16_t) * n_ + sizeof(uint64_t) * 3));
             nx.rows.clear();
             nx.rows.shrink_to_fit();
             nx.snaps.clear();
@@ -793,6 +797,8 @@ private:
             std::copy_n(st, 3, io_.stop_stats);
         }
     }
+    static constexpr size_t kMaxBuffered = size_t(16) << 30;
+    size_t buffered_ = 0;
     int KW_, n_;
     StreamIO& io_;
     std::unordered_map<uint32_t, Seg> segs_;
