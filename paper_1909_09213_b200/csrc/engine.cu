@@ -169,6 +169,38 @@ private:
     std::unordered_map<void*, size_t> live_;
 };
 
+// Sum of the segments' stats (nodes, failures, rounds) whose root key is not right of K (all of
+// them when K is null), except segment `skip`: the reference's DFS prefix up to K (search.cuh
+// segments). On the device, so the host downloads three numbers, not every segment.
+__global__ void seg_prefix_sum(const uint32_t* seg_key, const uint64_t* seg_st, uint64_t nseg, int KW,
+                               const uint32_t* K, int64_t skip, unsigned long long* tot) {
+    unsigned long long a = 0, b = 0, c = 0;
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < nseg; s += (uint64_t)gridDim.x * blockDim.x) {
+        if ((int64_t)s == skip) continue;
+        if (K) {
+            int cmp = 0; // K vs root key of s
+            for (int i = 0; i < KW && !cmp; ++i) {
+                const uint32_t x = K[i], y = seg_key[s * KW + i];
+                cmp = x < y ? -1 : (x > y ? 1 : 0);
+            }
+            if (cmp < 0) continue; // right of K
+        }
+        a += seg_st[s * 3 + 0];
+        b += seg_st[s * 3 + 1];
+        c += seg_st[s * 3 + 2];
+    }
+    for (int o = 16; o; o >>= 1) {
+        a += __shfl_down_sync(0xffffffffu, a, o);
+        b += __shfl_down_sync(0xffffffffu, b, o);
+        c += __shfl_down_sync(0xffffffffu, c, o);
+    }
+    if ((threadIdx.x & 31) == 0 && (a | b | c)) {
+        atomicAdd(tot + 0, a);
+        atomicAdd(tot + 1, b);
+        atomicAdd(tot + 2, c);
+    }
+}
+
 __global__ void rows_to_int64(const uint16_t* rows, const int64_t* off, int nv, uint64_t count, int64_t* out) {
     const uint64_t total = count * (uint64_t)nv;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x)
@@ -679,6 +711,7 @@ struct ShardIO {
     // (guide_key, reference-order kernel) emits the pending right branches of a recorded path
     bool root_first = false;
     bool static_bound = false;
+    bool prefix_sum = false; // seeded exact-first run: best solution and prefix stats as for first mode
     const std::vector<uint32_t>* guide_key = nullptr;
     std::vector<int64_t> guide_bound; // [KW * 32 + 1]
     std::vector<int32_t> guide_has;
@@ -1284,31 +1317,45 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
         float ms = 0;
         CU(cudaEventElapsedTime(&ms, e0, e1));
         out.device_ms = ms;
-        if (first_mode) { // the reference's prefix up to the DFS-first solution, summed exactly
-            const uint64_t nseg = (uint64_t)out.ws.hot.push_ticket + 1, nsol = out.ws.sol_count;
+        if (first_mode || (shard && shard->prefix_sum)) { // the reference's prefix up to the DFS-first solution
+            const uint64_t nseg = (uint64_t)out.ws.hot.push_ticket + 1 + (uint64_t)S.seg_base, nsol = out.ws.sol_count;
             if (nseg > (uint64_t)seg_cap || nsol > sol_cap)
                 throw StatusError{CUBICS_E_CAPACITY, "first-solution bookkeeping capacity"};
-            std::vector<uint32_t> sk(nseg * KW), solk(nsol * KW);
-            std::vector<uint64_t> ss(nseg * 3), sst(nsol * 3);
+            std::vector<uint32_t> solk(nsol * KW);
+            std::vector<uint64_t> sst(nsol * 3);
             std::vector<int32_t> sseg(nsol);
-            CU(cudaMemcpyAsync(sk.data(), base + a_segk, sizeof(uint32_t) * KW * nseg, cudaMemcpyDeviceToHost, st));
-            CU(cudaMemcpyAsync(ss.data(), base + a_segs, sizeof(uint64_t) * 3 * nseg, cudaMemcpyDeviceToHost, st));
             if (nsol) {
                 CU(cudaMemcpyAsync(solk.data(), base + a_skeys, sizeof(uint32_t) * KW * nsol, cudaMemcpyDeviceToHost, st));
                 CU(cudaMemcpyAsync(sst.data(), base + a_sstats, sizeof(uint64_t) * 3 * nsol, cudaMemcpyDeviceToHost, st));
                 CU(cudaMemcpyAsync(sseg.data(), base + a_sseg, sizeof(int32_t) * nsol, cudaMemcpyDeviceToHost, st));
             }
             CU(cudaStreamSynchronize(st));
-            out.d2h += sizeof(uint32_t) * KW * (nseg + nsol) + sizeof(uint64_t) * 3 * (nseg + nsol) + 4 * nsol;
+            out.d2h += sizeof(uint32_t) * KW * nsol + sizeof(uint64_t) * 3 * nsol + 4 * nsol;
             auto less = [&](const uint32_t* a, const uint32_t* b) { return std::lexicographical_compare(a, a + KW, b, b + KW); };
             int64_t best = -1;
             for (uint64_t i = 0; i < nsol; ++i)
                 if (best < 0 || less(&solk[i * KW], &solk[best * KW])) best = (int64_t)i;
+            // every segment not right of the answer, its own segment aside: summed on the device
             uint64_t tot[3] = {0, 0, 0};
-            for (uint64_t s = 0; s < nseg; ++s) {
-                if (best >= 0 && (int64_t)sseg[best] == (int64_t)s) continue;
-                if (best >= 0 && less(&solk[best * KW], &sk[s * KW])) continue; // right of the answer
-                for (int i = 0; i < 3; ++i) tot[i] += ss[s * 3 + i];
+            {
+                uint8_t* scratch = device_arena(dev, 256 + sizeof(uint32_t) * KW, 2);
+                unsigned long long* dtot = reinterpret_cast<unsigned long long*>(scratch);
+                uint32_t* dk = reinterpret_cast<uint32_t*>(scratch + 256);
+                CU(cudaMemsetAsync(dtot, 0, 3 * sizeof(unsigned long long), st));
+                if (best >= 0)
+                    CU(cudaMemcpyAsync(dk, base + a_skeys + sizeof(uint32_t) * KW * best, sizeof(uint32_t) * KW,
+                                       cudaMemcpyDeviceToDevice, st));
+                const int g = (int)std::max<uint64_t>(1, std::min<uint64_t>(1184, (nseg + 255) / 256));
+                seg_prefix_sum<<<g, 256, 0, st>>>(reinterpret_cast<const uint32_t*>(base + a_segk),
+                                                 reinterpret_cast<const uint64_t*>(base + a_segs), nseg, KW,
+                                                 best >= 0 ? dk : nullptr, best >= 0 ? (int64_t)sseg[best] : -1, dtot);
+                CU(cudaGetLastError());
+                out.launches += 1;
+                unsigned long long h[3];
+                CU(cudaMemcpyAsync(h, dtot, sizeof h, cudaMemcpyDeviceToHost, st));
+                CU(cudaStreamSynchronize(st));
+                out.d2h += sizeof h;
+                for (int i = 0; i < 3; ++i) tot[i] = h[i];
             }
             if (best >= 0) {
                 for (int i = 0; i < 3; ++i) tot[i] += sst[best * 3 + i];
@@ -1418,7 +1465,7 @@ void run_search(const HostModel& hm, const cubics_search_config& cfg, int engine
             out.d2h += (sizeof(uint64_t) * 4 + sizeof(int32_t) + sizeof(uint16_t) * n) * nb;
         }
         if (shard) shard->n_tasks = (uint64_t)out.ws.n_tasks;
-        if (shard && seg_mode) { // segments and the frontier tasks' positions, for the host's prefix sums
+        if (shard && seg_mode && !shard->prefix_sum) { // segments and the frontier tasks' positions, for the host's prefix sums
             const uint64_t nseg = (uint64_t)out.ws.hot.push_ticket + 1 + (uint64_t)S.seg_base;
             if (nseg > (uint64_t)seg_cap) throw StatusError{CUBICS_E_CAPACITY, "segment bookkeeping capacity"};
             shard->n_seg = nseg;
@@ -1986,31 +2033,19 @@ void exact_bnb(const HostModel& m, const cubics_search_config& cfg0, std::vector
         ph.seeds = &seeds;
         ph.first = 1;
         ph.static_bound = true;
+        ph.prefix_sum = true; // best solution + prefix stats summed on the device
         cubics_search_config cp = c;
         cp.has_initial_bound = 1;
         cp.initial_bound = objs.back();
         RunOut pr;
         run_search(m, cp, CUBICS_ENGINE_PARALLEL, true, 65536, pr, true, &ph);
         add(pr);
-        if (pr.ws.sol_count > pr.rec.count) throw StatusError{CUBICS_E_CAPACITY, "exact B&B solution bookkeeping"};
-        // K_i+1: the DFS-first solution of the phase; the stats up to it
-        int64_t bi = -1;
-        for (uint64_t i = 0; i < pr.rec.count; ++i)
-            if (bi < 0 || std::lexicographical_compare(pr.rec.keys.begin() + i * KW, pr.rec.keys.begin() + (i + 1) * KW,
-                                                       pr.rec.keys.begin() + bi * KW, pr.rec.keys.begin() + (bi + 1) * KW))
-                bi = (int64_t)i;
-        const int64_t own = bi >= 0 ? pr.rec.seg[bi] : -1;
-        for (uint64_t s = 0; s < ph.n_seg; ++s) {
-            if ((int64_t)s == own) continue;
-            if (bi >= 0 && !std::lexicographical_compare(ph.seg_key.begin() + s * KW, ph.seg_key.begin() + (s + 1) * KW,
-                                                         pr.rec.keys.begin() + bi * KW, pr.rec.keys.begin() + (bi + 1) * KW))
-                continue; // right of K_i+1
-            for (int i = 0; i < 3; ++i) tot[i] += ph.seg_st[s * 3 + i];
-        }
-        if (bi < 0) break; // no improving solution right of K_i: complete
-        for (int i = 0; i < 3; ++i) tot[i] += pr.rec.stats[bi * 3 + i];
-        keys.emplace_back(pr.rec.keys.begin() + bi * KW, pr.rec.keys.begin() + (bi + 1) * KW);
-        best.assign(pr.rec.vals.begin() + bi * n, pr.rec.vals.begin() + (bi + 1) * n);
+        // K_i+1 (the phase's DFS-first solution) and the reference's stats up to it, or the whole
+        // rest of the tree when the phase found none
+        for (int i = 0; i < 3; ++i) tot[i] += pr.ws.stats[i];
+        if (!pr.has_first) break; // no improving solution right of K_i: complete
+        keys.push_back(pr.first_key);
+        best.assign(pr.rec.vals.begin(), pr.rec.vals.begin() + n);
         const int64_t v = objective(best.data());
         if (!(minimizing ? v < objs.back() : v > objs.back()))
             throw StatusError{CUBICS_E_INVALID, "exact B&B: a phase returned a non-improving solution"};
