@@ -2018,6 +2018,7 @@ void exact_bnb(const HostModel& m, const cubics_search_config& cfg0, std::vector
         run_search(m, cr, CUBICS_ENGINE_PARITY, false, 0, rr, false, &rp);
         add(rr);
         const uint64_t nt = rp.n_tasks;
+        if (nt > rp.task_cap) throw StatusError{CUBICS_E_INVALID, "exact B&B: replay emitted more branches than its depth"};
         if (nt == 0) break; // nothing right of K_i: the search is complete
         std::vector<uint32_t> tkey(nt * KW);
         CU(cudaMemcpy2D(tkey.data(), sizeof(uint32_t) * KW, rp.task_dev + NWP, sizeof(uint32_t) * OS,
